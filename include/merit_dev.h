@@ -1,0 +1,253 @@
+/*
+ * merit_dev.h — C ABI of the B200 (sm_100a) MERIT device operator.
+ *
+ * This is the drop-in boundary for the reference's single execution entry
+ * point `merit::Tensor merit::run_full(const merit::Workload&)`
+ * (/root/reference/proj/include/merit/engine.hpp:282-287).  A reference
+ * caller describes the same Workload — two gather views (ViewSpec,
+ * view.hpp:24-49), two source tensors and a ranged-inner-product
+ * StrategyProgram (rip.hpp:85-107) — as plain C structs, asks the library to
+ * lower it to a device plan, and runs the plan on device or host buffers.
+ * No torch types, no C++ types cross this boundary.
+ *
+ * Lowering (merit_dev_plan_create) recognises the reduction skeletons the
+ * reference's templates emit (workloads.hpp:47-68, :376-385) and the affine
+ * view structure that goes with them, and picks one of four sm_100a kernels:
+ *   MERIT_KERNEL_MAXPOOL  window max on CUDA cores (K1)
+ *   MERIT_KERNEL_SAD      byte-SIMD block matching + fused argmin (K2)
+ *   MERIT_KERNEL_CONV_TC  implicit-GEMM convolution on tcgen05/TMEM (K3)
+ *   MERIT_KERNEL_GENERIC  exact device interpreter of any REAL32/FIX16 program
+ * There is no CPU execution path: a plan that cannot run on the device fails
+ * with a status code (mirroring merit::ErrorCode, tensor.hpp:15-29).
+ *
+ * Every entry point returns merit_status; on failure the thread-local message
+ * is available from merit_dev_last_error().  All functions are reentrant;
+ * plans are immutable after creation apart from the packed-operand cache
+ * filled by merit_dev_plan_pack_b (call it before sharing a plan).
+ */
+#ifndef MERIT_DEV_H_
+#define MERIT_DEV_H_
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MERIT_DEV_ABI_VERSION 1
+#define MERIT_MAX_RANK 8
+#define MERIT_MAX_TERMS 24
+#define MERIT_MAX_CONSTANTS 16
+#define MERIT_MAX_TABLES 4
+#define MERIT_MAX_TABLE_SAMPLES 1024
+#define MERIT_MAX_INSTRS 64
+
+/* Status codes.  1..13 mirror merit::ErrorCode in declaration order
+ * (tensor.hpp:15-29) offset by one so that 0 is success. */
+typedef enum merit_status {
+  MERIT_OK = 0,
+  MERIT_E_OUT_OF_RANGE = 1,        /* ErrorCode::OutOfRange (REJECT gather)     */
+  MERIT_E_BAD_MAGIC = 2,           /* ErrorCode::BadMagic                        */
+  MERIT_E_TRUNCATED_PAYLOAD = 3,   /* ErrorCode::TruncatedPayload                */
+  MERIT_E_UNKNOWN_DTYPE = 4,       /* ErrorCode::UnknownDtype                    */
+  MERIT_E_NEGATIVE_STRIDE = 5,     /* ErrorCode::NegativeStride                  */
+  MERIT_E_LUT_RANGE = 6,           /* ErrorCode::LutRange                        */
+  MERIT_E_DIV_BY_ZERO = 7,         /* ErrorCode::DivByZero                       */
+  MERIT_E_SCRATCHPAD_OVERFLOW = 8, /* ErrorCode::ScratchpadOverflow             */
+  MERIT_E_OUT_OF_FOOTPRINT = 9,    /* ErrorCode::OutOfFootprint                  */
+  MERIT_E_INDIVISIBLE = 10,        /* ErrorCode::Indivisible                     */
+  MERIT_E_UNKNOWN_TEMPLATE = 11,   /* ErrorCode::UnknownTemplate                 */
+  MERIT_E_BAD_PARAMS = 12,         /* ErrorCode::BadParams (Workload::validate)  */
+  MERIT_E_USAGE = 13,              /* ErrorCode::Usage                           */
+  MERIT_E_UNSUPPORTED_PROGRAM = 100, /* no device kernel for this program       */
+  MERIT_E_UNSUPPORTED_VIEW = 101,    /* no device kernel for this view shape    */
+  MERIT_E_CUDA = 102,                /* CUDA runtime / launch failure           */
+  MERIT_E_INVALID_ARGUMENT = 103     /* null pointer, bad enum, size mismatch   */
+} merit_status;
+
+/* view.hpp:11 */
+typedef enum merit_boundary {
+  MERIT_ZERO_PAD = 0,
+  MERIT_CLAMP = 1,
+  MERIT_REJECT = 2
+} merit_boundary;
+
+/* view.hpp:15-20: component j of the concatenated (p, a) index contributes
+ * k_j * stride + offset to source axis `axis`. */
+typedef struct merit_view_term {
+  int32_t component;
+  int32_t axis;
+  int64_t stride;
+  int64_t offset;
+} merit_view_term;
+
+/* view.hpp:24-49 */
+typedef struct merit_view_spec {
+  int32_t src_rank;
+  int32_t p_rank;
+  int32_t a_rank;
+  int32_t n_terms;
+  int64_t src_shape[MERIT_MAX_RANK];
+  int64_t p_shape[MERIT_MAX_RANK];
+  int64_t a_shape[MERIT_MAX_RANK];
+  merit_view_term terms[MERIT_MAX_TERMS];
+  int32_t boundary; /* merit_boundary */
+  int32_t _pad;
+} merit_view_spec;
+
+/* rip.hpp:15-31, same order. */
+typedef enum merit_op {
+  MERIT_OP_ADD = 0, MERIT_OP_SUB, MERIT_OP_L1, MERIT_OP_MAC, MERIT_OP_MAX,
+  MERIT_OP_MIN, MERIT_OP_SEL, MERIT_OP_BAND, MERIT_OP_BOR, MERIT_OP_BXOR,
+  MERIT_OP_BNOT, MERIT_OP_IDX, MERIT_OP_LUT, MERIT_OP_MOVC, MERIT_OP_DIV
+} merit_op;
+
+/* rip.hpp:33-41 Operand::Kind */
+typedef enum merit_operand_kind {
+  MERIT_OPND_REG = 0, MERIT_OPND_PORT_A = 1, MERIT_OPND_PORT_B = 2, MERIT_OPND_ZERO = 3
+} merit_operand_kind;
+
+/* rip.hpp:51-57 AluInstr (+ Operand, Dst) */
+typedef struct merit_alu_instr {
+  int32_t op;        /* merit_op */
+  int32_t dst_out;   /* Dst::out: 1 = emit to the output stream */
+  int32_t dst_reg;   /* Dst::reg */
+  int32_t a_kind, a_reg;
+  int32_t b_kind, b_reg;
+  int32_t c_kind, c_reg;
+  int32_t shift;
+  int32_t aux;
+} merit_alu_instr;
+
+/* rip.hpp:61-78 LookupTable */
+typedef struct merit_lookup_table {
+  double lo, hi;
+  int32_t n_samples;
+  int32_t clamp;
+  const double* samples;
+} merit_lookup_table;
+
+/* rip.hpp:85-107 StrategyProgram.  Segment s holds seg_len[s] instructions,
+ * stored back to back in `instrs` in segment order Pre_1..Pre_D, Body,
+ * Post_D..Post_1 (2*depth+1 segments). */
+typedef struct merit_program {
+  int32_t depth;
+  int32_t outputs;
+  int32_t n_segments;
+  int32_t n_constants;
+  int32_t n_tables;
+  int32_t _pad;
+  const int32_t* seg_len;
+  const merit_alu_instr* instrs;
+  const double* constants;
+  const merit_lookup_table* tables;
+} merit_program;
+
+/* Element types of the buffers crossing the ABI.  F32 and I16 are the
+ * reference's REAL32 / FIX16 (tensor.hpp:67); BF16 and U8 are device
+ * storage types for the same values (bf16-rounded activations, 8-bit frames);
+ * I32 is an exact integer SAD output. */
+typedef enum merit_dtype {
+  MERIT_F32 = 0, MERIT_I16 = 1, MERIT_BF16 = 2, MERIT_U8 = 3, MERIT_I32 = 4
+} merit_dtype;
+
+/* Request flags. */
+enum {
+  MERIT_FLAG_EXACT = 1u << 0,   /* force the bit-exact generic interpreter     */
+  MERIT_FLAG_ARGMIN = 1u << 1,  /* L1 block matching: also write (mv_y, mv_x,
+                                   min SAD) per block, lowest-raster tie-break */
+  MERIT_FLAG_NO_MAP = 1u << 2,  /* with ARGMIN: skip the full SAD map output   */
+  MERIT_FLAG_FAST_BF16 = 1u << 3 /* f32 MAC conv: one bf16 product instead of
+                                    the 3-term bf16 split (looser tolerance)  */
+};
+
+/* engine.hpp:16-39 Workload, as a descriptor.  Data pointers are supplied
+ * at run time. */
+typedef struct merit_workload_desc {
+  merit_view_spec view_a;
+  merit_view_spec view_b;
+  int32_t dtype_a;    /* merit_dtype of src_a buffers */
+  int32_t dtype_b;    /* merit_dtype of src_b buffers */
+  int32_t dtype_out;  /* merit_dtype of the output buffer */
+  int32_t frac_bits;  /* Tensor::frac_bits of FIX16 sources (tensor.hpp:78) */
+  uint32_t flags;
+  int32_t _pad;
+  merit_program program;
+} merit_workload_desc;
+
+typedef enum merit_kernel_kind {
+  MERIT_KERNEL_GENERIC = 0,
+  MERIT_KERNEL_MAXPOOL = 1,
+  MERIT_KERNEL_SAD = 2,
+  MERIT_KERNEL_CONV_TC = 3
+} merit_kernel_kind;
+
+/* What a plan needs and produces. */
+typedef struct merit_plan_info {
+  int32_t kernel;          /* merit_kernel_kind */
+  int32_t out_rank;        /* Workload::output_shape() rank */
+  int64_t out_shape[MERIT_MAX_RANK + 1];
+  int64_t out_elems;       /* 0 when MERIT_FLAG_NO_MAP */
+  int64_t out_bytes;
+  int64_t aux_elems;       /* int32 elements of the argmin record (3 per block) */
+  int64_t src_a_bytes;
+  int64_t src_b_bytes;
+  int64_t n_outputs;       /* ranged inner products computed = prod(p_shape) */
+  double algorithmic_ops;  /* MACs / abs-diffs / compares per run */
+  double algorithmic_bytes;/* compulsory HBM bytes per run */
+  int32_t launches_per_run;/* kernel launches issued by merit_dev_run */
+  int32_t _pad;
+  char description[256];
+} merit_plan_info;
+
+typedef struct merit_plan merit_plan;
+
+/* Library identification. */
+int32_t merit_dev_abi_version(void);
+const char* merit_dev_build_info(void);
+
+/* Thread-local message of the last failing call ("" if none). */
+const char* merit_dev_last_error(void);
+
+/* Validate (engine.hpp:30-38 Workload::validate, rip.hpp:96-106) and lower a
+ * workload to a device plan.  Host-only; needs no GPU. */
+merit_status merit_dev_plan_create(const merit_workload_desc* desc, merit_plan** out_plan);
+merit_status merit_dev_plan_destroy(merit_plan* plan);
+merit_status merit_dev_plan_query(const merit_plan* plan, merit_plan_info* info);
+
+/* Pack the B operand (e.g. convolution weights) into the kernel's operand
+ * layout on the device, once.  d_src_b is a device pointer.  Optional: run
+ * calls pack on the fly when no packed copy exists. */
+merit_status merit_dev_plan_pack_b(merit_plan* plan, const void* d_src_b, void* cuda_stream);
+
+/* Run on device buffers, asynchronously on `cuda_stream` (0 = default).
+ * d_out receives Workload::output_shape() elements of dtype_out (may be null
+ * with MERIT_FLAG_NO_MAP); d_aux receives the argmin records (may be null
+ * without MERIT_FLAG_ARGMIN). */
+merit_status merit_dev_run(const merit_plan* plan, const void* d_src_a, const void* d_src_b,
+                           void* d_out, void* d_aux, void* cuda_stream);
+
+/* Run on host buffers: H2D copies, run, D2H copies, synchronise — the
+ * reference's run_full calling convention (host tensors in, host tensor out). */
+merit_status merit_dev_run_host(const merit_plan* plan, const void* h_src_a, const void* h_src_b,
+                                void* h_out, void* h_aux, void* cuda_stream);
+
+/* Deterministic input synthesis shared by tests and the benchmark
+ * (workloads.hpp:74-105 SplitMix64 / fill_random, and the seeded frame
+ * generator of SURVEY §8(d)).  Host-only. */
+void merit_gen_uniform_f32(float* out, int64_t n, uint64_t seed, double lo, double hi);
+void merit_gen_normal_f32(float* out, int64_t n, uint64_t seed, double sigma);
+void merit_gen_range_i16(int16_t* out, int64_t n, uint64_t seed, int64_t lo, int64_t hi);
+void merit_gen_me_pair(uint8_t* cur, uint8_t* ref, int64_t h, int64_t w, int64_t blk,
+                       int64_t max_shift, int64_t noise, uint64_t seed);
+void merit_f32_to_bf16(const float* in, uint16_t* out, int64_t n);
+
+/* Counters of kernels launched through this library by the calling process
+ * (evidence for the benchmark's gpu_launches claim). */
+int64_t merit_dev_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MERIT_DEV_H_ */

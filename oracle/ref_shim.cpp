@@ -1,0 +1,228 @@
+// ref_shim.cpp — extern "C" wrappers around the UNMODIFIED reference
+// implementation, compiled from the read-only headers under
+// /root/reference/proj/include by oracle/build_ref.sh into
+// oracle/_ref/libmerit_ref.so.
+//
+// TEST / BASELINE INFRASTRUCTURE ONLY: used to pin the C restatement
+// (oracle.c) against the reference itself, to generate tests/golden/, and as
+// the CPU reference arm of bench.py.  No reference source is copied into the
+// repository; this file only includes the headers by path.
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+
+#include "merit/engine.hpp"
+#include "merit/workloads.hpp"
+#include "merit_dev.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+merit::ViewSpec to_view(const merit_view_spec& v) {
+  merit::ViewSpec s;
+  s.source_shape.assign(v.src_shape, v.src_shape + v.src_rank);
+  s.p_shape.assign(v.p_shape, v.p_shape + v.p_rank);
+  s.a_shape.assign(v.a_shape, v.a_shape + v.a_rank);
+  for (int t = 0; t < v.n_terms; ++t)
+    s.terms.push_back({v.terms[t].component, v.terms[t].axis, v.terms[t].stride, v.terms[t].offset});
+  s.boundary = static_cast<merit::Boundary>(v.boundary);
+  return s;
+}
+
+merit::Operand opnd(int kind, int reg) {
+  merit::Operand o;
+  o.kind = static_cast<merit::Operand::Kind>(kind);
+  o.reg = reg;
+  return o;
+}
+
+merit::StrategyProgram to_program(const merit_program& p) {
+  merit::StrategyProgram prog;
+  prog.depth = p.depth;
+  prog.outputs = p.outputs;
+  prog.segments.assign(p.n_segments, {});
+  int at = 0;
+  for (int s = 0; s < p.n_segments; ++s)
+    for (int q = 0; q < p.seg_len[s]; ++q, ++at) {
+      const merit_alu_instr& in = p.instrs[at];
+      merit::AluInstr ai;
+      ai.op = static_cast<merit::Op>(in.op);
+      ai.dst.out = in.dst_out != 0;
+      ai.dst.reg = in.dst_reg;
+      ai.a = opnd(in.a_kind, in.a_reg);
+      ai.b = opnd(in.b_kind, in.b_reg);
+      ai.c = opnd(in.c_kind, in.c_reg);
+      ai.shift = in.shift;
+      ai.aux = in.aux;
+      prog.segments[s].push_back(ai);
+    }
+  prog.constants.assign(p.constants, p.constants + p.n_constants);
+  for (int t = 0; t < p.n_tables; ++t) {
+    merit::LookupTable lt;
+    lt.lo = p.tables[t].lo;
+    lt.hi = p.tables[t].hi;
+    lt.clamp = p.tables[t].clamp != 0;
+    lt.samples.assign(p.tables[t].samples, p.tables[t].samples + p.tables[t].n_samples);
+    prog.tables.push_back(lt);
+  }
+  return prog;
+}
+
+// REAL32 tensors take f32 / u8 / bf16 storage (widened exactly); FIX16 takes i16.
+merit::Tensor to_tensor(const merit_view_spec& v, int dtype, int frac, const void* data) {
+  merit::Shape shape(v.src_shape, v.src_shape + v.src_rank);
+  if (dtype == MERIT_I16) {
+    merit::Tensor t = merit::Tensor::fix(shape, frac);
+    std::memcpy(t.qdata.data(), data, t.qdata.size() * 2);
+    return t;
+  }
+  merit::Tensor t = merit::Tensor::real(shape);
+  const size_t n = t.fdata.size();
+  for (size_t i = 0; i < n; ++i) {
+    switch (dtype) {
+      case MERIT_F32: t.fdata[i] = static_cast<const float*>(data)[i]; break;
+      case MERIT_U8: t.fdata[i] = static_cast<const uint8_t*>(data)[i]; break;
+      case MERIT_BF16: {
+        uint32_t u = static_cast<uint32_t>(static_cast<const uint16_t*>(data)[i]) << 16;
+        std::memcpy(&t.fdata[i], &u, 4);
+        break;
+      }
+      default: t.fdata[i] = 0.f;
+    }
+  }
+  return t;
+}
+
+int code_of(const merit::Error& e) { return static_cast<int>(e.code) + 1; }
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+
+// merit::run_full (engine.hpp:282-287).  Output: REAL32 -> float, FIX16 -> int16.
+int ref_run_full(const merit_workload_desc* d, const void* a, const void* b, void* out) {
+  try {
+    merit::Workload w;
+    w.view_a = to_view(d->view_a);
+    w.view_b = to_view(d->view_b);
+    w.src_a = to_tensor(d->view_a, d->dtype_a, d->frac_bits, a);
+    w.src_b = to_tensor(d->view_b, d->dtype_b, d->frac_bits, b);
+    w.program = to_program(d->program);
+    merit::Tensor t = merit::run_full(w);
+    if (t.dtype == merit::Dtype::Real32)
+      std::memcpy(out, t.fdata.data(), t.fdata.size() * 4);
+    else
+      std::memcpy(out, t.qdata.data(), t.qdata.size() * 2);
+    return 0;
+  } catch (const merit::Error& e) {
+    g_err = e.what();
+    return code_of(e);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return MERIT_E_BAD_PARAMS;
+  }
+}
+
+// merit::run_tiled (engine.hpp:289-295) with a tiling plan; also returns the
+// TrafficReport as 7 uint64 (engine.hpp:72-80).
+int ref_run_tiled(const merit_workload_desc* d, const void* a, const void* b, const int64_t* t_p,
+                  const int64_t* t_a, void* out, uint64_t* traffic) {
+  try {
+    merit::Workload w;
+    w.view_a = to_view(d->view_a);
+    w.view_b = to_view(d->view_b);
+    w.src_a = to_tensor(d->view_a, d->dtype_a, d->frac_bits, a);
+    w.src_b = to_tensor(d->view_b, d->dtype_b, d->frac_bits, b);
+    w.program = to_program(d->program);
+    merit::TilingPlan plan;
+    plan.t_p.assign(t_p, t_p + d->view_a.p_rank);
+    plan.t_a.assign(t_a, t_a + d->view_a.a_rank);
+    merit::EngineConfig cfg;
+    cfg.scratch_words_a = int64_t(1) << 40;
+    cfg.scratch_words_b = int64_t(1) << 40;
+    auto [t, rep] = merit::run_tiled(w, plan, cfg);
+    if (t.dtype == merit::Dtype::Real32)
+      std::memcpy(out, t.fdata.data(), t.fdata.size() * 4);
+    else
+      std::memcpy(out, t.qdata.data(), t.qdata.size() * 2);
+    const uint64_t r[7] = {rep.dram_read_words_a, rep.dram_read_words_b, rep.dram_write_words,
+                           rep.scratchpad_peak_words_a, rep.scratchpad_peak_words_b, rep.passes,
+                           rep.macs};
+    std::memcpy(traffic, r, sizeof(r));
+    return 0;
+  } catch (const merit::Error& e) {
+    g_err = e.what();
+    return code_of(e);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return MERIT_E_BAD_PARAMS;
+  }
+}
+
+// fill_random (workloads.hpp:96-105) on a REAL32 / FIX16 tensor of n elements.
+void ref_fill_random_f32(float* out, int64_t n, uint64_t seed, double lo, double hi) {
+  merit::Tensor t = merit::Tensor::real({n});
+  merit::fill_random(t, seed, lo, hi);
+  std::memcpy(out, t.fdata.data(), n * 4);
+}
+void ref_fill_random_i16(int16_t* out, int64_t n, uint64_t seed) {
+  merit::Tensor t = merit::Tensor::fix({n}, 8);
+  merit::fill_random(t, seed);
+  std::memcpy(out, t.qdata.data(), n * 2);
+}
+
+// Template builders + oracles by name (workloads.hpp:391-406, :675-693).
+// params: "k=v,k=v".  Writes the template's sources (filled like the
+// reference tests: fill_random(src_a, 2s+1), fill_random(src_b, 2s+2)) and
+// both the engine and the oracle outputs.  Returns element counts via sizes.
+static merit::Params parse_params(const char* s) {
+  merit::Params p;
+  std::string str(s ? s : "");
+  size_t pos = 0;
+  while (pos < str.size()) {
+    size_t comma = str.find(',', pos);
+    std::string kv = str.substr(pos, comma == std::string::npos ? std::string::npos : comma - pos);
+    size_t eq = kv.find('=');
+    if (eq != std::string::npos) p[kv.substr(0, eq)] = std::stod(kv.substr(eq + 1));
+    if (comma == std::string::npos) break;
+    pos = comma + 1;
+  }
+  return p;
+}
+
+int ref_template_case(const char* name, const char* params, uint64_t seed, void* src_a,
+                      int64_t* n_a, void* src_b, int64_t* n_b, void* engine_out, void* oracle_out,
+                      int64_t* n_out, int64_t cap) {
+  try {
+    merit::Params prm = parse_params(params);
+    merit::Workload w = merit::build_template(name, prm);
+    merit::fill_random(w.src_a, 2 * seed + 1);
+    merit::fill_random(w.src_b, 2 * seed + 2);
+    if (merit::template_shares_input(name)) w.src_b = w.src_a;
+    merit::Tensor got = merit::run_full(w);
+    merit::Tensor want = merit::oracle(name, prm, w.src_a, w.src_b);
+    const bool fix = w.src_a.dtype == merit::Dtype::Fix16;
+    const size_t es = fix ? 2 : 4;
+    *n_a = w.src_a.size();
+    *n_b = w.src_b.size();
+    *n_out = got.size();
+    if (*n_a > cap || *n_b > cap || *n_out > cap) return MERIT_E_INVALID_ARGUMENT;
+    std::memcpy(src_a, fix ? (const void*)w.src_a.qdata.data() : (const void*)w.src_a.fdata.data(), *n_a * es);
+    std::memcpy(src_b, fix ? (const void*)w.src_b.qdata.data() : (const void*)w.src_b.fdata.data(), *n_b * es);
+    std::memcpy(engine_out, fix ? (const void*)got.qdata.data() : (const void*)got.fdata.data(), *n_out * es);
+    std::memcpy(oracle_out, fix ? (const void*)want.qdata.data() : (const void*)want.fdata.data(), *n_out * es);
+    return 0;
+  } catch (const merit::Error& e) {
+    g_err = e.what();
+    return code_of(e);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return MERIT_E_BAD_PARAMS;
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,16 @@
+"""B200-native MERIT transform operator (arXiv 1911.03458 hot path).
+
+The product is the C-ABI library ``libmerit_dev.so`` (include/merit_dev.h)
+with four sm_100a kernels; this package is its Python mirror of the
+reference's operator API (``merit.py``) plus the workload templates and the
+BASELINE configurations (``workloads.py``).
+"""
+from .merit import (AluInstr, Boundary, Dst, Dtype, Error, ErrorCode, Kernel, LookupTable, Op,
+                    Operand, Plan, StrategyProgram, ViewSpec, ViewTerm, Workload, run_full,
+                    run_full_argmin, FLAG_ARGMIN, FLAG_EXACT, FLAG_FAST_BF16, FLAG_NO_MAP)
+from . import workloads
+
+__all__ = ["AluInstr", "Boundary", "Dst", "Dtype", "Error", "ErrorCode", "Kernel", "LookupTable",
+           "Op", "Operand", "Plan", "StrategyProgram", "ViewSpec", "ViewTerm", "Workload",
+           "run_full", "run_full_argmin", "workloads", "FLAG_ARGMIN", "FLAG_EXACT",
+           "FLAG_FAST_BF16", "FLAG_NO_MAP"]

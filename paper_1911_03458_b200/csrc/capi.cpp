@@ -1,0 +1,329 @@
+// C ABI entry points (include/merit_dev.h).  Host-side plumbing only: plan
+// lifetime, lazy device state, host<->device copies for merit_dev_run_host,
+// and deterministic input synthesis.  All compute is in the .cu kernels.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "plan.hpp"
+
+namespace merit_dev {
+
+namespace {
+thread_local std::string g_last_error;
+std::atomic<int64_t> g_launches{0};
+}  // namespace
+
+merit_status fail(merit_status st, const std::string& msg) {
+  g_last_error = msg;
+  return st;
+}
+
+merit_status cuda_check(int err, const char* what) {
+  if (err == cudaSuccess) return MERIT_OK;
+  return fail(MERIT_E_CUDA, std::string(what) + ": " +
+                                cudaGetErrorString(static_cast<cudaError_t>(err)));
+}
+
+void count_launch(int n) { g_launches += n; }
+
+}  // namespace merit_dev
+
+using namespace merit_dev;
+
+namespace {
+
+// Device-side state a plan needs lazily (program image, error flag).
+merit_status ensure_device_state(const merit_plan& plan) {
+  std::lock_guard<std::mutex> lk(plan.mu);
+  int dev = 0;
+  merit_status st = cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  if (st != MERIT_OK) return st;
+  if (plan.device >= 0 && plan.device != dev)
+    return fail(MERIT_E_INVALID_ARGUMENT, "plan was first used on another device");
+  plan.device = dev;
+  if (!plan.d_err) {
+    if ((st = cuda_check(cudaMalloc(&plan.d_err, 16), "cudaMalloc(err)")) != MERIT_OK) return st;
+    if ((st = cuda_check(cudaMemset(plan.d_err, 0, 16), "cudaMemset(err)")) != MERIT_OK) return st;
+  }
+  if (plan.kernel == MERIT_KERNEL_GENERIC && !plan.d_prog) {
+    if ((st = cuda_check(cudaMalloc(&plan.d_prog, sizeof(ProgramImage)), "cudaMalloc(prog)")) !=
+        MERIT_OK)
+      return st;
+    if ((st = cuda_check(cudaMemcpy(plan.d_prog, &plan.prog, sizeof(ProgramImage),
+                                    cudaMemcpyHostToDevice),
+                         "cudaMemcpy(prog)")) != MERIT_OK)
+      return st;
+  }
+  if (plan.kernel == MERIT_KERNEL_CONV_TC && !plan.d_packed_b) {
+    if ((st = cuda_check(cudaMalloc(&plan.d_packed_b, plan.conv.packed_b_bytes),
+                         "cudaMalloc(packed_b)")) != MERIT_OK)
+      return st;
+  }
+  return MERIT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t merit_dev_abi_version(void) { return MERIT_DEV_ABI_VERSION; }
+
+const char* merit_dev_build_info(void) {
+  return "merit_dev: sm_100a kernels {generic, maxpool, sad(vabsdiff4), conv_tc(tcgen05)}";
+}
+
+const char* merit_dev_last_error(void) { return g_last_error.c_str(); }
+
+int64_t merit_dev_launch_count(void) { return g_launches.load(); }
+
+merit_status merit_dev_plan_create(const merit_workload_desc* desc, merit_plan** out_plan) {
+  if (!desc || !out_plan) return fail(MERIT_E_INVALID_ARGUMENT, "null argument");
+  *out_plan = nullptr;
+  merit_plan* plan = new (std::nothrow) merit_plan();
+  if (!plan) return fail(MERIT_E_INVALID_ARGUMENT, "out of host memory");
+  plan->desc = *desc;
+  // The program's arrays are copied into plan->prog by lower(); the copied
+  // descriptor must not keep dangling caller pointers.
+  merit_status st = lower(*desc, *plan);
+  plan->desc.program.seg_len = nullptr;
+  plan->desc.program.instrs = nullptr;
+  plan->desc.program.constants = nullptr;
+  plan->desc.program.tables = nullptr;
+  if (st != MERIT_OK) {
+    delete plan;
+    return st;
+  }
+  g_last_error.clear();
+  *out_plan = plan;
+  return MERIT_OK;
+}
+
+merit_status merit_dev_plan_destroy(merit_plan* plan) {
+  if (!plan) return MERIT_OK;
+  if (plan->device >= 0) {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(plan->device);
+    if (plan->d_prog) cudaFree(plan->d_prog);
+    if (plan->d_err) cudaFree(plan->d_err);
+    if (plan->d_packed_b) cudaFree(plan->d_packed_b);
+    cudaSetDevice(cur);
+  }
+  delete plan;
+  return MERIT_OK;
+}
+
+merit_status merit_dev_plan_query(const merit_plan* plan, merit_plan_info* info) {
+  if (!plan || !info) return fail(MERIT_E_INVALID_ARGUMENT, "null argument");
+  *info = plan->info;
+  return MERIT_OK;
+}
+
+merit_status merit_dev_plan_pack_b(merit_plan* plan, const void* d_src_b, void* stream) {
+  if (!plan) return fail(MERIT_E_INVALID_ARGUMENT, "null plan");
+  if (plan->kernel != MERIT_KERNEL_CONV_TC) return MERIT_OK;  // nothing to pack
+  if (!d_src_b) return fail(MERIT_E_INVALID_ARGUMENT, "null weights");
+  merit_status st = ensure_device_state(*plan);
+  if (st != MERIT_OK) return st;
+  st = launch_conv_pack(*plan, d_src_b, plan->d_packed_b, stream);
+  if (st == MERIT_OK) plan->packed_valid = true;
+  return st;
+}
+
+static merit_status check_error_flag(const merit_plan& plan, cudaStream_t s) {
+  int32_t err[2] = {0, 0};
+  merit_status st = cuda_check(
+      cudaMemcpyAsync(err, plan.d_err, sizeof(err), cudaMemcpyDeviceToHost, s), "read error flag");
+  if (st != MERIT_OK) return st;
+  if ((st = cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize")) != MERIT_OK) return st;
+  if (err[0] != 0) {
+    cudaMemsetAsync(plan.d_err, 0, 16, s);
+    cudaStreamSynchronize(s);
+    const char* what = "device execution error";
+    switch (err[0]) {
+      case MERIT_E_OUT_OF_RANGE: what = "gather outside source tensor"; break;
+      case MERIT_E_DIV_BY_ZERO: what = "DIV by zero"; break;
+      case MERIT_E_LUT_RANGE: what = "lookup outside table range"; break;
+      case MERIT_E_BAD_PARAMS: what = "program emitted wrong output count or bad aux index"; break;
+      default: break;
+    }
+    return fail(static_cast<merit_status>(err[0]), what);
+  }
+  return MERIT_OK;
+}
+
+merit_status merit_dev_run(const merit_plan* plan, const void* d_a, const void* d_b, void* d_out,
+                           void* d_aux, void* stream) {
+  if (!plan) return fail(MERIT_E_INVALID_ARGUMENT, "null plan");
+  const merit_plan_info& info = plan->info;
+  if (info.out_elems > 0 && !d_out) return fail(MERIT_E_INVALID_ARGUMENT, "null output");
+  if (info.aux_elems > 0 && !d_aux) return fail(MERIT_E_INVALID_ARGUMENT, "null aux output");
+  merit_status st = ensure_device_state(*plan);
+  if (st != MERIT_OK) return st;
+  switch (plan->kernel) {
+    case MERIT_KERNEL_GENERIC:
+      if (!d_a || !d_b) return fail(MERIT_E_INVALID_ARGUMENT, "null source");
+      st = launch_generic(*plan, d_a, d_b, d_out, stream);
+      if (st == MERIT_OK) st = check_error_flag(*plan, static_cast<cudaStream_t>(stream));
+      return st;
+    case MERIT_KERNEL_MAXPOOL:
+      if (!d_a) return fail(MERIT_E_INVALID_ARGUMENT, "null source");
+      return launch_maxpool(*plan, d_a, d_out, stream);
+    case MERIT_KERNEL_SAD:
+      if (!d_a || !d_b) return fail(MERIT_E_INVALID_ARGUMENT, "null source");
+      return launch_sad(*plan, d_a, d_b, d_out, d_aux, stream);
+    case MERIT_KERNEL_CONV_TC: {
+      const void* in = plan->conv_swapped ? d_b : d_a;
+      const void* w = plan->conv_swapped ? d_a : d_b;
+      if (!in) return fail(MERIT_E_INVALID_ARGUMENT, "null source");
+      if (!plan->packed_valid) {
+        if (!w) return fail(MERIT_E_INVALID_ARGUMENT, "null weights and no packed copy");
+        st = launch_conv_pack(*plan, w, plan->d_packed_b, stream);
+        if (st != MERIT_OK) return st;
+      }
+      return launch_conv(*plan, in, plan->d_packed_b, d_out, stream);
+    }
+    default:
+      return fail(MERIT_E_INVALID_ARGUMENT, "corrupt plan");
+  }
+}
+
+merit_status merit_dev_run_host(const merit_plan* plan, const void* h_a, const void* h_b,
+                                void* h_out, void* h_aux, void* stream) {
+  if (!plan) return fail(MERIT_E_INVALID_ARGUMENT, "null plan");
+  const merit_plan_info& info = plan->info;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  void *da = nullptr, *db = nullptr, *dout = nullptr, *daux = nullptr;
+  merit_status st = MERIT_OK;
+  // Port B is copied whenever the caller provides it (for a packed
+  // convolution plan the run ignores it).
+  const bool need_b = h_b != nullptr && info.src_b_bytes > 0;
+  auto cleanup = [&]() {
+    if (da) cudaFreeAsync(da, s);
+    if (db) cudaFreeAsync(db, s);
+    if (dout) cudaFreeAsync(dout, s);
+    if (daux) cudaFreeAsync(daux, s);
+    cudaStreamSynchronize(s);
+  };
+#define MERIT_TRY(expr, what)                                  \
+  do {                                                         \
+    st = cuda_check((expr), what);                             \
+    if (st != MERIT_OK) { cleanup(); return st; }              \
+  } while (0)
+  MERIT_TRY(cudaMallocAsync(&da, info.src_a_bytes, s), "cudaMallocAsync(a)");
+  MERIT_TRY(cudaMemcpyAsync(da, h_a, info.src_a_bytes, cudaMemcpyHostToDevice, s), "H2D a");
+  if (need_b) {
+    MERIT_TRY(cudaMallocAsync(&db, info.src_b_bytes, s), "cudaMallocAsync(b)");
+    MERIT_TRY(cudaMemcpyAsync(db, h_b, info.src_b_bytes, cudaMemcpyHostToDevice, s), "H2D b");
+  }
+  if (info.out_bytes > 0) MERIT_TRY(cudaMallocAsync(&dout, info.out_bytes, s), "cudaMallocAsync(out)");
+  if (info.aux_elems > 0)
+    MERIT_TRY(cudaMallocAsync(&daux, info.aux_elems * 4, s), "cudaMallocAsync(aux)");
+  st = merit_dev_run(plan, da, db, dout, daux, stream);
+  if (st != MERIT_OK) {
+    std::string msg = g_last_error;
+    cleanup();
+    return fail(st, msg);
+  }
+  if (info.out_bytes > 0)
+    MERIT_TRY(cudaMemcpyAsync(h_out, dout, info.out_bytes, cudaMemcpyDeviceToHost, s), "D2H out");
+  if (info.aux_elems > 0)
+    MERIT_TRY(cudaMemcpyAsync(h_aux, daux, info.aux_elems * 4, cudaMemcpyDeviceToHost, s),
+              "D2H aux");
+  MERIT_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+#undef MERIT_TRY
+  cleanup();
+  return MERIT_OK;
+}
+
+// ------------------------------------------------------------ generators --
+// SplitMix64 exactly as workloads.hpp:74-94.
+namespace {
+struct SplitMix64 {
+  uint64_t state;
+  explicit SplitMix64(uint64_t s) : state(s) {}
+  uint64_t next() {
+    uint64_t z = (state += 0x9e3779b97f4a7c15ull);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+  }
+  double uniform(double lo, double hi) {
+    return lo + (hi - lo) * (static_cast<double>(next() >> 11) * 0x1.0p-53);
+  }
+  int64_t range(int64_t lo, int64_t hi) {
+    return lo + static_cast<int64_t>(next() % static_cast<uint64_t>(hi - lo + 1));
+  }
+};
+}  // namespace
+
+void merit_gen_uniform_f32(float* out, int64_t n, uint64_t seed, double lo, double hi) {
+  SplitMix64 rng(seed);  // fill_random, workloads.hpp:96-105
+  for (int64_t i = 0; i < n; ++i) out[i] = static_cast<float>(rng.uniform(lo, hi));
+}
+
+void merit_gen_range_i16(int16_t* out, int64_t n, uint64_t seed, int64_t lo, int64_t hi) {
+  SplitMix64 rng(seed);
+  for (int64_t i = 0; i < n; ++i) out[i] = static_cast<int16_t>(rng.range(lo, hi));
+}
+
+void merit_gen_normal_f32(float* out, int64_t n, uint64_t seed, double sigma) {
+  // Box-Muller over SplitMix64 uniforms (SURVEY §8(d) C3/C4 weights).
+  SplitMix64 rng(seed);
+  const double two_pi = 6.283185307179586476925286766559;
+  for (int64_t i = 0; i < n; i += 2) {
+    double u1 = rng.uniform(0.0, 1.0), u2 = rng.uniform(0.0, 1.0);
+    if (u1 < 1e-300) u1 = 1e-300;
+    double r = std::sqrt(-2.0 * std::log(u1));
+    out[i] = static_cast<float>(sigma * r * std::cos(two_pi * u2));
+    if (i + 1 < n) out[i + 1] = static_cast<float>(sigma * r * std::sin(two_pi * u2));
+  }
+}
+
+void merit_gen_me_pair(uint8_t* cur, uint8_t* ref, int64_t h, int64_t w, int64_t blk,
+                       int64_t max_shift, int64_t noise, uint64_t seed) {
+  // ref = box5x5(uniform bytes); cur = per-block shifted ref + noise.
+  SplitMix64 rng(seed);
+  uint8_t* raw = new uint8_t[h * w];
+  for (int64_t i = 0; i < h * w; ++i) raw[i] = static_cast<uint8_t>(rng.range(0, 255));
+  auto cl = [](int64_t v, int64_t lo, int64_t hi) { return v < lo ? lo : v > hi ? hi : v; };
+  for (int64_t y = 0; y < h; ++y)
+    for (int64_t x = 0; x < w; ++x) {
+      int64_t s = 0;
+      for (int64_t dy = -2; dy <= 2; ++dy)
+        for (int64_t dx = -2; dx <= 2; ++dx) s += raw[cl(y + dy, 0, h - 1) * w + cl(x + dx, 0, w - 1)];
+      ref[y * w + x] = static_cast<uint8_t>((s + 12) / 25);  // round half up
+    }
+  delete[] raw;
+  const int64_t by = (h + blk - 1) / blk, bx = (w + blk - 1) / blk;
+  for (int64_t b = 0; b < by * bx; ++b) {
+    const int64_t y0 = (b / bx) * blk, x0 = (b % bx) * blk;
+    const int64_t sx = rng.range(-max_shift, max_shift), sy = rng.range(-max_shift, max_shift);
+    for (int64_t i = 0; i < blk && y0 + i < h; ++i)
+      for (int64_t j = 0; j < blk && x0 + j < w; ++j) {
+        const int64_t y = y0 + i, x = x0 + j;
+        int64_t v = ref[cl(y + sy, 0, h - 1) * w + cl(x + sx, 0, w - 1)] + rng.range(-noise, noise);
+        cur[y * w + x] = static_cast<uint8_t>(cl(v, 0, 255));
+      }
+  }
+}
+
+void merit_f32_to_bf16(const float* in, uint16_t* out, int64_t n) {
+  for (int64_t i = 0; i < n; ++i) {
+    uint32_t u;
+    std::memcpy(&u, &in[i], 4);
+    if ((u & 0x7fffffffu) > 0x7f800000u) {  // NaN stays NaN
+      out[i] = static_cast<uint16_t>((u >> 16) | 0x40);
+      continue;
+    }
+    u += 0x7fffu + ((u >> 16) & 1u);  // round to nearest even
+    out[i] = static_cast<uint16_t>(u >> 16);
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,154 @@
+// Internal plan representation shared by the lowering (lower.cpp), the C ABI
+// (capi.cpp) and the kernel launchers (*.cu).  Not part of the public ABI.
+#pragma once
+
+#include <cstdint>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "merit_dev.h"
+
+namespace merit_dev {
+
+constexpr int kMaxRank = MERIT_MAX_RANK;
+constexpr int kMaxK = 2 * MERIT_MAX_RANK;  // concatenated (p, a) rank
+
+// Affine form of one ViewSpec (view.hpp:37-42, Eq. 5): for source axis i,
+// x_i = sum_j coef[i][j] * k_j + off[i].
+struct ViewAffine {
+  int src_rank = 0;
+  int k_rank = 0;
+  int boundary = MERIT_ZERO_PAD;
+  int64_t src_shape[kMaxRank] = {};
+  int64_t coef[kMaxRank][kMaxK] = {};
+  int64_t off[kMaxRank] = {};
+};
+
+// Flattened StrategyProgram for the generic device interpreter.
+struct ProgramImage {
+  int32_t depth = 0;
+  int32_t outputs = 1;
+  int32_t n_segments = 0;
+  int32_t n_instrs = 0;
+  int32_t seg_start[2 * kMaxRank + 2] = {};
+  int32_t seg_len[2 * kMaxRank + 2] = {};
+  merit_alu_instr instrs[MERIT_MAX_INSTRS] = {};
+  double constants[MERIT_MAX_CONSTANTS] = {};
+  int32_t n_constants = 0;
+  int32_t n_tables = 0;
+  double tab_lo[MERIT_MAX_TABLES] = {};
+  double tab_hi[MERIT_MAX_TABLES] = {};
+  int32_t tab_n[MERIT_MAX_TABLES] = {};
+  int32_t tab_clamp[MERIT_MAX_TABLES] = {};
+  int32_t tab_off[MERIT_MAX_TABLES] = {};
+  int32_t n_table_samples = 0;
+  double table_samples[MERIT_MAX_TABLES * MERIT_MAX_TABLE_SAMPLES] = {};
+};
+
+// K0: exact interpreter (engine.hpp:120-143 with rip.hpp:210-267 semantics).
+struct GenericParams {
+  int32_t fix16 = 0;   // Fix16Mode (rip.hpp:144-158) instead of Real32Mode
+  int32_t p_rank = 0, a_rank = 0;
+  int64_t p_shape[kMaxRank] = {};
+  int64_t a_shape[kMaxRank] = {};
+  int64_t rows = 0;    // prod(p_shape)
+  int64_t a_vol = 0;
+  int32_t dtype_a = MERIT_F32, dtype_b = MERIT_F32, dtype_out = MERIT_F32;
+  int32_t uses_a = 1, uses_b = 1;
+  ViewAffine va, vb;
+};
+
+// Epilogue of the MAC / MAX skeletons (Post_1 of the program).
+enum PostOp : int32_t { POST_ADD_ZERO = 0, POST_RELU = 1 };
+
+// K1: window max (maxpool program, workloads.hpp:376-385).
+struct MaxpoolParams {
+  int64_t planes = 0;  // product of the leading (batch, channel) extents
+  int32_t H = 0, W = 0, Ho = 0, Wo = 0, KH = 0, KW = 0;
+  int32_t sy = 1, sx = 1, dy = 1, dx = 1, oy = 0, ox = 0;
+  int32_t boundary = MERIT_CLAMP;  // CLAMP (coordinate clamp) or ZERO_PAD (value 0)
+  int32_t post = POST_ADD_ZERO;
+  float init = -3.0e38f;           // MOVC constant of Pre_1
+  int32_t fast = 0;                // 3x3 / stride 2 / offset -1 warp-row path
+};
+
+// K2: L1 block matching (motion estimation, workloads.hpp:255-279).
+struct SadParams {
+  int64_t pairs = 1;
+  int32_t Hc = 0, Wc = 0;   // current-frame extents
+  int32_t Hr = 0, Wr = 0;   // reference-frame extents
+  int32_t BY = 0, BX = 0;   // block grid
+  int32_t BH = 16, BW = 16; // block extents (a_shape)
+  int32_t WY = 0, WX = 0;   // displacement window (p extents)
+  int32_t oy = 0, ox = 0;   // reference offset at displacement 0
+  int32_t cy = 0, cx = 0;   // current-frame offset of block (0,0)
+  int32_t boundary = MERIT_ZERO_PAD;  // reference-frame boundary
+  int32_t ref_is_b = 1;     // port B carries the displaced reference view
+  int32_t write_map = 1;
+  int32_t argmin = 0;
+  int32_t out_f32 = 0;      // SAD map as float (REAL32) instead of int32
+};
+
+// K3: implicit-GEMM convolution on tcgen05 (mac_program over conv views).
+struct ConvParams {
+  int32_t N = 1, Cin = 0, H = 0, W = 0;
+  int32_t Cout = 0, Ho = 0, Wo = 0, KH = 0, KW = 0;
+  int32_t sy = 1, sx = 1, dy = 1, dx = 1, oy = 0, ox = 0;
+  int32_t in_bf16 = 0;      // activations stored as bf16 (else f32)
+  int32_t w_bf16 = 0;       // weights stored as bf16 (else f32)
+  int32_t split = 3;        // bf16 terms per product: 1 (bf16) or 3 (f32 via hi/lo)
+  int32_t post = POST_ADD_ZERO;
+  int32_t BN = 0;           // N tile (multiple of 16, <= 256)
+  int32_t n_tiles_n = 0;
+  int32_t CB = 0;           // 64-channel blocks
+  int32_t n_kb = 0;         // k-blocks per tile = KH*KW*CB
+  int64_t npix = 0;         // N*Ho*Wo
+  int64_t packed_b_bytes = 0;
+};
+
+}  // namespace merit_dev
+
+struct merit_plan {
+  int32_t kernel = MERIT_KERNEL_GENERIC;
+  merit_workload_desc desc{};
+  merit_plan_info info{};
+  merit_dev::ProgramImage prog{};
+  merit_dev::GenericParams gen{};
+  merit_dev::MaxpoolParams mp{};
+  merit_dev::SadParams sad{};
+  merit_dev::ConvParams conv{};
+  bool conv_swapped = false;  // input tensor is src_b, weights are src_a
+  // Lazily created device state (plan creation itself needs no GPU).
+  mutable std::mutex mu;
+  mutable void* d_prog = nullptr;      // ProgramImage copy for K0
+  mutable void* d_err = nullptr;       // int32 device error flag
+  mutable void* d_packed_b = nullptr;  // K3 packed weights
+  mutable bool packed_valid = false;
+  mutable int device = -1;
+};
+
+namespace merit_dev {
+
+// Set the thread-local error message and return the status.
+merit_status fail(merit_status st, const std::string& msg);
+
+merit_status lower(const merit_workload_desc& d, merit_plan& plan);
+
+// Kernel launchers (defined in the .cu files).  All asynchronous on `stream`.
+merit_status launch_generic(const merit_plan& plan, const void* a, const void* b, void* out,
+                            void* stream);
+merit_status launch_maxpool(const merit_plan& plan, const void* a, void* out, void* stream);
+merit_status launch_sad(const merit_plan& plan, const void* a, const void* b, void* out,
+                        void* aux, void* stream);
+merit_status launch_conv_pack(const merit_plan& plan, const void* b, void* packed, void* stream);
+merit_status launch_conv(const merit_plan& plan, const void* a, const void* packed_b, void* out,
+                         void* stream);
+
+// Check a CUDA status from C++ host code; returns MERIT_E_CUDA with context.
+merit_status cuda_check(int err, const char* what);
+void count_launch(int n = 1);
+
+int64_t elem_size(int dtype);
+
+}  // namespace merit_dev

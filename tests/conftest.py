@@ -1,0 +1,28 @@
+import os
+import sys
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+if str(ROOT) not in sys.path:
+    sys.path.insert(0, str(ROOT))
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a)")
+    config.addinivalue_line("markers", "slow: long-running parity case at config scale")
+
+
+@pytest.fixture(scope="session")
+def devlib():
+    from paper_1911_03458_b200 import _capi
+    return _capi.load()
+
+
+@pytest.fixture(scope="session")
+def cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for @pytest.mark.gpu tests (no CPU fallback exists)")
+    return torch.device("cuda:0")
