@@ -1,0 +1,64 @@
+"""Multi-GPU sharding of a workload along its leading batch / frame-pair axis.
+
+The MERIT outputs of different images (conv, max-pool) or frame pairs (motion
+estimation) are independent ranged inner products, so a workload with a
+leading p-axis that maps 1:1 onto a leading source axis of every view that
+uses it shards with no exchange at all: rank r gets a
+contiguous slice of that axis, runs the unchanged device plan on it, and the
+output slices concatenate.  Views that do not use the batch component
+(weights) are replicated.  No collective is on the data path.
+"""
+from __future__ import annotations
+
+import copy
+from typing import Tuple
+
+import numpy as np
+
+from .merit import Error, ErrorCode, Workload
+
+
+def shard_range(total: int, world: int, rank: int) -> Tuple[int, int]:
+    """Contiguous balanced split: [start, stop) of `total` items for `rank`."""
+    if world < 1 or not 0 <= rank < world:
+        raise Error(ErrorCode.InvalidArgument, "bad rank/world")
+    base, rem = divmod(total, world)
+    start = rank * base + min(rank, rem)
+    return start, start + base + (1 if rank < rem else 0)
+
+
+def _batch_axis_of(view, comp: int):
+    """Source axis fed only by component `comp` with stride 1, or None if the
+    view does not use `comp`."""
+    axes = [t.axis for t in view.terms if t.component == comp]
+    if not axes:
+        return None
+    ax = axes[0]
+    ts = [t for t in view.terms if t.axis == ax]
+    if len(axes) != 1 or len(ts) != 1 or ts[0].stride != 1 or ts[0].offset != 0:
+        raise Error(ErrorCode.BadParams, "leading p-axis is not a plain batch axis")
+    return ax
+
+
+def shard_workload(w: Workload, world: int, rank: int) -> Tuple[Workload, Tuple[int, int]]:
+    """Slice p-axis 0 of `w` for `rank`; returns (shard, (start, stop))."""
+    total = w.view_a.p_shape[0]
+    start, stop = shard_range(total, world, rank)
+    s = copy.copy(w)
+    s.view_a = copy.deepcopy(w.view_a)
+    s.view_b = copy.deepcopy(w.view_b)
+    for attr_v, attr_s in (("view_a", "src_a"), ("view_b", "src_b")):
+        v = getattr(s, attr_v)
+        v.p_shape[0] = stop - start
+        ax = _batch_axis_of(v, 0)
+        src = getattr(w, attr_s)
+        if ax is None:
+            continue  # replicated operand (e.g. weights)
+        if ax != 0:
+            raise Error(ErrorCode.BadParams, "batch axis must be the leading source axis")
+        if v.source_shape[0] != total:
+            raise Error(ErrorCode.BadParams, "batch extent differs between p and source")
+        v.source_shape[0] = stop - start
+        if src is not None:
+            setattr(s, attr_s, np.ascontiguousarray(src[start:stop]))
+    return s, (start, stop)

@@ -1,0 +1,172 @@
+"""CPU tests of the C ABI boundary: the library loads, exports every symbol
+include/merit_dev.h declares, its struct layouts match the Python mirror,
+and plan creation (lowering) behaves like Workload::validate — no GPU needed."""
+import ctypes as C
+import re
+import subprocess
+import tempfile
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_1911_03458_b200 import (FLAG_ARGMIN, FLAG_EXACT, FLAG_NO_MAP, Error, ErrorCode, Kernel,
+                                   Plan, ViewTerm, _capi)
+from paper_1911_03458_b200 import workloads as W
+
+ROOT = Path(__file__).resolve().parent.parent
+HEADER = ROOT / "include" / "merit_dev.h"
+
+
+def declared_functions():
+    text = HEADER.read_text()
+    return sorted(set(re.findall(r"^\s*(?:[a-z_0-9]+\s*\*?\s+)+\*?(merit_[a-z_0-9]+)\s*\(", text, re.M)))
+
+
+def test_library_exports_every_declared_symbol(devlib):
+    names = declared_functions()
+    assert len(names) >= 15
+    for n in names:
+        assert hasattr(devlib, n), f"{n} declared in merit_dev.h but not exported"
+        assert n in _capi.PROTOTYPES, f"{n} missing from the ctypes prototypes"
+
+
+def test_abi_version_and_build_info(devlib):
+    assert devlib.merit_dev_abi_version() == 1
+    assert b"sm_100a" in devlib.merit_dev_build_info()
+
+
+def test_struct_layouts_match_c():
+    prog = r'''
+#include <stdio.h>
+#include <stddef.h>
+#include "merit_dev.h"
+int main(void){
+ printf("%zu %zu %zu %zu %zu %zu %zu %zu\n", sizeof(merit_view_term), sizeof(merit_view_spec),
+  sizeof(merit_alu_instr), sizeof(merit_lookup_table), sizeof(merit_program),
+  sizeof(merit_workload_desc), sizeof(merit_plan_info), offsetof(merit_workload_desc, program));
+ return 0;}
+'''
+    with tempfile.TemporaryDirectory() as d:
+        src = Path(d) / "s.c"
+        src.write_text(prog)
+        exe = Path(d) / "s"
+        subprocess.run(["gcc", f"-I{ROOT / 'include'}", str(src), "-o", str(exe)], check=True)
+        got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()]
+    want = [C.sizeof(_capi.ViewTermC), C.sizeof(_capi.ViewSpecC), C.sizeof(_capi.AluInstrC),
+            C.sizeof(_capi.LookupTableC), C.sizeof(_capi.ProgramC), C.sizeof(_capi.WorkloadDescC),
+            C.sizeof(_capi.PlanInfoC), _capi.WorkloadDescC.program.offset]
+    assert got == want
+
+
+@pytest.mark.parametrize("cfg,kernel,flags", [
+    ("C1", Kernel.MAXPOOL, 0), ("C2", Kernel.SAD, FLAG_ARGMIN), ("C3", Kernel.CONV_TC, 0),
+    ("C4", Kernel.CONV_TC, 0)])
+def test_configs_lower_to_specialised_kernels(cfg, kernel, flags):
+    p = Plan(W.config_workload(cfg, with_inputs=False), flags)
+    assert p.kernel == kernel
+    assert p.info.launches_per_run == 1
+
+
+def test_config_plan_accounting():
+    # SURVEY §8(d) per-unit figures
+    p = Plan(W.config_workload("C1", with_inputs=False))
+    assert p.info.n_outputs == 1605632 and p.info.algorithmic_bytes == 32112640
+    p = Plan(W.config_workload("C2", with_inputs=False), FLAG_ARGMIN)
+    assert p.info.n_outputs == 8755560 and p.info.algorithmic_ops == 2241423360
+    assert p.out_shape == (67, 120, 33, 33) and p.info.aux_elems == 8040 * 3
+    p = Plan(W.config_workload("C3", with_inputs=False))
+    assert 2 * p.info.algorithmic_ops == 7398752256
+    p = Plan(W.config_workload("C4", with_inputs=False))
+    assert 2 * p.info.algorithmic_ops == 118380036096 and p.info.algorithmic_bytes == 411631616
+    p = Plan(W.config_workload("C5", with_inputs=False, pairs=64), FLAG_ARGMIN | FLAG_NO_MAP)
+    assert p.info.out_elems == 0 and p.info.n_outputs * 256 == 64 * 35043840000
+
+
+def test_templates_lower():
+    kinds = {t: Plan(W.build_template(t, {})).kernel for t in W.TEMPLATES}
+    assert kinds["maxpool"] == Kernel.MAXPOOL
+    assert kinds["alexnet_conv1"] == Kernel.CONV_TC
+    for t in ("gemm", "correlation", "bilateral", "motion_estimation", "conv2d", "dilated"):
+        assert kinds[t] == Kernel.GENERIC
+    assert Plan(W.build_template("conv2d", {"cin": 4, "cout": 8})).kernel == Kernel.CONV_TC
+    assert Plan(W.build_template("relu_fused_conv", {"cin": 4, "cout": 8})).description.endswith("relu")
+    # FIX16 always runs the exact interpreter
+    assert Plan(W.build_template("maxpool", {"fix": 1})).kernel == Kernel.GENERIC
+    assert Plan(W.build_template("conv2d", {"cin": 4, "cout": 8, "fix": 1})).kernel == Kernel.GENERIC
+    # EXACT forces the interpreter
+    assert Plan(W.config_workload("C3", with_inputs=False), FLAG_EXACT).kernel == Kernel.GENERIC
+
+
+def test_validate_errors_mirror_reference():
+    w = W.build_template("gemm", {})
+    w.view_b.p_shape = [8, 9]
+    with pytest.raises(Error) as e:
+        Plan(w)
+    assert e.value.code == ErrorCode.BadParams            # views must share p and a shapes
+    w = W.build_template("gemm", {})
+    w.program.depth = 2
+    with pytest.raises(Error) as e:
+        Plan(w)
+    assert e.value.code == ErrorCode.BadParams            # depth must match |a|
+    w = W.build_template("gemm", {})
+    w.program.segments.append([])
+    with pytest.raises(Error) as e:
+        Plan(w)
+    assert e.value.code == ErrorCode.BadParams            # 2*depth+1 segments
+    w = W.build_template("gemm", {})
+    w.program.segments[1][0].dst.reg = 16
+    with pytest.raises(Error) as e:
+        Plan(w)
+    assert e.value.code == ErrorCode.BadParams            # register id < 16
+    w = W.build_template("gemm", {})
+    w.program.segments[1][0].shift = 16
+    with pytest.raises(Error) as e:
+        Plan(w)
+    assert e.value.code == ErrorCode.BadParams            # shift 0..15
+    w = W.build_template("gemm", {})
+    w.view_a.terms.append(ViewTerm(0, 5, 1, 0))
+    with pytest.raises(Error) as e:
+        Plan(w)
+    assert e.value.code == ErrorCode.BadParams            # AXIS_OUT_OF_RANGE
+    w = W.build_template("gemm", {})
+    w.view_a.a_shape = [0]
+    w.view_b.a_shape = [0]
+    with pytest.raises(Error) as e:
+        Plan(w)
+    assert e.value.code == ErrorCode.OutOfRange           # phase_range on an empty extent
+    with pytest.raises(Error) as e:
+        Plan(W.build_template("gemm", {}), FLAG_ARGMIN)
+    assert e.value.code == ErrorCode.UnsupportedProgram   # argmin needs the SAD kernel
+
+
+def test_reject_out_of_range_views_go_to_checking_interpreter():
+    w = W.build_template("maxpool", {"h": 4, "w": 4, "k": 2})
+    w.view_a.terms[1].offset = -1
+    assert Plan(w).kernel == Kernel.GENERIC   # the interpreter raises OutOfRange at run time
+
+
+def test_generators_match_reference_fill_random():
+    from tests.golden_io import load
+    g = load()
+    for seed in (1, 2, 3, 4, 5, 2001, 2002):
+        assert np.array_equal(W.gen_uniform([256], seed), g[f"fill_f32/{seed}"])
+        assert np.array_equal(W.gen_range_i16([256], seed), g[f"fill_i16/{seed}"])
+
+
+def test_bf16_conversion_rne():
+    x = np.array([1.0, 1.00390625, 1.01171875, -2.5, 3.3e38, np.inf, -0.0], np.float32)
+    b = W.to_bf16_bits(x)
+    back = W.bf16_bits_to_f32(b)
+    assert back[0] == 1.0 and back[1] == 1.0 and back[2] == 1.015625 and back[3] == -2.5
+    assert np.isinf(back[5]) and np.signbit(back[6])
+
+
+def test_device_entry_points_fail_loudly_without_a_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    w = W.config_workload("C1", scale=8)
+    with pytest.raises(Error) as e:
+        Plan(w).run_host(w.src_a, w.src_b)
+    assert e.value.code == ErrorCode.Cuda
