@@ -33,7 +33,11 @@ namespace {
 
 constexpr int kBM = 128;
 constexpr int kMaxStages = 6;
-constexpr int kThreads = 320;
+constexpr int kProducerWarps = 8;                 // warps 0-7: the MERIT gather
+constexpr int kProducers = kProducerWarps * 32;
+constexpr int kWarpLoad = kProducerWarps;         // warp 8: TMEM alloc + B loader
+constexpr int kWarpMma = kProducerWarps + 1;      // warp 9: MMA issuer
+constexpr int kThreads = (kProducerWarps + 2 + 4) * 32;  // + 4 epilogue warps
 constexpr uint32_t kAPlane = kBM * 128;  // 128 rows x 64 bf16
 
 struct ConvArgs {
@@ -47,6 +51,7 @@ struct ConvArgs {
   uint32_t stage_bytes;
   uint32_t tmem_cols;
   int stages;
+  int tap3;  // 3-tap shared-load gather (KW=3, dx=1, ox=-1, sx in {1,2})
 };
 
 // ------------------------------------------------------------- PTX shims --
@@ -141,7 +146,7 @@ __device__ __forceinline__ float bf16_round(float x) {
 }
 
 // --------------------------------------------------------------- kernel --
-template <bool IN_BF16, bool SPLIT3>
+template <bool IN_BF16, bool SPLIT3, int TAPS>
 __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(ConvArgs A) {
   extern __shared__ uint8_t smem_raw[];
   const ConvParams& p = A.p;
@@ -163,7 +168,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(ConvArgs A) {
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(full_bar(s), 128 + 1);
+      mbar_init(full_bar(s), kProducers + 1);
       mbar_init(empty_bar(s), 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -172,7 +177,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(ConvArgs A) {
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 4) {
+  if (warp == kWarpLoad) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot),
                  "r"(A.tmem_cols)
                  : "memory");
@@ -187,16 +192,205 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(ConvArgs A) {
   const long long HW = (long long)p.H * p.W;
   const int BN = p.BN;
 
-  if (warp < 4) {
+  if (warp < kProducerWarps) {
     // ================= A producers: the MERIT gather M(.) ==================
-    const int tid = threadIdx.x;  // row of the 128-pixel tile
-    const uint32_t row_off = (tid >> 3) * 1024u + (tid & 7) * 128u;
-    const uint32_t swz = tid & 7;
+    // Thread = (pixel row m of the 128-pixel tile, channel half h): it writes
+    // chunks 4h..4h+3 (channels 32h..32h+31 of the 64-channel block) of row m.
+    const int m_local = threadIdx.x & 127;
+    const int h = threadIdx.x >> 7;
+    const uint32_t row_off = (m_local >> 3) * 1024u + (m_local & 7) * 128u;
+    const uint32_t swz = m_local & 7;
     int stage = 0;
     uint32_t phase = 0;
+    // Stage bookkeeping for the 3-tap groups (stage, phase of slot i ahead).
+    auto slot = [&](int ahead, int& st, uint32_t& ph) {
+      st = stage + ahead;
+      ph = phase;
+      while (st >= kStages) { st -= kStages; ph ^= 1u; }
+    };
+    auto advance = [&](int n) {
+      stage += n;
+      while (stage >= kStages) { stage -= kStages; phase ^= 1u; }
+    };
+    // Pack 8 consecutive channel values (fp32) of one tap into 16 bytes of the
+    // swizzled K-major row (and the lo residual plane for the 3-term split).
+    auto put8 = [&](uint32_t a_hi, int j, const float* q) {
+      const uint32_t dst = row_off + ((j ^ swz) << 4);
+      st_shared_v4(a_hi + dst, pack_bf16(q[0], q[1]), pack_bf16(q[2], q[3]), pack_bf16(q[4], q[5]),
+                   pack_bf16(q[6], q[7]));
+      if (SPLIT3) {
+        float l[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) l[e] = q[e] - bf16_round(q[e]);
+        st_shared_v4(a_hi + kAPlane + dst, pack_bf16(l[0], l[1]), pack_bf16(l[2], l[3]),
+                     pack_bf16(l[4], l[5]), pack_bf16(l[6], l[7]));
+      }
+    };
+    const int lane_ = threadIdx.x & 31;
+    // Load one (ky, cb) group: this lane's 32 channel values (a 32-bit word
+    // for bf16 stride 2 = input columns 2x, 2x+1; else the element at column
+    // sx*x) plus the edge values for channel `lane_`.
+    struct Grp {
+      uint32_t w[32];  // raw words / floats (bit patterns)
+      uint32_t fl, fr; // left / right edge value for channel lane_
+    };
+    auto load_grp = [&](Grp& g, bool valid, int n, int iy, int x, int cb) {
+      const bool rowok = valid && iy >= 0 && iy < p.H;
+      const int c0 = cb * 64 + h * 32;
+      const int nc = rowok ? min(32, p.Cin - c0) : 0;
+      const long long plane0 = ((long long)n * p.Cin + c0) * HW + (long long)iy * p.W;
+      // edge pixels: lane 0's left neighbour, lane 31's right neighbour
+      const int x0 = __shfl_sync(0xffffffffu, x, 0);
+      const int x31 = __shfl_sync(0xffffffffu, x, 31);
+      const bool ok0 = __shfl_sync(0xffffffffu, rowok ? 1 : 0, 0) != 0;
+      const bool ok31 = __shfl_sync(0xffffffffu, rowok ? 1 : 0, 31) != 0;
+      const long long pl0 = __shfl_sync(0xffffffffu, plane0, 0);
+      const long long pl31 = __shfl_sync(0xffffffffu, plane0, 31);
+      const int nc0 = __shfl_sync(0xffffffffu, nc, 0);
+      const int nc31 = __shfl_sync(0xffffffffu, nc, 31);
+      if (IN_BF16) {
+        const uint16_t* src = static_cast<const uint16_t*>(A.in);
+        if (TAPS == 2) {
+#pragma unroll
+          for (int c = 0; c < 32; ++c)
+            g.w[c] = c < nc ? __ldg(reinterpret_cast<const uint32_t*>(src + plane0 + c * HW + 2 * x)) : 0u;
+          g.fl = (ok0 && x0 > 0 && lane_ < nc0) ? __ldg(src + pl0 + lane_ * HW + 2 * x0 - 1) : 0u;
+          g.fr = 0u;
+        } else {
+#pragma unroll
+          for (int c = 0; c < 32; ++c) g.w[c] = c < nc ? __ldg(src + plane0 + c * HW + x) : 0u;
+          g.fl = (ok0 && x0 > 0 && lane_ < nc0) ? __ldg(src + pl0 + lane_ * HW + x0 - 1) : 0u;
+          g.fr = (ok31 && x31 + 1 < p.W && lane_ < nc31) ? __ldg(src + pl31 + lane_ * HW + x31 + 1) : 0u;
+        }
+      } else {
+        const float* src = static_cast<const float*>(A.in);
+        if (false) {  // f32 stride 2 uses the general gather
+#pragma unroll
+          for (int c = 0; c < 32; ++c)
+            g.w[c] = c < nc ? __float_as_uint(__ldg(src + plane0 + c * HW + 2 * x)) : 0u;
+          g.fl = (ok0 && x0 > 0 && lane_ < nc0) ? __float_as_uint(__ldg(src + pl0 + lane_ * HW + 2 * x0 - 1)) : 0u;
+          g.fr = 0u;
+        } else {
+#pragma unroll
+          for (int c = 0; c < 32; ++c) g.w[c] = c < nc ? __float_as_uint(__ldg(src + plane0 + c * HW + x)) : 0u;
+          g.fl = (ok0 && x0 > 0 && lane_ < nc0) ? __float_as_uint(__ldg(src + pl0 + lane_ * HW + x0 - 1)) : 0u;
+          g.fr = (ok31 && x31 + 1 < p.W && lane_ < nc31) ? __float_as_uint(__ldg(src + pl31 + lane_ * HW + x31 + 1)) : 0u;
+        }
+      }
+    };
+    // f32 stride 2 needs column 2x+1 too: loaded synchronously (rare path).
+    auto odd_f32 = [&](bool valid, int n, int iy, int x, int cb, int c) -> float {
+      const bool rowok = valid && iy >= 0 && iy < p.H;
+      const int c0 = cb * 64 + h * 32;
+      if (!rowok || c0 + c >= p.Cin || 2 * x + 1 >= p.W) return 0.f;
+      return __ldg(static_cast<const float*>(A.in) + ((long long)n * p.Cin + c0 + c) * HW +
+                   (long long)iy * p.W + 2 * x + 1);
+    };
+    // Emit the three taps of a loaded group into three consecutive ring slots.
+    auto emit_grp = [&](const Grp& g, bool valid, int n, int iy, int x, int cb) {
+      for (int kx = 0; kx < 3; ++kx) {
+        mbar_wait(empty_bar(stage), phase ^ 1);
+        const uint32_t a_hi = ring + stage * A.stage_bytes;
+#pragma unroll
+        for (int q8 = 0; q8 < 4; ++q8) {
+          float t[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int c = q8 * 8 + e;
+            const uint32_t wv = g.w[c];
+            float v;
+            if (IN_BF16 && TAPS == 2) {
+              if (kx == 0) {
+                uint32_t l = __shfl_up_sync(0xffffffffu, wv, 1) >> 16;
+                const uint32_t f = __shfl_sync(0xffffffffu, g.fl, c);
+                if (lane_ == 0) l = f;
+                if (x == 0) l = 0;
+                v = __uint_as_float(l << 16);
+              } else if (kx == 1) {
+                v = __uint_as_float(wv << 16);
+              } else {
+                v = __uint_as_float(wv & 0xffff0000u);
+              }
+            } else if (IN_BF16) {
+              if (kx == 0) {
+                uint32_t l = __shfl_up_sync(0xffffffffu, wv, 1);
+                const uint32_t f = __shfl_sync(0xffffffffu, g.fl, c);
+                if (lane_ == 0) l = f;
+                if (x == 0) l = 0;
+                v = __uint_as_float(l << 16);
+              } else if (kx == 1) {
+                v = __uint_as_float(wv << 16);
+              } else {
+                uint32_t r = __shfl_down_sync(0xffffffffu, wv, 1);
+                const uint32_t f = __shfl_sync(0xffffffffu, g.fr, c);
+                if (lane_ == 31) r = f;
+                if (x + 1 >= p.W) r = 0;  // Wo == W: a wrapped lane means the right pad
+                v = __uint_as_float(r << 16);
+              }
+            } else if (false) {
+              if (kx == 0) {
+                float l = __shfl_up_sync(0xffffffffu, odd_f32(valid, n, iy, x, cb, c), 1);
+                const float f = __uint_as_float(__shfl_sync(0xffffffffu, g.fl, c));
+                if (lane_ == 0) l = f;
+                if (x == 0) l = 0.f;
+                v = l;
+              } else if (kx == 1) {
+                v = __uint_as_float(wv);
+              } else {
+                v = odd_f32(valid, n, iy, x, cb, c);
+              }
+            } else {
+              if (kx == 0) {
+                float l = __uint_as_float(__shfl_up_sync(0xffffffffu, wv, 1));
+                const float f = __uint_as_float(__shfl_sync(0xffffffffu, g.fl, c));
+                if (lane_ == 0) l = f;
+                if (x == 0) l = 0.f;
+                v = l;
+              } else if (kx == 1) {
+                v = __uint_as_float(wv);
+              } else {
+                float r = __uint_as_float(__shfl_down_sync(0xffffffffu, wv, 1));
+                const float f = __uint_as_float(__shfl_sync(0xffffffffu, g.fr, c));
+                if (lane_ == 31) r = f;
+                if (x + 1 >= p.W) r = 0.f;  // Wo == W: a wrapped lane means the right pad
+                v = r;
+              }
+            }
+            t[e] = v;
+          }
+          put8(a_hi, h * 4 + q8, t);
+        }
+        fence_proxy_async();
+        mbar_arrive(full_bar(stage));
+        advance(1);
+      }
+    };
+    // One tile: walk its (ky, cb) groups with a one-group-deep load pipeline.
+    auto tap3_tile = [&](int tile, bool valid, int n, int y, int x, int by) {
+      (void)tile;
+      // Two named buffers (no dynamic indexing: both stay in registers).
+      Grp ga, gb;
+      const int ngrp = p.KH * p.CB;
+      load_grp(ga, valid, n, by, x, 0);
+      for (int gi = 0; gi < ngrp; gi += 2) {
+        const int ky0 = gi / p.CB, cb0 = gi - ky0 * p.CB;
+        if (gi + 1 < ngrp) {
+          const int ky1 = (gi + 1) / p.CB, cb1 = (gi + 1) - ky1 * p.CB;
+          load_grp(gb, valid, n, by + ky1 * p.dy, x, cb1);
+        }
+        emit_grp(ga, valid, n, by + ky0 * p.dy, x, cb0);
+        if (gi + 1 >= ngrp) break;
+        if (gi + 2 < ngrp) {
+          const int ky2 = (gi + 2) / p.CB, cb2 = (gi + 2) - ky2 * p.CB;
+          load_grp(ga, valid, n, by + ky2 * p.dy, x, cb2);
+        }
+        const int ky1 = (gi + 1) / p.CB, cb1 = (gi + 1) - ky1 * p.CB;
+        emit_grp(gb, valid, n, by + ky1 * p.dy, x, cb1);
+      }
+    };
     for (int tile = blockIdx.x; tile < A.n_tiles; tile += gridDim.x) {
       const int mt = tile / p.n_tiles_n;
-      const long long m = (long long)mt * kBM + tid;
+      const long long m = (long long)mt * kBM + m_local;
       const bool valid = m < p.npix;
       int n = 0, y = 0, x = 0;
       if (valid) {
@@ -206,61 +400,46 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(ConvArgs A) {
         x = rem % p.Wo;
       }
       const int by = y * p.sy + p.oy, bx = x * p.sx + p.ox;
-      for (int kb = 0; kb < p.n_kb; ++kb) {
-        const int tap = kb / p.CB, cb = kb - tap * p.CB;
-        const int ky = tap / p.KW, kx = tap - ky * p.KW;
-        const int iy = by + ky * p.dy, ix = bx + kx * p.dx;
-        const bool inb = valid && iy >= 0 && iy < p.H && ix >= 0 && ix < p.W;
-        const int c0 = cb * 64;
-        const int nc = inb ? min(64, p.Cin - c0) : 0;
-        const long long off = ((long long)n * p.Cin + c0) * HW + (long long)iy * p.W + ix;
-        mbar_wait(empty_bar(stage), phase ^ 1);
-        const uint32_t a_hi = ring + stage * A.stage_bytes;
-        const uint32_t a_lo = a_hi + kAPlane;
-#pragma unroll
-        for (int half = 0; half < 2; ++half) {
+      if (TAPS != 0) {
+        // KW == 3, dx == 1, ox == -1, sx in {1, 2}: one coalesced load per
+        // (channel, input row) serves all three kx taps; the neighbours come
+        // from adjacent lanes by shuffle, and the two values beyond the
+        // warp's edge pixels are prefetched one channel per lane.  The next
+        // (ky, cb) group's loads are in flight while this one is packed.
+        tap3_tile(tile, valid, n, y, x, by);
+      } else {
+        // General view: any KH x KW, strides, dilations, offsets.
+        for (int kb = 0; kb < p.n_kb; ++kb) {
+          const int kx = kb % p.KW;
+          const int t = kb / p.KW;
+          const int cb = t % p.CB, ky = t / p.CB;
+          const int iy = by + ky * p.dy, ix = bx + kx * p.dx;
+          const bool inb = valid && iy >= 0 && iy < p.H && ix >= 0 && ix < p.W;
+          const int c0 = cb * 64 + h * 32;
+          const int nc = inb ? min(32, p.Cin - c0) : 0;
+          const long long off = ((long long)n * p.Cin + c0) * HW + (long long)iy * p.W + ix;
+          mbar_wait(empty_bar(stage), phase ^ 1);
+          const uint32_t a_hi = ring + stage * A.stage_bytes;
           float v[32];
           if (IN_BF16) {
-            const uint16_t* src = static_cast<const uint16_t*>(A.in) + off + half * 32 * HW;
+            const uint16_t* src = static_cast<const uint16_t*>(A.in) + off;
 #pragma unroll
-            for (int c = 0; c < 32; ++c) {
-              const int ci = half * 32 + c;
-              uint16_t u = ci < nc ? __ldg(src + c * HW) : uint16_t(0);
-              v[c] = __uint_as_float(static_cast<uint32_t>(u) << 16);
-            }
+            for (int c = 0; c < 32; ++c)
+              v[c] = c < nc ? __uint_as_float(static_cast<uint32_t>(__ldg(src + c * HW)) << 16) : 0.f;
           } else {
-            const float* src = static_cast<const float*>(A.in) + off + half * 32 * HW;
+            const float* src = static_cast<const float*>(A.in) + off;
 #pragma unroll
-            for (int c = 0; c < 32; ++c) {
-              const int ci = half * 32 + c;
-              v[c] = ci < nc ? __ldg(src + c * HW) : 0.f;
-            }
+            for (int c = 0; c < 32; ++c) v[c] = c < nc ? __ldg(src + c * HW) : 0.f;
           }
 #pragma unroll
-          for (int j4 = 0; j4 < 4; ++j4) {
-            const int j = half * 4 + j4;
-            const float* q = v + j4 * 8;
-            const uint32_t dst = row_off + ((j ^ swz) << 4);
-            st_shared_v4(a_hi + dst, pack_bf16(q[0], q[1]), pack_bf16(q[2], q[3]),
-                         pack_bf16(q[4], q[5]), pack_bf16(q[6], q[7]));
-            if (SPLIT3) {
-              float l[8];
-#pragma unroll
-              for (int e = 0; e < 8; ++e) l[e] = q[e] - bf16_round(q[e]);
-              st_shared_v4(a_lo + dst, pack_bf16(l[0], l[1]), pack_bf16(l[2], l[3]),
-                           pack_bf16(l[4], l[5]), pack_bf16(l[6], l[7]));
-            }
-          }
-        }
-        fence_proxy_async();
-        mbar_arrive(full_bar(stage));
-        if (++stage == kStages) {
-          stage = 0;
-          phase ^= 1;
+          for (int j4 = 0; j4 < 4; ++j4) put8(a_hi, h * 4 + j4, v + j4 * 8);
+          fence_proxy_async();
+          mbar_arrive(full_bar(stage));
+          advance(1);
         }
       }
     }
-  } else if (warp == 4) {
+  } else if (warp == kWarpLoad) {
     // ================= B loader (weights, bulk async copy) =================
     if (lane == 0) {
       const uint32_t b_bytes = A.b_plane * (SPLIT3 ? 2 : 1);
@@ -281,7 +460,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(ConvArgs A) {
       }
     }
     __syncwarp();
-  } else if (warp == 5) {
+  } else if (warp == kWarpMma) {
     // ================= MMA issuer (single thread) ===========================
     if (lane == 0) {
       const uint32_t idesc = make_idesc(BN);
@@ -367,7 +546,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(ConvArgs A) {
     }
   }
   __syncthreads();
-  if (warp == 4) {
+  if (warp == kWarpLoad) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                  "r"(A.tmem_cols)
@@ -389,8 +568,8 @@ __global__ void conv_pack_kernel(const void* __restrict__ w, uint8_t* __restrict
     const long long t2 = t / p.BN;
     const int kb = static_cast<int>(t2 % p.n_kb);
     const int nt = static_cast<int>(t2 / p.n_kb);
-    const int tap = kb / p.CB, cb = kb % p.CB;
-    const int ky = tap / p.KW, kx = tap % p.KW;
+    const int kx = kb % p.KW, t3 = kb / p.KW;
+    const int cb = t3 % p.CB, ky = t3 / p.CB;  // k-block order (ky, cb, kx)
     const int co = nt * p.BN + n;
     float hi[8], lo[8];
 #pragma unroll
@@ -457,27 +636,39 @@ merit_status launch_conv(const merit_plan& plan, const void* a, const void* pack
   uint32_t cols = 32;
   while (cols < static_cast<uint32_t>(2 * p.BN)) cols <<= 1;
   A.tmem_cols = cols;
+  A.tap3 = (p.KW == 3 && p.dx == 1 && p.ox == -1 &&
+            ((p.sx == 1 && p.Wo == p.W) || (p.sx == 2 && p.in_bf16 && p.W % 2 == 0 &&
+                           (reinterpret_cast<uintptr_t>(a) % 4) == 0)))
+               ? 1 : 0;
   if (A.n_tiles == 0) return MERIT_OK;
   const size_t fixed = 1024 + 8 * (2 * kMaxStages + 4) + 16;
   A.stages = static_cast<int>((227 * 1024 - fixed) / A.stage_bytes);
   if (A.stages > kMaxStages) A.stages = kMaxStages;
   if (A.stages < 2) return fail(MERIT_E_UNSUPPORTED_VIEW, "conv tile exceeds shared memory");
+  if (A.stages < 3) A.tap3 = 0;  // a 3-tap group holds three ring slots
   const size_t smem = fixed + (size_t)A.stages * A.stage_bytes;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int grid = num_sms();
   if (grid > A.n_tiles) grid = A.n_tiles;
   cudaError_t e;
-#define MERIT_LAUNCH_CONV(INB, S3)                                                             \
+#define MERIT_LAUNCH_CONV(INB, S3, TP)                                                         \
   do {                                                                                         \
-    auto k = conv_tc_kernel<INB, S3>;                                                          \
+    auto k = conv_tc_kernel<INB, S3, TP>;                                                      \
     e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);       \
     if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(conv)");                  \
     k<<<grid, kThreads, smem, s>>>(A);                                                         \
   } while (0)
+  const int taps = A.tap3 ? p.sx : 0;
   if (p.in_bf16) {
-    if (split3) MERIT_LAUNCH_CONV(true, true); else MERIT_LAUNCH_CONV(true, false);
+    if (split3) MERIT_LAUNCH_CONV(true, true, 0);
+    else if (taps == 2) MERIT_LAUNCH_CONV(true, false, 2);
+    else if (taps == 1) MERIT_LAUNCH_CONV(true, false, 1);
+    else MERIT_LAUNCH_CONV(true, false, 0);
   } else {
-    if (split3) MERIT_LAUNCH_CONV(false, true); else MERIT_LAUNCH_CONV(false, false);
+    if (split3 && taps == 1) MERIT_LAUNCH_CONV(false, true, 1);
+    else if (split3) MERIT_LAUNCH_CONV(false, true, 0);
+    else if (taps == 1) MERIT_LAUNCH_CONV(false, false, 1);
+    else MERIT_LAUNCH_CONV(false, false, 0);
   }
 #undef MERIT_LAUNCH_CONV
   return launch_status("conv_tc_kernel");

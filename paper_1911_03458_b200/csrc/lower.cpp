@@ -292,6 +292,7 @@ bool match_sad_views(const merit_view_spec& vc, const ViewAffine& fc,
   kshape[P + 1] = BW;
   if (!view_in_range(fc, kshape)) return false;
   if (sp.WY < 1 || sp.WX < 1 || sp.WY > 256 || sp.WX > 256) return false;
+  if (sad_rows_per_thread(sp.BH, sp.WY, sp.WX) == 0) return false;
   if (vr.boundary == MERIT_REJECT && !view_in_range(fr, kshape)) return false;  // -> generic error
   sp.boundary = vr.boundary == MERIT_REJECT ? MERIT_ZERO_PAD : vr.boundary;
   return true;

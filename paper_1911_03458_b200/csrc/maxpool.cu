@@ -57,7 +57,7 @@ __global__ void maxpool_generic_kernel(const float* __restrict__ in, float* __re
 // 64-bit store.  Every input row is read once per band (one shared row per
 // band boundary).
 template <int RB>
-__global__ void __launch_bounds__(256) maxpool3s2_kernel(const float* __restrict__ in,
+__global__ void __launch_bounds__(256, 3) maxpool3s2_kernel(const float* __restrict__ in,
                                                          float* __restrict__ out, MaxpoolParams p,
                                                          int nseg, int nband) {
   const long long wg = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
@@ -131,7 +131,7 @@ merit_status launch_maxpool(const merit_plan& plan, const void* a, void* out, vo
   const bool aligned = (reinterpret_cast<uintptr_t>(in) % 16 == 0) &&
                        (reinterpret_cast<uintptr_t>(out) % 8 == 0);
   if (p.fast && aligned) {
-    constexpr int RB = 8;
+    constexpr int RB = 4;
     const int nseg = (p.W + 127) / 128;
     const int nband = (p.Ho + RB - 1) / RB;
     const long long warps = p.planes * nband * nseg;

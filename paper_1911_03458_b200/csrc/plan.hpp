@@ -139,6 +139,8 @@ merit_status lower(const merit_workload_desc& d, merit_plan& plan);
 merit_status launch_generic(const merit_plan& plan, const void* a, const void* b, void* out,
                             void* stream);
 merit_status launch_maxpool(const merit_plan& plan, const void* a, void* out, void* stream);
+// Rows per thread of the SAD kernel variant for a window, 0 if none fits.
+int sad_rows_per_thread(int BH, int WY, int WX);
 merit_status launch_sad(const merit_plan& plan, const void* a, const void* b, void* out,
                         void* aux, void* stream);
 merit_status launch_conv_pack(const merit_plan& plan, const void* b, void* packed, void* stream);
