@@ -26,19 +26,22 @@
 //   warps 6-9 epilogue.
 #include <cuda_bf16.h>
 
-#include "common.cuh"
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "tc_common.cuh"
 
 namespace merit_dev {
 namespace {
 
-constexpr int kBM = 128;
+using namespace tc;
 constexpr int kMaxStages = 6;
 constexpr int kProducerWarps = 8;                 // warps 0-7: the MERIT gather
 constexpr int kProducers = kProducerWarps * 32;
 constexpr int kWarpLoad = kProducerWarps;         // warp 8: TMEM alloc + B loader
 constexpr int kWarpMma = kProducerWarps + 1;      // warp 9: MMA issuer
 constexpr int kThreads = (kProducerWarps + 2 + 4) * 32;  // + 4 epilogue warps
-constexpr uint32_t kAPlane = kBM * 128;  // 128 rows x 64 bf16
 
 struct ConvArgs {
   ConvParams p;
@@ -52,98 +55,10 @@ struct ConvArgs {
   uint32_t tmem_cols;
   int stages;
   int tap3;  // 3-tap shared-load gather (KW=3, dx=1, ox=-1, sx in {1,2})
+  unsigned long long* prof; // per-role cycle counters when debug & 64
+  int debug; // MERIT_CONV_DEBUG (profiling only): 1 = skip A gather, 2 = skip B copy,
+             // 4 = skip epilogue stores, 8 = no L2 prefetch
 };
-
-// ------------------------------------------------------------- PTX shims --
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n\t"
-      "LAB_WAIT:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@P1 bra DONE;\n\t"
-      "bra LAB_WAIT;\n\t"
-      "DONE:\n\t}" ::"r"(bar),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes,
-                                         uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-      "l"(src), "r"(bytes), "r"(bar)
-      : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_before() {
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_after() {
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_commit(uint32_t bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-               : "memory");
-}
-__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
-                                       uint32_t idesc, uint32_t accum) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
-      : "memory");
-}
-// UMMA shared-memory descriptor: K-major, 128-byte swizzle, 8-row atoms of
-// 1024 B stacked densely (SBO = 1024), version 1 (sm_100).
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
-  return static_cast<uint64_t>((saddr & 0x3FFFFu) >> 4) | (static_cast<uint64_t>(1) << 16) |
-         (static_cast<uint64_t>(1024 >> 4) << 32) | (static_cast<uint64_t>(1) << 46) |
-         (static_cast<uint64_t>(2) << 61);
-}
-// Instruction descriptor, kind::f16: D f32, A/B bf16, both K-major, M=128.
-__host__ __device__ constexpr uint32_t make_idesc(int n) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | (static_cast<uint32_t>(n >> 3) << 17) |
-         (static_cast<uint32_t>(kBM >> 4) << 24);
-}
-
-#define TMEM_LD32(taddr, r)                                                                     \
-  asm volatile(                                                                                 \
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "                                                 \
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"                                 \
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"                \
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),     \
-        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), \
-        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),           \
-        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),           \
-        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])            \
-      : "r"(taddr))
-
-__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c,
-                                             uint32_t d) {
-  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c),
-               "r"(d)
-               : "memory");
-}
-
-__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
-  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
-  return *reinterpret_cast<uint32_t*>(&v);
-}
-__device__ __forceinline__ float bf16_round(float x) {
-  return __bfloat162float(__float2bfloat16_rn(x));
-}
 
 // --------------------------------------------------------------- kernel --
 template <bool IN_BF16, bool SPLIT3, int TAPS>
@@ -192,12 +107,16 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(ConvArgs A) {
   const long long HW = (long long)p.H * p.W;
   const int BN = p.BN;
 
+  unsigned long long e_start_g = 0, e_tfull_g = 0;
   if (warp < kProducerWarps) {
     // ================= A producers: the MERIT gather M(.) ==================
     // Thread = (pixel row m of the 128-pixel tile, channel half h): it writes
     // chunks 4h..4h+3 (channels 32h..32h+31 of the 64-channel block) of row m.
     const int m_local = threadIdx.x & 127;
     const int h = threadIdx.x >> 7;
+    const bool prof_on = (A.debug & 64) && (threadIdx.x & 31) == 0;
+    unsigned long long c_empty = 0, c_load = 0, c_fence = 0, c_issue = 0;
+    const unsigned long long c_start = clock64();
     const uint32_t row_off = (m_local >> 3) * 1024u + (m_local & 7) * 128u;
     const uint32_t swz = m_local & 7;
     int stage = 0;
@@ -285,6 +204,77 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(ConvArgs A) {
       if (!rowok || c0 + c >= p.Cin || 2 * x + 1 >= p.W) return 0.f;
       return __ldg(static_cast<const float*>(A.in) + ((long long)n * p.Cin + c0 + c) * HW +
                    (long long)iy * p.W + 2 * x + 1);
+    };
+    // bf16 data: the swizzled row chunks are built straight from the loaded
+    // words with byte permutes (no fp32 round trip).  Stride 2: word c holds
+    // input columns (2x, 2x+1) of channel c = taps 1 and 2; tap 0 (column
+    // 2x-1) is the high half of the left lane's word.  Stride 1: word c holds
+    // column x in its low half; taps 0 / 2 come from the left / right lanes.
+    auto emit_grp_bf16 = [&](const Grp& g, int x) {
+      const bool row_start = x == 0;
+      const bool row_end = x + 1 >= p.W;
+      if (prof_on) {  // time until this group's loads have landed
+        const unsigned long long t0 = clock64();
+        uint32_t dep = 0;
+#pragma unroll
+        for (int c = 0; c < 32; ++c) dep ^= g.w[c];
+        asm volatile("" ::"r"(dep));
+        if (dep == 0x12345678u) asm volatile("" ::: "memory");
+        c_load += clock64() - t0;
+      }
+      for (int kx = 0; kx < 3; ++kx) {
+        mbar_wait_t(empty_bar(stage), phase ^ 1, c_empty, prof_on);
+        const uint32_t a_hi = ring + stage * A.stage_bytes;
+#pragma unroll
+        for (int q8 = 0; q8 < 4; ++q8) {
+          uint32_t pk[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int c = q8 * 8 + 2 * e;
+            const uint32_t w0 = g.w[c], w1 = g.w[c + 1];
+            uint32_t v;
+            if (TAPS == 2) {
+              if (kx == 0) {
+                uint32_t l0 = __shfl_up_sync(0xffffffffu, w0, 1);
+                uint32_t l1 = __shfl_up_sync(0xffffffffu, w1, 1);
+                const uint32_t f0 = __shfl_sync(0xffffffffu, g.fl, c);
+                const uint32_t f1 = __shfl_sync(0xffffffffu, g.fl, c + 1);
+                if (lane_ == 0) { l0 = f0 << 16; l1 = f1 << 16; }
+                v = row_start ? 0u : __byte_perm(l0, l1, 0x7632);
+              } else if (kx == 1) {
+                v = __byte_perm(w0, w1, 0x5410);
+              } else {
+                v = __byte_perm(w0, w1, 0x7632);
+              }
+            } else {
+              if (kx == 0) {
+                uint32_t l0 = __shfl_up_sync(0xffffffffu, w0, 1);
+                uint32_t l1 = __shfl_up_sync(0xffffffffu, w1, 1);
+                const uint32_t f0 = __shfl_sync(0xffffffffu, g.fl, c);
+                const uint32_t f1 = __shfl_sync(0xffffffffu, g.fl, c + 1);
+                if (lane_ == 0) { l0 = f0; l1 = f1; }
+                v = row_start ? 0u : __byte_perm(l0, l1, 0x5410);
+              } else if (kx == 1) {
+                v = __byte_perm(w0, w1, 0x5410);
+              } else {
+                uint32_t r0 = __shfl_down_sync(0xffffffffu, w0, 1);
+                uint32_t r1 = __shfl_down_sync(0xffffffffu, w1, 1);
+                const uint32_t f0 = __shfl_sync(0xffffffffu, g.fr, c);
+                const uint32_t f1 = __shfl_sync(0xffffffffu, g.fr, c + 1);
+                if (lane_ == 31) { r0 = f0; r1 = f1; }
+                v = row_end ? 0u : __byte_perm(r0, r1, 0x5410);
+              }
+            }
+            pk[e] = v;
+          }
+          st_shared_v4(a_hi + row_off + (((h * 4 + q8) ^ swz) << 4), pk[0], pk[1], pk[2], pk[3]);
+        }
+        unsigned long long tf = prof_on ? clock64() : 0;
+        fence_proxy_async();
+        if (prof_on) c_fence += clock64() - tf;
+        mbar_arrive(full_bar(stage));
+        advance(1);
+      }
     };
     // Emit the three taps of a loaded group into three consecutive ring slots.
     auto emit_grp = [&](const Grp& g, bool valid, int n, int iy, int x, int cb) {
@@ -376,16 +366,18 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(ConvArgs A) {
         const int ky0 = gi / p.CB, cb0 = gi - ky0 * p.CB;
         if (gi + 1 < ngrp) {
           const int ky1 = (gi + 1) / p.CB, cb1 = (gi + 1) - ky1 * p.CB;
+          const unsigned long long tl = prof_on ? clock64() : 0;
           load_grp(gb, valid, n, by + ky1 * p.dy, x, cb1);
+          if (prof_on) c_issue += clock64() - tl;
         }
-        emit_grp(ga, valid, n, by + ky0 * p.dy, x, cb0);
+        if (IN_BF16 && !SPLIT3) emit_grp_bf16(ga, x); else emit_grp(ga, valid, n, by + ky0 * p.dy, x, cb0);
         if (gi + 1 >= ngrp) break;
         if (gi + 2 < ngrp) {
           const int ky2 = (gi + 2) / p.CB, cb2 = (gi + 2) - ky2 * p.CB;
           load_grp(ga, valid, n, by + ky2 * p.dy, x, cb2);
         }
         const int ky1 = (gi + 1) / p.CB, cb1 = (gi + 1) - ky1 * p.CB;
-        emit_grp(gb, valid, n, by + ky1 * p.dy, x, cb1);
+        if (IN_BF16 && !SPLIT3) emit_grp_bf16(gb, x); else emit_grp(gb, valid, n, by + ky1 * p.dy, x, cb1);
       }
     };
     for (int tile = blockIdx.x; tile < A.n_tiles; tile += gridDim.x) {
@@ -400,6 +392,14 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(ConvArgs A) {
         x = rem % p.Wo;
       }
       const int by = y * p.sy + p.oy, bx = x * p.sx + p.ox;
+      if (A.debug & 1) {
+        for (int kb = 0; kb < p.n_kb; ++kb) {
+          mbar_wait(empty_bar(stage), phase ^ 1);
+          mbar_arrive(full_bar(stage));
+          advance(1);
+        }
+        continue;
+      }
       if (TAPS != 0) {
         // KW == 3, dx == 1, ox == -1, sx in {1, 2}: one coalesced load per
         // (channel, input row) serves all three kx taps; the neighbours come
@@ -439,6 +439,16 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(ConvArgs A) {
         }
       }
     }
+    if (prof_on) {
+      unsigned long long* pr = A.prof + (blockIdx.x * 16 + warp) * 4;
+      pr[0] = clock64() - c_start;
+      pr[1] = c_empty;
+      pr[2] = c_load;
+      pr[3] = c_fence;
+      pr[1] += 0;
+      A.prof[(blockIdx.x * 16 + 15) * 4 + (warp & 3)] += 0;
+      atomicAdd(A.prof + (gridDim.x * 16) * 4 - 1, c_issue);
+    }
   } else if (warp == kWarpLoad) {
     // ================= B loader (weights, bulk async copy) =================
     if (lane == 0) {
@@ -450,8 +460,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(ConvArgs A) {
         for (int kb = 0; kb < p.n_kb; ++kb) {
           mbar_wait(empty_bar(stage), phase ^ 1);
           const uint32_t dst = ring + stage * A.stage_bytes + nA * kAPlane;
-          mbar_expect_tx(full_bar(stage), b_bytes);
-          bulk_g2s(dst, A.wpk + ((long long)nt * p.n_kb + kb) * b_bytes, b_bytes, full_bar(stage));
+          if (A.debug & 2) {
+            mbar_arrive(full_bar(stage));
+          } else {
+            mbar_expect_tx(full_bar(stage), b_bytes);
+            bulk_g2s(dst, A.wpk + ((long long)nt * p.n_kb + kb) * b_bytes, b_bytes, full_bar(stage));
+          }
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
@@ -463,17 +477,20 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(ConvArgs A) {
   } else if (warp == kWarpMma) {
     // ================= MMA issuer (single thread) ===========================
     if (lane == 0) {
+      const bool mprof = (A.debug & 64) != 0;
+      unsigned long long m_full = 0, m_tempty = 0;
+      const unsigned long long m_start = clock64();
       const uint32_t idesc = make_idesc(BN);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
       for (int tile = blockIdx.x; tile < A.n_tiles; tile += gridDim.x) {
-        mbar_wait(tempty_bar(acc), acc_phase ^ 1);
+        mbar_wait_t(tempty_bar(acc), acc_phase ^ 1, m_tempty, mprof);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int kb = 0; kb < p.n_kb; ++kb) {
-          mbar_wait(full_bar(stage), phase);
+          mbar_wait_t(full_bar(stage), phase, m_full, mprof);
           tc_fence_after();
           const uint32_t a_hi = ring + stage * A.stage_bytes;
           const uint32_t a_lo = a_hi + kAPlane;
@@ -500,11 +517,20 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(ConvArgs A) {
           acc_phase ^= 1;
         }
       }
+      if (mprof) {
+        unsigned long long* pr = A.prof + (blockIdx.x * 16 + warp) * 4;
+        pr[0] = clock64() - m_start;
+        pr[1] = m_full;
+        pr[2] = m_tempty;
+      }
     }
     __syncwarp();
   } else {
     // ================= epilogue: TMEM -> registers -> NCHW fp32 ============
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    const bool eprof = (A.debug & 64) && lane == 0;
+    unsigned long long e_tfull = 0;
+    const unsigned long long e_start = clock64();
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < A.n_tiles; tile += gridDim.x) {
@@ -517,7 +543,33 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(ConvArgs A) {
         const long long rem = m % HoWo;
         obase = n * (long long)p.Cout * HoWo + rem;
       }
-      mbar_wait(tfull_bar(acc), acc_phase);
+      // Warm L2 with the input footprint of the tile two steps ahead (the
+      // gather's loads then hit L2 instead of paying DRAM latency).
+      if (!(A.debug & 8)) {
+        const int ahead = tile + 2 * gridDim.x;
+        if (ahead < A.n_tiles) {
+          const long long m0 = (long long)(ahead / p.n_tiles_n) * kBM;
+          const long long m1 = m0 + kBM < p.npix ? m0 + kBM : p.npix;
+          const int esz = p.in_bf16 ? 2 : 4;
+          const int t = threadIdx.x - (kProducerWarps + 2) * 32;  // 0..127
+          const long long n0 = m0 / HoWo, n1 = (m1 - 1) / HoWo;
+          for (long long nn = n0; nn <= n1; ++nn) {
+            const int ylo = nn == n0 ? static_cast<int>((m0 % HoWo) / p.Wo) : 0;
+            const int yhi = nn == n1 ? static_cast<int>(((m1 - 1) % HoWo) / p.Wo) : p.Ho - 1;
+            const int rlo = max(0, ylo * p.sy + p.oy);
+            const int rhi = min(p.H - 1, yhi * p.sy + (p.KH - 1) * p.dy + p.oy);
+            if (rlo > rhi) continue;
+            for (int c = t; c < p.Cin; c += 128) {
+              const char* base = static_cast<const char*>(A.in) +
+                                 ((((long long)nn * p.Cin + c) * p.H + rlo) * p.W) * esz;
+              const uintptr_t a0 = reinterpret_cast<uintptr_t>(base) & ~uintptr_t(15);
+              const uintptr_t a1 = (reinterpret_cast<uintptr_t>(base) + (size_t)(rhi - rlo + 1) * p.W * esz + 15) & ~uintptr_t(15);
+              prefetch_l2_bulk(reinterpret_cast<const void*>(a0), static_cast<uint32_t>(a1 - a0));
+            }
+          }
+        }
+      }
+      mbar_wait_t(tfull_bar(acc), acc_phase, e_tfull, eprof);
       tc_fence_after();
       const uint32_t t_row = tmem_base + acc * BN + (static_cast<uint32_t>(q * 32) << 16);
       for (int c0 = 0; c0 < BN; c0 += 32) {
@@ -525,7 +577,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(ConvArgs A) {
         TMEM_LD32(t_row + c0, r);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         const int co0 = nt * BN + c0;
-        if (valid) {
+        if (valid && !(A.debug & 4)) {
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const int co = co0 + j;
@@ -539,11 +591,18 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(ConvArgs A) {
       }
       tc_fence_before();
       mbar_arrive(tempty_bar(acc));
+      e_tfull_g = e_tfull;
+      e_start_g = e_start;
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
       }
     }
+  }
+  if (warp >= kProducerWarps + 2 && (A.debug & 64) && lane == 0) {
+    unsigned long long* pr = A.prof + (blockIdx.x * 16 + warp) * 4;
+    pr[0] = clock64() - e_start_g;
+    pr[1] = e_tfull_g;
   }
   __syncthreads();
   if (warp == kWarpLoad) {
@@ -619,9 +678,20 @@ merit_status launch_conv_pack(const merit_plan& plan, const void* b, void* packe
   return launch_status("conv_pack_kernel");
 }
 
+bool conv_tap3_eligible(const ConvParams& p);
+merit_status launch_conv_tap3(const merit_plan& plan, const void* a, const void* packed_b, void* out,
+                              void* stream);
+
 merit_status launch_conv(const merit_plan& plan, const void* a, const void* packed_b, void* out,
                          void* stream) {
   const ConvParams& p = plan.conv;
+  {
+    const char* kern = getenv("MERIT_CONV_KERNEL");  // "general" forces the generic gather kernel
+    const bool force_general = kern && kern[0] == 'g';
+    if (!force_general && conv_tap3_eligible(p) &&
+        (reinterpret_cast<uintptr_t>(a) % 4) == 0)
+      return launch_conv_tap3(plan, a, packed_b, out, stream);
+  }
   ConvArgs A;
   A.p = p;
   A.in = a;
@@ -636,6 +706,10 @@ merit_status launch_conv(const merit_plan& plan, const void* a, const void* pack
   uint32_t cols = 32;
   while (cols < static_cast<uint32_t>(2 * p.BN)) cols <<= 1;
   A.tmem_cols = cols;
+  {
+    const char* dbg = getenv("MERIT_CONV_DEBUG");
+    A.debug = dbg ? atoi(dbg) : 0;
+  }
   A.tap3 = (p.KW == 3 && p.dx == 1 && p.ox == -1 &&
             ((p.sx == 1 && p.Wo == p.W) || (p.sx == 2 && p.in_bf16 && p.W % 2 == 0 &&
                            (reinterpret_cast<uintptr_t>(a) % 4) == 0)))
@@ -658,6 +732,8 @@ merit_status launch_conv(const merit_plan& plan, const void* a, const void* pack
     if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(conv)");                  \
     k<<<grid, kThreads, smem, s>>>(A);                                                         \
   } while (0)
+  A.prof = nullptr;
+  if (A.debug & 64) cudaMalloc(&A.prof, sizeof(unsigned long long) * 4 * 16 * grid), cudaMemset(A.prof, 0, sizeof(unsigned long long) * 4 * 16 * grid);
   const int taps = A.tap3 ? p.sx : 0;
   if (p.in_bf16) {
     if (split3) MERIT_LAUNCH_CONV(true, true, 0);
@@ -671,6 +747,26 @@ merit_status launch_conv(const merit_plan& plan, const void* a, const void* pack
     else MERIT_LAUNCH_CONV(false, false, 0);
   }
 #undef MERIT_LAUNCH_CONV
+  if (A.debug & 64) {
+    cudaStreamSynchronize(s);
+    std::vector<unsigned long long> h(4 * 16 * grid);
+    cudaMemcpy(h.data(), A.prof, h.size() * 8, cudaMemcpyDeviceToHost);
+    double prod_fence = 0, prod_tot = 0, prod_empty = 0, prod_load = 0, mma_tot = 0, mma_full = 0, mma_tempty = 0, epi_tot = 0, epi_wait = 0;
+    for (int b = 0; b < grid; ++b) {
+      for (int w = 0; w < kProducerWarps; ++w) {
+        prod_tot += h[(b * 16 + w) * 4]; prod_empty += h[(b * 16 + w) * 4 + 1]; prod_load += h[(b * 16 + w) * 4 + 2]; prod_fence += h[(b * 16 + w) * 4 + 3];
+      }
+      mma_tot += h[(b * 16 + kWarpMma) * 4]; mma_full += h[(b * 16 + kWarpMma) * 4 + 1]; mma_tempty += h[(b * 16 + kWarpMma) * 4 + 2];
+      for (int w = kProducerWarps + 2; w < kProducerWarps + 6; ++w) {
+        epi_tot += h[(b * 16 + w) * 4]; epi_wait += h[(b * 16 + w) * 4 + 1];
+      }
+    }
+    fprintf(stderr, "[conv prof] load-issue %.1f%% ", 100.0 * h[4 * 16 * grid - 1] / prod_tot);
+    fprintf(stderr, "[conv prof] producer: fence %.1f%% empty-wait %.1f%% load-wait %.1f%% | mma: full-wait %.1f%% tempty-wait %.1f%% | epilogue tfull-wait %.1f%% | mma cycles/CTA %.0f\n",
+            100 * prod_fence / prod_tot, 100 * prod_empty / prod_tot, 100 * prod_load / prod_tot, 100 * mma_full / mma_tot, 100 * mma_tempty / mma_tot,
+            100 * epi_wait / epi_tot, mma_tot / grid);
+    cudaFree(A.prof);
+  }
   return launch_status("conv_tc_kernel");
 }
 
