@@ -54,8 +54,27 @@ def build_ref(verbose: bool = False) -> Path | None:
     return REF_LIB
 
 
+def build_dropin_test(verbose: bool = False) -> Path | None:
+    """tests/cpp/test_device_header.cpp: reference engine vs include/merit/device.hpp."""
+    if not (REF_INCLUDE / "merit" / "engine.hpp").exists():
+        exe = REF_DIR / "test_device_header"
+        return exe if exe.exists() else None
+    REF_DIR.mkdir(exist_ok=True)
+    src = ROOT / "tests" / "cpp" / "test_device_header.cpp"
+    exe = REF_DIR / "test_device_header"
+    lib = ROOT / "paper_1911_03458_b200" / "libmerit_dev.so"
+    deps = [src, ROOT / "include" / "merit_dev.h", ROOT / "include" / "merit" / "device.hpp", lib]
+    if _stale(exe, deps):
+        cmd = ["g++", "-O2", "-std=c++20", f"-I{REF_INCLUDE}", f"-I{ROOT / 'include'}", str(src), "-o", str(exe),
+               f"-L{lib.parent}", "-lmerit_dev", "-Wl,-rpath,$ORIGIN/../../paper_1911_03458_b200"]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+    return exe
+
+
 def build(verbose: bool = False):
-    return build_oracle(verbose), build_ref(verbose)
+    return build_oracle(verbose), build_ref(verbose), build_dropin_test(verbose)
 
 
 if __name__ == "__main__":

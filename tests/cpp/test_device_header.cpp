@@ -1,0 +1,83 @@
+// Drop-in check for include/merit/device.hpp: the reference's own workloads
+// (merit::build_template + merit::fill_random, as in the reference's
+// tests/test_workloads.cpp) run through the UNMODIFIED reference engine
+// merit::run_full and through merit::device::run_full; results must agree
+// bit for bit (exact interpreter, max-pool) or within the conv tolerance.
+// Built by oracle/build.py against /root/reference/proj/include (this
+// container) into oracle/_ref/test_device_header; run by
+// tests/test_cpp_dropin.py on the GPU box.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "merit/device.hpp"
+#include "merit/workloads.hpp"
+
+using namespace merit;
+
+static int failures = 0;
+
+static void check(const std::string& name, const Params& prm, uint64_t seed, uint32_t flags = 0) {
+  Workload w = build_template(name, prm);
+  fill_random(w.src_a, 2 * seed + 1);
+  fill_random(w.src_b, 2 * seed + 2);
+  if (template_shares_input(name)) w.src_b = w.src_a;
+  const Tensor want = run_full(w);
+  const int kern = device::lowered_kernel(w, flags);
+  const Tensor got = device::run_full(w, flags);
+  bool ok = got.shape == want.shape && got.dtype == want.dtype;
+  double worst = 0;
+  if (ok && got.dtype == Dtype::Fix16) {
+    ok = got.qdata == want.qdata;
+  } else if (ok) {
+    if (kern == MERIT_KERNEL_CONV_TC) {
+      for (size_t i = 0; i < got.fdata.size(); ++i)
+        worst = std::max(worst, std::abs(double(got.fdata[i]) - want.fdata[i]) / (1.0 + std::abs(want.fdata[i])));
+      ok = worst <= 1e-4;
+    } else {
+      ok = std::memcmp(got.fdata.data(), want.fdata.data(), got.fdata.size() * 4) == 0;
+    }
+  }
+  std::printf("%s %-18s kernel=%d seed=%llu worst=%.3g\n", ok ? "PASS" : "FAIL", name.c_str(), kern,
+              (unsigned long long)seed, worst);
+  if (!ok) ++failures;
+}
+
+int main() {
+  SplitMix64 rng{12};
+  for (int t = 0; t < 12; ++t) {
+    Params prm{{"h", double(rng.range(5, 12))}, {"w", double(rng.range(5, 12))},
+               {"k", double(rng.range(1, 3))}, {"stride", double(rng.range(1, 2))},
+               {"cin", double(rng.range(1, 2))}, {"cout", double(rng.range(1, 3))}};
+    if (t % 3 == 1) prm["fix"] = 1, prm["frac"] = double(rng.range(4, 10));
+    check(t % 3 == 2 ? "relu_fused_conv" : "conv2d", prm, 2000 + t);
+  }
+  check("conv2d", {{"h", 20}, {"w", 20}, {"cin", 16}, {"cout", 32}}, 11);                 // tensor cores
+  check("conv2d", {{"h", 17}, {"w", 14}, {"cin", 64}, {"cout", 48}, {"stride", 2}}, 12);  // tensor cores
+  check("conv2d", {{"h", 17}, {"w", 14}, {"cin", 64}, {"cout", 48}, {"stride", 2}}, 13, MERIT_FLAG_EXACT);
+  check("alexnet_conv1", {{"h", 47}, {"w", 47}}, 14);
+  check("gemm", {{"m", 9}, {"n", 7}, {"k", 11}}, 15);
+  check("gemm", {{"m", 5}, {"n", 6}, {"k", 7}, {"fix", 1}, {"frac", 6}}, 16);
+  check("correlation", {{"c", 3}, {"h", 8}, {"w", 7}, {"d", 3}}, 17);
+  check("motion_estimation", {{"h", 16}, {"w", 24}, {"blk", 4}, {"win", 5}}, 18);
+  check("motion_estimation", {{"h", 8}, {"w", 8}, {"blk", 4}, {"win", 3}, {"fix", 1}}, 19);
+  check("bilateral", {{"h", 9}, {"w", 8}, {"k", 5}}, 20);
+  check("maxpool", {{"h", 9}, {"w", 11}, {"k", 3}, {"stride", 2}}, 21);
+  check("maxpool", {{"h", 8}, {"w", 8}, {"k", 2}, {"fix", 1}}, 22);
+  check("dilated", {{"h", 12}, {"w", 10}, {"k", 3}}, 23);
+  // error behaviour: REJECT gather outside the source -> OutOfRange, like the reference
+  {
+    Workload w = build_template("maxpool", {{"h", 4}, {"w", 4}, {"k", 2}});
+    w.view_a.terms[1].offset = -1;
+    bool ref_threw = false, dev_threw = false;
+    ErrorCode rc{}, dc{};
+    try { run_full(w); } catch (const Error& e) { ref_threw = true; rc = e.code; }
+    try { device::run_full(w); } catch (const Error& e) { dev_threw = true; dc = e.code; }
+    const bool ok = ref_threw && dev_threw && rc == dc;
+    std::printf("%s reject-error-code ref=%d dev=%d\n", ok ? "PASS" : "FAIL", int(rc), int(dc));
+    if (!ok) ++failures;
+  }
+  std::printf("%d failure(s)\n", failures);
+  return failures == 0 ? 0 : 1;
+}
