@@ -26,12 +26,15 @@
 //  * Argmin: per-thread min over its D rows, then a shared-memory atomicMin
 //    on the packed key (sad << 16 | dy*WX + dx): lowest SAD, then lowest
 //    raster index — the tie-break BASELINE.json asks for.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace merit_dev {
 namespace {
 
-constexpr int kSadMaxThreads = 288;  // 2 CTAs/SM at <= 112 registers
+constexpr int kSadThreads = 256;     // 8 warps: 2 per SM sub-partition, 2 CTAs/SM at <= 128 regs
+constexpr int kSadMaxThreads = kSadThreads;
 
 __device__ __forceinline__ uint32_t vabsdiff4_acc(uint32_t a, uint32_t b, uint32_t c) {
   uint32_t d;
@@ -146,7 +149,7 @@ __device__ __forceinline__ void stage_tile(const SadLaunch& L, const uint8_t* __
 }
 
 template <int BLK, int D>
-__global__ void __maxnreg__(112)
+__global__ void __launch_bounds__(kSadThreads, 2)
 sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, void* __restrict__ out,
            int32_t* __restrict__ aux, SadLaunch L) {
   extern __shared__ __align__(16) uint32_t smem[];
@@ -154,11 +157,12 @@ sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, voi
   constexpr int BWW = BLK / 4;  // words per block row
   const int raw_words = L.R * L.rw;
   const int cur_words = L.TBX * BLK * BWW;
-  // --- shared memory carve-up: copies | raw[2] | cur[2] | keys
+  // --- shared memory carve-up: raw[2] | cur[2] | keys | counters
   uint32_t* copies = smem;
   uint32_t* raw0 = copies + 4 * L.CS;
   uint32_t* cur0 = raw0 + 2 * raw_words;
-  uint32_t* keys = cur0 + 2 * cur_words;
+  uint32_t* keys = cur0 + 2 * cur_words;   // per block: running argmin key
+  uint32_t* cnt = keys + L.TBX;             // per block: contributions so far
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
 
   // per-thread item: (block, dx); the thread walks all dy groups
@@ -167,6 +171,10 @@ sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, voi
   const int idx = item - ib * p.WX;
   const bool has_item = item < L.items;
 
+  if (threadIdx.x < L.TBX) {
+    keys[threadIdx.x] = 0xffffffffu;
+    cnt[threadIdx.x] = 0u;
+  }
   long long tile = blockIdx.x;
   int buf = 0;
   if (tile < L.n_tiles) {
@@ -191,7 +199,6 @@ sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, voi
         copies[3 * L.CS + o] = __byte_perm(lo, hi, 0x6543);
       }
     }
-    if (threadIdx.x < L.TBX) keys[threadIdx.x] = 0xffffffffu;
     __syncthreads();
     // prefetch the next tile into the other buffer while this one computes
     const long long next = tile + gridDim.x;
@@ -241,35 +248,47 @@ sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, voi
           }
         }
         const int dy0 = ig * D;
-        const long long obase = (blk_index * p.WY + dy0) * p.WX + idx;
+        const int nd = min(D, p.WY - dy0);
+        uint32_t key = (static_cast<uint32_t>(dy0) * p.WX + idx);
+        const uint32_t kstep = static_cast<uint32_t>(p.WX);
 #pragma unroll
         for (int d = 0; d < D; ++d) {
-          if (dy0 + d < p.WY) {
-            const uint32_t key = (acc[d] << 16) | static_cast<uint32_t>((dy0 + d) * p.WX + idx);
-            best = key < best ? key : best;
-            if (p.write_map) {
-              const long long o = obase + (long long)d * p.WX;
-              if (p.out_f32)
-                __stcs(static_cast<float*>(out) + o, static_cast<float>(acc[d]));
-              else
-                __stcs(static_cast<int32_t*>(out) + o, static_cast<int32_t>(acc[d]));
-            }
+          const uint32_t k = (acc[d] << 16) | (key + d * kstep);
+          if (d < nd) best = k < best ? k : best;
+        }
+        if (p.write_map) {
+          const long long obase = (blk_index * p.WY + dy0) * p.WX + idx;
+          if (p.out_f32) {
+            float* o = static_cast<float*>(out) + obase;
+#pragma unroll
+            for (int d = 0; d < D; ++d)
+              if (d < nd) __stcs(o + d * p.WX, static_cast<float>(acc[d]));
+          } else {
+            int32_t* o = static_cast<int32_t*>(out) + obase;
+#pragma unroll
+            for (int d = 0; d < D; ++d)
+              if (d < nd) __stcs(o + d * p.WX, static_cast<int32_t>(acc[d]));
           }
         }
       }
-      if (p.argmin) atomicMin(&keys[ib], best);
-    }
-    if (p.argmin) {
-      __syncthreads();
-      if (threadIdx.x < nb) {
-        const uint32_t key = keys[threadIdx.x];
-        const int k = static_cast<int>(key & 0xffffu);
-        const int dy = k / p.WX, dx = k - (k / p.WX) * p.WX;
-        const long long blk_index = (pair * p.BY + by) * (long long)p.BX + bx0 + threadIdx.x;
-        int32_t* a = aux + blk_index * 3;
-        a[0] = dy + p.oy - p.cy;
-        a[1] = dx + p.ox - p.cx;
-        a[2] = static_cast<int32_t>(key >> 16);
+      if (p.argmin) {
+        // Barrier-free per-block argmin: every (block, dx) thread folds its key
+        // in; the thread that arrives last writes the record and re-arms the
+        // slot for the next tile (the next tile's atomics follow the barrier at
+        // the top of the loop).
+        atomicMin(&keys[ib], best);
+        __threadfence_block();
+        if (atomicAdd(&cnt[ib], 1u) == static_cast<uint32_t>(p.WX - 1)) {
+          __threadfence_block();
+          const uint32_t key = atomicExch(&keys[ib], 0xffffffffu);
+          cnt[ib] = 0u;
+          const int k = static_cast<int>(key & 0xffffu);
+          const int dy = k / p.WX, dx = k - (k / p.WX) * p.WX;
+          int32_t* a = aux + blk_index * 3;
+          a[0] = dy + p.oy - p.cy;
+          a[1] = dx + p.ox - p.cx;
+          a[2] = static_cast<int32_t>(key >> 16);
+        }
       }
     }
   }
@@ -304,7 +323,7 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
   L.R = L.G * D + BLK - 1;
   L.span = L.TBX * BLK + p.WX - 1;
   L.Ww = (L.span + 3) / 4;
-  L.rw = (L.Ww + 1 + 3) / 4 * 4;  // raw rows padded to 16-byte chunks
+  L.rw = (L.Ww + 1 + 3) / 4 * 4;  // raw rows (+1 word for the shift) padded to 16-byte chunks
   L.CS = L.R * L.Ww;
   L.CS += ((8 - (L.CS % 32)) + 32) % 32;
   L.word_path = ((p.ox % 4) == 0 && (p.cx % 4) == 0 && (p.Wr % 4) == 0 && (p.Wc % 4) == 0 &&
@@ -312,7 +331,7 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
                     ? 1 : 0;
   L.vec_path = (L.word_path && (p.ox % 16) == 0 && (p.Wr % 16) == 0 && (BLK % 16) == 0 &&
                 (reinterpret_cast<uintptr_t>(ref) % 16) == 0) ? 1 : 0;
-  const size_t smem = 4ull * (4ull * L.CS + 2ull * L.R * L.rw + 2ull * L.TBX * BLK * (BLK / 4) + L.TBX);
+  const size_t smem = 4ull * (4ull * L.CS + 2ull * L.R * L.rw + 2ull * L.TBX * BLK * (BLK / 4) + 2ull * L.TBX);
   if (L.n_tiles == 0) return MERIT_OK;
   if (smem > 110 * 1024) return fail(MERIT_E_UNSUPPORTED_VIEW, "SAD footprint exceeds shared memory");
   auto kern = sad_kernel<BLK, D>;
@@ -332,7 +351,11 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
 // fits the thread budget.  Used by the lowering to decide eligibility.
 int sad_rows_per_thread(int BH, int WY, int WX) {
   if (WX > kSadMaxThreads || WY > 256) return 0;
-  if (BH == 16) return WY <= 33 ? 11 : 17;
+  if (BH == 16) {
+    const char* e = getenv("MERIT_SAD_D");  // tuning override: 11 or 33
+    if (WY <= 33) return (e && atoi(e) == 11) ? 11 : 33;
+    return 17;
+  }
   return WY <= 33 ? 11 : 22;
 }
 
@@ -345,6 +368,7 @@ merit_status launch_sad(const merit_plan& plan, const void* a, const void* b, vo
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int D = sad_rows_per_thread(p.BH, p.WY, p.WX);
   if (p.BH == 16) {
+    if (D == 33) return launch_sad_t<16, 33>(p, cur, ref, out, ax, s);
     if (D == 11) return launch_sad_t<16, 11>(p, cur, ref, out, ax, s);
     if (D == 17) return launch_sad_t<16, 17>(p, cur, ref, out, ax, s);
   } else {

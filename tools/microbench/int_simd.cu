@@ -46,7 +46,31 @@ double run(uint32_t* din, uint32_t* dout, int blocks, int iters) {
   return instr / (ms * 1e-3);  // thread-instructions per second
 }
 
-int main() {
+template <int MODE>
+double run_occ(uint32_t* din, uint32_t* dout, int blocks, int threads, int iters) {
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  kbench<MODE><<<blocks, threads>>>(din, dout, iters);
+  cudaEventRecord(e0);
+  kbench<MODE><<<blocks, threads>>>(din, dout, iters);
+  cudaEventRecord(e1); cudaEventSynchronize(e1);
+  float ms; cudaEventElapsedTime(&ms, e0, e1);
+  return double(blocks) * threads * iters * 16 * 8 / (ms * 1e-3);
+}
+
+int main(int argc, char** argv) {
+  if (argc > 1) {  // occupancy sweep: warps per SM -> VABSDIFF4 instr/s
+    cudaDeviceProp p; cudaGetDeviceProperties(&p, 0);
+    uint32_t *din, *dout; cudaMalloc(&din, 4096 * 4); cudaMemset(din, 0x5a, 4096 * 4);
+    cudaMalloc(&dout, 148 * 64 * 32 * 4 * 8);
+    for (int wps : {4, 8, 12, 16, 24, 32, 64}) {
+      const int threads = wps >= 8 ? 256 : wps * 32;
+      const int bps = wps * 32 / threads;
+      double v = run_occ<0>(din, dout, p.multiProcessorCount * bps, threads, 1000);
+      printf("{\"warps_per_sm\": %d, \"vabsdiff4_instr_per_s\": %.4e, \"frac_of_64_lanes\": %.3f}\n", wps, v,
+             v / (p.multiProcessorCount * 1.965e9 * 64));
+    }
+    return 0;
+  }
   int dev = 0; cudaDeviceProp p; cudaGetDeviceProperties(&p, dev);
   int clk = 0; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, dev);
   uint32_t *din, *dout; cudaMalloc(&din, 4096 * 4); cudaMemset(din, 0x5a, 4096 * 4);
