@@ -26,6 +26,14 @@ inline int num_sms() {
   return sms;
 }
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (device, kernel,
+// size): keeps the per-launch host path short for microsecond-scale kernels.
+cudaError_t set_smem_attr_impl(const void* fn, cudaFuncAttribute attr, int bytes);
+template <typename K>
+inline cudaError_t set_smem_attr(K kernel, cudaFuncAttribute attr, int bytes) {
+  return set_smem_attr_impl(reinterpret_cast<const void*>(kernel), attr, bytes);
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

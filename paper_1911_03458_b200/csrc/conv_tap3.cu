@@ -515,8 +515,8 @@ merit_status launch_conv_tap3(const merit_plan& plan, const void* a, const void*
 #define MERIT_LAUNCH_TAP3(INB, S3, SXV)                                                        \
   do {                                                                                        \
     auto k = conv_tap3_kernel<INB, S3, SXV>;                                                  \
-    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);      \
-    if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(conv_tap3)");            \
+    e = set_smem_attr(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);      \
+    if (e != cudaSuccess) return cuda_check(e, "set_smem_attr(conv_tap3)");            \
     k<<<grid, kThreads, smem, s>>>(A);                                                        \
   } while (0)
   if (p.sx == 2) MERIT_LAUNCH_TAP3(true, false, 2);

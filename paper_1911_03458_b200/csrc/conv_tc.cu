@@ -728,8 +728,8 @@ merit_status launch_conv(const merit_plan& plan, const void* a, const void* pack
 #define MERIT_LAUNCH_CONV(INB, S3, TP)                                                         \
   do {                                                                                         \
     auto k = conv_tc_kernel<INB, S3, TP>;                                                      \
-    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);       \
-    if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(conv)");                  \
+    e = set_smem_attr(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);       \
+    if (e != cudaSuccess) return cuda_check(e, "set_smem_attr(conv)");                  \
     k<<<grid, kThreads, smem, s>>>(A);                                                         \
   } while (0)
   A.prof = nullptr;

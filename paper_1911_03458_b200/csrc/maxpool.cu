@@ -49,6 +49,11 @@ __global__ void maxpool_generic_kernel(const float* __restrict__ in, float* __re
   }
 }
 
+template <int RB>
+__device__ __forceinline__ void maxpool3s2_item(const float* __restrict__ in, float* __restrict__ out,
+                                                const MaxpoolParams& p, int nseg, int nband,
+                                                long long wg);
+
 // Fast path for 3x3 / stride 2 / offset -1 / CLAMP with Ho = H/2, Wo = W/2,
 // W % 4 == 0.  A warp owns one plane, RB output rows and a 128-column input
 // segment: lane l holds input columns 4l..4l+3 of every input row it needs as
@@ -57,10 +62,22 @@ __global__ void maxpool_generic_kernel(const float* __restrict__ in, float* __re
 // 64-bit store.  Every input row is read once per band (one shared row per
 // band boundary).
 template <int RB>
-__global__ void __launch_bounds__(256, 3) maxpool3s2_kernel(const float* __restrict__ in,
+__global__ void __launch_bounds__(128, 6) maxpool3s2_kernel(const float* __restrict__ in,
                                                          float* __restrict__ out, MaxpoolParams p,
-                                                         int nseg, int nband) {
-  const long long wg = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+                                                         int nseg, int nband, long long n_items,
+                                                         int per_warp) {
+  // Each warp owns `per_warp` consecutive (plane, band, segment) items; the
+  // grid is sized so that every warp is resident at once and all warps carry
+  // the same number of items (no partial second wave).
+  const long long w0 = ((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5) * per_warp;
+  for (long long wg = w0; wg < w0 + per_warp && wg < n_items; ++wg)
+    maxpool3s2_item<RB>(in, out, p, nseg, nband, wg);
+}
+
+template <int RB>
+__device__ __forceinline__ void maxpool3s2_item(const float* __restrict__ in, float* __restrict__ out,
+                                                const MaxpoolParams& p, int nseg, int nband,
+                                                long long wg) {
   const int lane = threadIdx.x & 31;
   const int seg = static_cast<int>(wg % nseg);
   const long long t = wg / nseg;
@@ -119,6 +136,111 @@ __global__ void __launch_bounds__(256, 3) maxpool3s2_kernel(const float* __restr
   }
 }
 
+
+// Streaming path for the same shape: a band's input rows are contiguous in
+// memory, so one cp.async.bulk (TMA engine) per band moves them into a
+// shared-memory ring NS bands deep; warps compute from shared memory.  Bytes
+// in flight no longer cost registers, so HBM stays busy.
+constexpr int kMpStages = 4;
+constexpr int kMpRB = 8;   // output rows per band
+constexpr int kMpThreads = 128;
+
+__device__ __forceinline__ void mp_mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mp_mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "LAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE;\n\t"
+      "bra LAB_WAIT;\n\t"
+      "DONE:\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(kMpThreads) maxpool3s2_bulk_kernel(const float* __restrict__ in,
+                                                                     float* __restrict__ out,
+                                                                     MaxpoolParams p, int nband,
+                                                                     long long n_items) {
+  extern __shared__ __align__(128) float sbuf[];
+  const int H = p.H, W = p.W, Ho = p.Ho, Wo = p.Wo;
+  const int rows_max = 2 * kMpRB + 1;
+  const int stage_floats = rows_max * W;
+  __shared__ __align__(8) unsigned long long bars[kMpStages];
+  const uint32_t bar0 = smem_u32(&bars[0]);
+  const uint32_t buf0 = smem_u32(sbuf);
+  auto rows_of = [&](long long item, int& r0, int& nr) {
+    const int band = static_cast<int>(item % nband);
+    const int y0 = band * kMpRB;
+    const int lo = max(0, 2 * y0 - 1);
+    const int hi = min(H - 1, 2 * (y0 + kMpRB) - 1);
+    r0 = lo;
+    nr = hi - lo + 1;
+  };
+  auto issue = [&](long long item, int st) {
+    int r0, nr;
+    rows_of(item, r0, nr);
+    const long long plane = item / nband;
+    const float* src = in + (plane * H + r0) * (long long)W;
+    const uint32_t bytes = static_cast<uint32_t>(nr) * W * 4u;
+    const uint32_t bar = bar0 + 8u * st;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(buf0 + 4u * st * stage_floats), "l"(src), "r"(bytes), "r"(bar) : "memory");
+  };
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kMpStages; ++i) mp_mbar_init(bar0 + 8u * i, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const long long first = blockIdx.x;
+  const long long step = gridDim.x;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < kMpStages; ++i)
+      if (first + i * step < n_items) issue(first + i * step, i);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int it = 0;
+  for (long long item = first; item < n_items; item += step, ++it) {
+    const int st = it % kMpStages;
+    const uint32_t parity = (it / kMpStages) & 1;
+    mp_mbar_wait(bar0 + 8u * st, parity);
+    int r0, nr;
+    rows_of(item, r0, nr);
+    const long long plane = item / nband;
+    const int y0 = static_cast<int>(item % nband) * kMpRB;
+    const float* sb = sbuf + st * stage_floats;
+    // warp w computes output rows y0 + w, y0 + w + 4 (RB = 8, 4 warps)
+    for (int yy = warp; yy < kMpRB; yy += kMpThreads / 32) {
+      const int y = y0 + yy;
+      if (y >= Ho) break;
+      for (int c4 = lane; c4 * 4 < W; c4 += 32) {
+        const int col0 = c4 * 4;
+        float r0v = p.init, r1v = p.init;
+#pragma unroll
+        for (int ky = 0; ky < 3; ++ky) {
+          int iy = 2 * y - 1 + ky;
+          iy = iy < 0 ? 0 : (iy > H - 1 ? H - 1 : iy);
+          const float* row = sb + (iy - r0) * W;
+          const float4 q = *reinterpret_cast<const float4*>(row + col0);
+          const float l = col0 == 0 ? q.x : row[col0 - 1];
+          r0v = fold_max(r0v, l);
+          r0v = fold_max(r0v, q.x);
+          r0v = fold_max(r0v, q.y);
+          r1v = fold_max(r1v, q.y);
+          r1v = fold_max(r1v, q.z);
+          r1v = fold_max(r1v, q.w);
+        }
+        *reinterpret_cast<float2*>(out + (plane * Ho + y) * (long long)Wo + col0 / 2) =
+            make_float2(post_op(r0v, p.post), post_op(r1v, p.post));
+      }
+    }
+    __syncthreads();  // everyone is done with stage st: refill it
+    if (threadIdx.x == 0 && item + kMpStages * step < n_items) issue(item + kMpStages * step, st);
+  }
+}
+
 }  // namespace
 
 merit_status launch_maxpool(const merit_plan& plan, const void* a, void* out, void* stream) {
@@ -130,14 +252,32 @@ merit_status launch_maxpool(const merit_plan& plan, const void* a, void* out, vo
   if (total == 0) return MERIT_OK;
   const bool aligned = (reinterpret_cast<uintptr_t>(in) % 16 == 0) &&
                        (reinterpret_cast<uintptr_t>(out) % 8 == 0);
-  if (p.fast && aligned) {
+  if (p.fast && aligned && p.W % 4 == 0) {
+    const int nband = (p.Ho + kMpRB - 1) / kMpRB;
+    const long long items = p.planes * nband;
+    const size_t smem = (size_t)kMpStages * (2 * kMpRB + 1) * p.W * 4;
+    if (smem <= 200 * 1024) {
+      cudaError_t e = set_smem_attr(maxpool3s2_bulk_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return cuda_check(e, "set_smem_attr(maxpool)");
+      int per_sm = static_cast<int>((220 * 1024) / (smem + 1024));
+      if (per_sm > 8) per_sm = 8;
+      if (per_sm < 1) per_sm = 1;
+      long long grid = (long long)num_sms() * per_sm;
+      if (grid > items) grid = items;
+      maxpool3s2_bulk_kernel<<<static_cast<unsigned>(grid), kMpThreads, smem, s>>>(in, o, p, nband, items);
+      return launch_status("maxpool3s2_bulk_kernel");
+    }
     constexpr int RB = 4;
     const int nseg = (p.W + 127) / 128;
-    const int nband = (p.Ho + RB - 1) / RB;
-    const long long warps = p.planes * nband * nseg;
-    const long long threads = warps * 32;
-    const long long blocks = (threads + 255) / 256;
-    maxpool3s2_kernel<RB><<<static_cast<unsigned>(blocks), 256, 0, s>>>(in, o, p, nseg, nband);
+    const int nband4 = (p.Ho + RB - 1) / RB;
+    const long long items4 = p.planes * nband4 * nseg;
+    const long long resident = (long long)num_sms() * 6 * 4;  // 6 CTAs x 4 warps per SM
+    const int per_warp = static_cast<int>((items4 + resident - 1) / resident);
+    const long long warps = (items4 + per_warp - 1) / per_warp;
+    const long long blocks = (warps + 3) / 4;
+    maxpool3s2_kernel<RB><<<static_cast<unsigned>(blocks), 128, 0, s>>>(in, o, p, nseg, nband4, items4,
+                                                                      per_warp);
     return launch_status("maxpool3s2_kernel");
   }
   const int threads = 256;

@@ -335,9 +335,9 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
   if (L.n_tiles == 0) return MERIT_OK;
   if (smem > 110 * 1024) return fail(MERIT_E_UNSUPPORTED_VIEW, "SAD footprint exceeds shared memory");
   auto kern = sad_kernel<BLK, D>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = set_smem_attr(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
-  if (e != cudaSuccess) return cuda_check(e, "cudaFuncSetAttribute(sad)");
+  if (e != cudaSuccess) return cuda_check(e, "set_smem_attr(sad)");
   const int threads = (L.items + 31) / 32 * 32;
   long long grid = 2LL * num_sms();
   if (grid > L.n_tiles) grid = L.n_tiles;
