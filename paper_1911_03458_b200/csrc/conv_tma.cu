@@ -1,0 +1,460 @@
+// K3c — stride-2, 3-wide bf16 convolution with the MERIT gather done by the
+// TMA engine (the C4 shape: NCHW, KW = 3, ox = -1, sx = 2).
+//
+// The view's strided row term (y*2 + ky - 1) is a TMA tensor-map traversal
+// stride on the H dimension, its zero padding is the TMA out-of-bounds fill,
+// and one cp.async.bulk.tensor per (tile, ky, 64-channel block) lands the raw
+// rows [c][4 rows][W] in a shared-memory ring several groups deep — no
+// registers are spent on bytes in flight and no load instructions are issued
+// by the SM.  Eight repack warps turn the raw rows into the two UMMA A planes
+// (tap 1 = even columns, tap 2 = odd columns; tap 0 is tap 2 read one slot row
+// earlier, the shifted-view trick of conv_tap3.cu), and the MMA / epilogue
+// roles are those of conv_tap3.cu.
+//
+// Slots: 32 per output row (4 leading pads + Wo = 28), a tile = 128 slots =
+// 4 output rows of one image, so every tile starts on a pad slot and tap 0
+// never needs a guard row.
+//
+// Warps: 0-7 repack, 8 B loader + TMEM alloc, 9 MMA, 10-13 epilogue, 14 TMA.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "tc_common.cuh"
+
+namespace merit_dev {
+namespace {
+
+using namespace tc;
+
+constexpr int kRepackWarps = 8;
+constexpr int kRepackers = kRepackWarps * 32;
+constexpr int kWarpB = 8, kWarpMma = 9, kWarpEpi0 = 10, kWarpTma = 14;
+constexpr int kThreads = 15 * 32;
+constexpr int kMaxRing = 8;
+constexpr uint32_t kPlane = kAPlane;           // 16 KB
+constexpr uint32_t kASlot = 2 * kPlane;        // [tap2][tap1]
+constexpr int kEpiCo = 32;                     // output channels per TMA store
+
+struct TmaArgs {
+  ConvParams p;
+  const uint8_t* wpk;
+  float* out;
+  int tiles_per_img;   // Ho / 4
+  int n_tiles;
+  int n_groups;        // KH * CB
+  uint32_t raw_bytes;  // W * 4 rows * 32 ch * 2 (half a 64-channel k-block)
+  uint32_t b_bytes;
+  int nr, na, nb;
+  uint32_t tmem_cols;
+  uint32_t stage_bytes;  // epilogue staging: kEpiCo co x 4 rows x Wo fp32
+  unsigned long long* prof;  // MERIT_CONV_DEBUG & 64: per-warp [total, wait1, wait2, wait3]
+  int debug;
+};
+
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, int x, int y, int c,
+                                            int n, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(c), "r"(n), "r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void twait(uint32_t bar, uint32_t par, unsigned long long& acc, bool on) {
+  if (on) {
+    const unsigned long long t0 = clock64();
+    mbar_wait(bar, par);
+    acc += clock64() - t0;
+  } else {
+    mbar_wait(bar, par);
+  }
+}
+
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, uint32_t src, int x, int y, int c, int n) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(src), "r"(x), "r"(y), "r"(c), "r"(n)
+               : "memory");
+}
+
+__global__ void __maxnreg__(128)  // 15 warps: <= 4 per SM sub-partition x 128 regs
+conv_tma_kernel(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap out_map,
+                TmaArgs A) {
+  extern __shared__ uint8_t smem_raw[];
+  const ConvParams& p = A.p;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  // B first: tap 0's view of A row 0 starts 128 B before the tap-2 plane,
+  // which must be a valid shared address (its value only feeds the pad slot
+  // of output row 0, which is never stored).
+  const uint32_t bring = base;                          // nb x b_bytes
+  const uint32_t aring = bring + A.nb * A.b_bytes;      // na x kASlot
+  const uint32_t rring = aring + A.na * kASlot;         // nr x raw_bytes
+  const uint32_t ering = rring + A.nr * A.raw_bytes;    // 2 x stage_bytes (epilogue)
+  const uint32_t bars = (ering + 2 * A.stage_bytes + 7u) & ~7u;
+  auto r_full = [&](int s) { return bars + 8u * s; };
+  auto r_empty = [&](int s) { return bars + 8u * (kMaxRing + s); };
+  auto a_full = [&](int s) { return bars + 8u * (2 * kMaxRing + s); };
+  auto a_empty = [&](int s) { return bars + 8u * (3 * kMaxRing + s); };
+  auto b_full = [&](int s) { return bars + 8u * (4 * kMaxRing + s); };
+  auto b_empty = [&](int s) { return bars + 8u * (5 * kMaxRing + s); };
+  auto tfull = [&](int a) { return bars + 8u * (6 * kMaxRing + a); };
+  auto tempty = [&](int a) { return bars + 8u * (6 * kMaxRing + 2 + a); };
+  const uint32_t tmem_slot = bars + 8u * (6 * kMaxRing + 4);
+  volatile uint32_t* tmem_slot_ptr =
+      reinterpret_cast<volatile uint32_t*>(smem_raw + (tmem_slot - smem_u32(smem_raw)));
+  auto tap2_plane = [&](int s) { return aring + s * kASlot; };
+  auto tap1_plane = [&](int s) { return aring + s * kASlot + kPlane; };
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < A.nr; ++s) {
+      mbar_init(r_full(s), 1);
+      mbar_init(r_empty(s), kRepackers / 2);  // one half of the repack warps
+    }
+    for (int s = 0; s < A.na; ++s) {
+      mbar_init(a_full(s), kRepackers);
+      mbar_init(a_empty(s), 1);
+    }
+    for (int s = 0; s < A.nb; ++s) {
+      mbar_init(b_full(s), 1);
+      mbar_init(b_empty(s), 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull(a), 1);
+      mbar_init(tempty(a), 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == kWarpB) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot),
+                 "r"(A.tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot_ptr;
+  const int BN = p.BN;
+  const int W = p.W;
+  const bool pon = (A.debug & 64) && lane == 0;
+  unsigned long long w1 = 0, w2 = 0, w3 = 0;
+  const unsigned long long t_start = clock64();
+
+  if (warp == kWarpTma) {
+    // ============ raw-row loader: the MERIT gather on the TMA engine ======
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&in_map)) : "memory");
+      int st = 0;
+      uint32_t ph = 0;
+      for (int tile = blockIdx.x; tile < A.n_tiles; tile += gridDim.x) {
+        const int mt = tile / p.n_tiles_n;
+        const int n = mt / A.tiles_per_img;
+        const int y0 = (mt - n * A.tiles_per_img) * 4;
+        for (int g = 0; g < A.n_groups; ++g) {
+          const int ky = g / p.CB, cb = g - (g / p.CB) * p.CB;
+          for (int h = 0; h < 2; ++h) {
+            twait(r_empty(st), ph ^ 1, w1, pon);
+            mbar_expect_tx(r_full(st), A.raw_bytes);
+            // rows 2*y0 + ky - 1 + {0, 2, 4, 6} (traversal stride 2), all W
+            // columns, 32 channels; out-of-range rows / channels read as zero.
+            tma_load_4d(rring + st * A.raw_bytes, &in_map, 0, y0 * p.sy + ky * p.dy + p.oy, cb * 64 + 32 * h,
+                        n, r_full(st));
+            if (++st == A.nr) { st = 0; ph ^= 1; }
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp < kRepackWarps) {
+    // ============ repack: raw [c][r][W] -> UMMA K-major planes =============
+    // warp w: channels 8w..8w+7 (chunk column w of every A row); lane l:
+    // output column x = l - 4 (lanes 0-3 are the row's pad slots) of all four
+    // output rows, i.e. A rows 32k + l, k = 0..3.  One 32-bit shared load per
+    // (channel, row) brings input columns 2x, 2x+1 = taps 1 and 2; in step k
+    // the 8 lanes of an STS.128 phase write 8 consecutive rows, so the 128-B
+    // swizzle spreads them over all banks.
+    const int w = warp, l = lane;
+    const int x = l - 4;
+    const bool pad = x < 0;
+    const uint32_t rowbytes = static_cast<uint32_t>(W) * 2u;
+    // raw entries alternate channel halves: warps 0-3 consume the even
+    // entries (channels 0-31 of the k-block), warps 4-7 the odd ones.  nr is
+    // even, so every slot belongs to one half and its mbarrier phases follow
+    // that half's program order (an odd ring would let the halves' phases
+    // alias).
+    const uint32_t roff = static_cast<uint32_t>(8 * (w & 3)) * 4u * rowbytes + (pad ? 0u : 4u * x);
+    int rs = w >> 2, as = 0;
+    uint32_t rph = 0, aph = 0;
+    for (int tile = blockIdx.x; tile < A.n_tiles; tile += gridDim.x) {
+      for (int g = 0; g < A.n_groups; ++g) {
+        twait(r_full(rs), rph, w1, pon);
+        uint32_t v[4][8];  // [row k][channel c]: (tap1 | tap2 << 16)
+        const uint32_t src = rring + rs * A.raw_bytes + roff;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            uint32_t t = 0u;
+            if (!pad)
+              asm volatile("ld.shared.u32 %0, [%1];" : "=r"(t) : "r"(src + (c * 4u + k) * rowbytes));
+            v[k][c] = t;
+          }
+        mbar_arrive(r_empty(rs));
+        rs += 2;
+        while (rs >= A.nr) { rs -= A.nr; rph ^= 1; }
+        twait(a_empty(as), aph ^ 1, w2, pon);
+        const uint32_t p2 = tap2_plane(as), p1 = tap1_plane(as);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int row = 32 * k + l;
+          const uint32_t off = (row >> 3) * 1024u + (row & 7) * 128u + (((uint32_t)w ^ (uint32_t)(row & 7)) << 4);
+          const uint32_t* wv = v[k];
+          st_shared_v4(p1 + off, __byte_perm(wv[0], wv[1], 0x5410), __byte_perm(wv[2], wv[3], 0x5410),
+                       __byte_perm(wv[4], wv[5], 0x5410), __byte_perm(wv[6], wv[7], 0x5410));
+          st_shared_v4(p2 + off, __byte_perm(wv[0], wv[1], 0x7632), __byte_perm(wv[2], wv[3], 0x7632),
+                       __byte_perm(wv[4], wv[5], 0x7632), __byte_perm(wv[6], wv[7], 0x7632));
+        }
+        fence_proxy_async();
+        mbar_arrive(a_full(as));
+        if (++as == A.na) { as = 0; aph ^= 1; }
+      }
+    }
+  } else if (warp == kWarpB) {
+    // ============ B loader =====================================================
+    if (lane == 0) {
+      int st = 0;
+      uint32_t ph = 0;
+      for (int tile = blockIdx.x; tile < A.n_tiles; tile += gridDim.x) {
+        const int nt = tile % p.n_tiles_n;
+        for (int kb = 0; kb < p.n_kb; ++kb) {
+          twait(b_empty(st), ph ^ 1, w1, pon);
+          mbar_expect_tx(b_full(st), A.b_bytes);
+          bulk_g2s(bring + st * A.b_bytes, A.wpk + ((long long)nt * p.n_kb + kb) * A.b_bytes, A.b_bytes,
+                   b_full(st));
+          if (++st == A.nb) { st = 0; ph ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == kWarpMma) {
+    // ============ MMA issuer ===================================================
+    if (lane == 0) {
+      const uint32_t idesc = make_idesc(BN);
+      int as = 0, bs = 0, acc = 0;
+      uint32_t aph = 0, bph = 0, acc_phase = 0;
+      for (int tile = blockIdx.x; tile < A.n_tiles; tile += gridDim.x) {
+        twait(tempty(acc), acc_phase ^ 1, w3, pon);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int g = 0; g < A.n_groups; ++g) {
+          twait(a_full(as), aph, w1, pon);
+          tc_fence_after();
+          for (int kx = 0; kx < 3; ++kx) {
+            twait(b_full(bs), bph, w2, pon);
+            tc_fence_after();
+            // tap 0 = tap-2 plane one slot row earlier; tap 1; tap 2
+            const uint32_t a0 = kx == 1 ? tap1_plane(as) : tap2_plane(as) - (kx == 0 ? 128u : 0u);
+            const uint32_t b0 = bring + bs * A.b_bytes;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              const uint32_t accum = (g > 0 || kx > 0 || k > 0) ? 1u : 0u;
+              tc_mma(d_tmem, sw128_desc(a0 + 32 * k), sw128_desc(b0 + 32 * k), idesc, accum);
+            }
+            tc_commit(b_empty(bs));
+            if (++bs == A.nb) { bs = 0; bph ^= 1; }
+          }
+          tc_commit(a_empty(as));
+          if (++as == A.na) { as = 0; aph ^= 1; }
+        }
+        tc_commit(tfull(acc));
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+    __syncwarp();
+  } else if (warp >= kWarpEpi0 && warp < kWarpEpi0 + 4) {
+    // ============ epilogue: TMEM -> smem [co][4][Wo] -> TMA store =========
+    // Warp quadrant qd holds slot rows 32qd..32qd+31 = output row y0 + qd,
+    // lane = x + 4.  Each kEpiCo-channel chunk is staged in shared memory and
+    // written to NCHW by ONE tensor store (box Wo x 4 x kEpiCo) issued by one
+    // thread; TMEM is released right after the last tcgen05.ld of the tile.
+    const int qd = warp & 3;
+    const int x = lane - 4;
+    const bool valid = x >= 0 && x < p.Wo;
+    const bool leader = warp == kWarpEpi0 && lane == 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    int sb = 0;  // staging buffer
+    for (int tile = blockIdx.x; tile < A.n_tiles; tile += gridDim.x) {
+      const int mt = tile / p.n_tiles_n, nt = tile % p.n_tiles_n;
+      const int n = mt / A.tiles_per_img;
+      const int y0 = (mt - n * A.tiles_per_img) * 4;
+      twait(tfull(acc), acc_phase, w1, pon);
+      tc_fence_after();
+      const uint32_t t_row = tmem_base + acc * BN + (static_cast<uint32_t>(qd * 32) << 16);
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t rr[32];
+        TMEM_LD32(t_row + c0, rr);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (c0 + 32 >= BN) {  // accumulator drained: let the MMA reuse it
+          tc_fence_before();
+          mbar_arrive(tempty(acc));
+        }
+#pragma unroll
+        for (int hh = 0; hh < 32 / kEpiCo; ++hh) {
+          // staging buffer sb must no longer be read by an in-flight store
+          if (leader) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          const uint32_t sbase = ering + sb * A.stage_bytes;
+          if (valid) {
+#pragma unroll
+            for (int j = 0; j < kEpiCo; ++j) {
+              float v = __uint_as_float(rr[kEpiCo * hh + j]);
+              v = p.post == POST_RELU ? ((v < 0.f) ? 0.f : v) : __fadd_rn(v, 0.f);
+              asm volatile("st.shared.f32 [%0], %1;" ::"r"(sbase + 4u * ((j * 4 + qd) * p.Wo + x)), "f"(v)
+                           : "memory");
+            }
+          }
+          fence_proxy_async();
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (leader && nt * BN + c0 + kEpiCo * hh < p.Cout) {
+            tma_store_4d(&out_map, sbase, 0, y0, nt * BN + c0 + kEpiCo * hh, n);
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          }
+          sb ^= 1;
+        }
+      }
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+    if (leader) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  }
+  if (pon) {
+    unsigned long long* pr = A.prof + (blockIdx.x * 16 + warp) * 4;
+    pr[0] = clock64() - t_start; pr[1] = w1; pr[2] = w2; pr[3] = w3;
+  }
+  __syncthreads();
+  if (warp == kWarpB) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(A.tmem_cols)
+                 : "memory");
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+}  // namespace
+
+bool conv_tma_eligible(const ConvParams& p, const void* a) {
+  const char* e = getenv("MERIT_CONV_TMA");
+  if (e && e[0] == '0') return false;
+  return p.KW == 3 && p.dx == 1 && p.ox == -1 && p.sx == 2 && p.in_bf16 && p.split == 1 &&
+         p.W % 8 == 0 && 2 * p.Wo == p.W && p.Wo + 4 == 32 && p.Ho % 4 == 0 && p.W <= 256 &&
+         (p.Wo * 4) % 16 == 0 &&
+         (reinterpret_cast<uintptr_t>(a) % 16) == 0 && get_encode() != nullptr;
+}
+
+merit_status launch_conv_tma(const merit_plan& plan, const void* a, const void* packed_b, void* out,
+                             void* stream) {
+  const ConvParams& p = plan.conv;
+  TmaArgs A;
+  A.p = p;
+  A.wpk = static_cast<const uint8_t*>(packed_b);
+  A.out = static_cast<float*>(out);
+  A.tiles_per_img = p.Ho / 4;
+  A.n_tiles = p.N * A.tiles_per_img * p.n_tiles_n;
+  A.n_groups = p.KH * p.CB;
+  A.raw_bytes = static_cast<uint32_t>(p.W) * 4u * 32u * 2u;
+  A.b_bytes = static_cast<uint32_t>(p.BN) * 128u;
+  uint32_t cols = 32;
+  while (cols < static_cast<uint32_t>(2 * p.BN)) cols <<= 1;
+  A.tmem_cols = cols;
+  const size_t fixed = 1024 + 8 * (6 * kMaxRing + 4) + 16 + 8;
+  const size_t budget = 227 * 1024 - fixed;
+  A.stage_bytes = kEpiCo * 4u * static_cast<uint32_t>(p.Wo) * 4u;
+  A.na = 2;
+  A.nr = 2;
+  A.nb = 2;
+  // grow the rings in the order that hides the most latency: B, raw, A
+  for (;;) {
+    const size_t used = A.na * (size_t)kASlot + A.nb * (size_t)A.b_bytes + A.nr * (size_t)A.raw_bytes +
+                        2 * (size_t)A.stage_bytes;
+    if (A.nb < 4 && used + A.b_bytes <= budget) { ++A.nb; continue; }
+    if (A.nr < kMaxRing && used + 2 * A.raw_bytes <= budget) { A.nr += 2; continue; }  // even
+    if (A.na < 3 && used + kASlot <= budget) { ++A.na; continue; }
+    break;
+  }
+  const size_t used = A.na * (size_t)kASlot + A.nb * (size_t)A.b_bytes + A.nr * (size_t)A.raw_bytes +
+                      2 * (size_t)A.stage_bytes;
+  if (used > budget) return fail(MERIT_E_UNSUPPORTED_VIEW, "TMA conv rings exceed shared memory");
+  const size_t smem = fixed + used;
+  CUtensorMap map;
+  const cuuint64_t dims[4] = {(cuuint64_t)p.W, (cuuint64_t)p.H, (cuuint64_t)p.Cin, (cuuint64_t)p.N};
+  const cuuint64_t strides[3] = {(cuuint64_t)p.W * 2, (cuuint64_t)p.H * p.W * 2,
+                                 (cuuint64_t)p.Cin * p.H * p.W * 2};
+  const cuuint32_t box[4] = {(cuuint32_t)p.W, 8, 32, 1};
+  const cuuint32_t estr[4] = {1, (cuuint32_t)p.sy, 1, 1};
+  CUresult cr = get_encode()(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(a), dims, strides,
+                             box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return fail(MERIT_E_CUDA, "cuTensorMapEncodeTiled failed for the conv input");
+  CUtensorMap omap;
+  const cuuint64_t odims[4] = {(cuuint64_t)p.Wo, (cuuint64_t)p.Ho, (cuuint64_t)p.Cout, (cuuint64_t)p.N};
+  const cuuint64_t ostr[3] = {(cuuint64_t)p.Wo * 4, (cuuint64_t)p.Ho * p.Wo * 4, (cuuint64_t)p.Cout * p.Ho * p.Wo * 4};
+  const cuuint32_t obox[4] = {(cuuint32_t)p.Wo, 4, kEpiCo, 1};
+  const cuuint32_t oestr[4] = {1, 1, 1, 1};
+  cr = get_encode()(&omap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, out, odims, ostr, obox, oestr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return fail(MERIT_E_CUDA, "cuTensorMapEncodeTiled failed for the conv output");
+  if (A.n_tiles == 0) return MERIT_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = set_smem_attr(conv_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return cuda_check(e, "set_smem_attr(conv_tma)");
+  int grid = num_sms();
+  if (grid > A.n_tiles) grid = A.n_tiles;
+  {
+    const char* dbg = getenv("MERIT_CONV_DEBUG");
+    A.debug = dbg ? atoi(dbg) : 0;
+  }
+  A.prof = nullptr;
+  if (A.debug & 64) {
+    cudaMalloc(&A.prof, 8ull * 4 * 16 * grid);
+    cudaMemset(A.prof, 0, 8ull * 4 * 16 * grid);
+  }
+  conv_tma_kernel<<<grid, kThreads, smem, s>>>(map, omap, A);
+  if (A.debug & 64) {
+    cudaStreamSynchronize(s);
+    std::vector<unsigned long long> h(4 * 16 * grid);
+    cudaMemcpy(h.data(), A.prof, h.size() * 8, cudaMemcpyDeviceToHost);
+    auto frac = [&](int w0, int w1_, int idx) {
+      double t = 0, v = 0;
+      for (int b = 0; b < grid; ++b)
+        for (int ww = w0; ww < w1_; ++ww) { t += h[(b * 16 + ww) * 4]; v += h[(b * 16 + ww) * 4 + idx]; }
+      return t > 0 ? 100.0 * v / t : 0.0;
+    };
+    fprintf(stderr, "[tma prof] rings nr=%d na=%d nb=%d | tma: r_empty-wait %.1f%% | repack: r_full-wait %.1f%% a_empty-wait %.1f%% | B: b_empty-wait %.1f%% | mma: a_full %.1f%% b_full %.1f%% tempty %.1f%% | epi: tfull-wait %.1f%%\n",
+            A.nr, A.na, A.nb, frac(kWarpTma, kWarpTma + 1, 1), frac(0, 8, 1), frac(0, 8, 2), frac(kWarpB, kWarpB + 1, 1),
+            frac(kWarpMma, kWarpMma + 1, 1), frac(kWarpMma, kWarpMma + 1, 2), frac(kWarpMma, kWarpMma + 1, 3),
+            frac(kWarpEpi0, kWarpEpi0 + 4, 1));
+    cudaFree(A.prof);
+  }
+  return launch_status("conv_tma_kernel");
+}
+
+}  // namespace merit_dev
