@@ -74,7 +74,7 @@ __device__ __forceinline__ void st_shared_u16(uint32_t addr, uint32_t v) {
   asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"(static_cast<unsigned short>(v)) : "memory");
 }
 
-template <bool IN_BF16, bool SPLIT3, int SX, bool QUAD>
+template <bool IN_BF16, bool SPLIT3, int SX>
 __global__ void __launch_bounds__(kThreads, 1) conv_tap3_kernel(Tap3Args A) {
   extern __shared__ uint8_t smem_raw[];
   const ConvParams& p = A.p;
@@ -130,97 +130,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tap3_kernel(Tap3Args A) {
   const int BN = p.BN;
   const long long HoS = (long long)p.Ho * A.S;
 
-  if (QUAD && warp < kProducerWarps) {
-    // ============ A producers, quad mapping (bf16, stride 2) ==================
-    // Slot rows are padded to S = 32 per output row with 4 leading pads, so a
-    // lane's 4 consecutive slots (quad) map to 8 consecutive input columns
-    // starting at a 16-byte boundary: ONE 16-byte load per (lane, channel)
-    // brings taps 1 and 2 of four slots.  Warp w owns channels 8w..8w+7 (one
-    // 16-byte chunk column of every A row); lane l owns slots 4l..4l+3.
-    // Tiles (128 slots = 4 output rows) start on a pad slot, so the shifted
-    // tap-0 view never needs a guard row.  Stores are rotated across lanes
-    // (row 4l + (k + (l%8)/2) % 4 in step k) so every 8-lane STS.128 phase hits
-    // 8 distinct swizzle positions (no bank conflicts).
-    const int w = warp;           // chunk column j
-    const int l = lane;
-    const int rot = (l & 7) >> 1;
-    int stage = 0;
-    uint32_t phase = 0;
-    const int S = A.S;
-    struct QGrp { uint4 v[8]; };
-    auto load_q = [&](QGrp& G, int tile, int ky, int cb) {
-      const int slot = (tile / p.n_tiles_n) * kBM + 4 * l;
-      const bool in_slot = slot < static_cast<int>(A.slots);
-      const int rowi = slot / S;
-      const int x0 = slot - rowi * S - A.padL;
-      const int n = rowi / p.Ho, y = rowi - (rowi / p.Ho) * p.Ho;
-      const int iy = y * p.sy + ky * p.dy + p.oy;
-      const bool ok = in_slot && x0 >= 0 && iy >= 0 && iy < p.H;
-      const int c0 = cb * 64 + 8 * w;
-      const uint16_t* src = static_cast<const uint16_t*>(A.in) +
-                            (((long long)n * p.Cin + c0) * p.H + iy) * p.W + 2 * x0;
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-        G.v[c] = (ok && c0 + c < p.Cin) ? __ldg(reinterpret_cast<const uint4*>(src + c * HW))
-                                        : make_uint4(0u, 0u, 0u, 0u);
-    };
-    // rotate a quad's four slot words by `rot` with selects (register-only)
-    auto rotq = [&](const uint4& q) {
-      uint4 o;
-      o.x = rot == 0 ? q.x : rot == 1 ? q.y : rot == 2 ? q.z : q.w;
-      o.y = rot == 0 ? q.y : rot == 1 ? q.z : rot == 2 ? q.w : q.x;
-      o.z = rot == 0 ? q.z : rot == 1 ? q.w : rot == 2 ? q.x : q.y;
-      o.w = rot == 0 ? q.w : rot == 1 ? q.x : rot == 2 ? q.y : q.z;
-      return o;
-    };
-    auto emit_q = [&](const QGrp& G) {
-      uint4 vr[8];
-#pragma unroll
-      for (int c = 0; c < 8; ++c) vr[c] = rotq(G.v[c]);
-      mbar_wait(a_empty(stage), phase ^ 1);
-      const uint32_t p_t2 = plane(stage, 0, 0), p_t1 = plane(stage, 1, 0);
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        const int k = (kk + rot) & 3;
-        const int r = 4 * l + k;
-        const uint32_t off = (r >> 3) * 1024u + (r & 7) * 128u + (((uint32_t)w ^ (uint32_t)(r & 7)) << 4);
-        uint32_t wv[8];
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-          wv[c] = kk == 0 ? vr[c].x : kk == 1 ? vr[c].y : kk == 2 ? vr[c].z : vr[c].w;
-        st_shared_v4(p_t1 + off, __byte_perm(wv[0], wv[1], 0x5410), __byte_perm(wv[2], wv[3], 0x5410),
-                     __byte_perm(wv[4], wv[5], 0x5410), __byte_perm(wv[6], wv[7], 0x5410));
-        st_shared_v4(p_t2 + off, __byte_perm(wv[0], wv[1], 0x7632), __byte_perm(wv[2], wv[3], 0x7632),
-                     __byte_perm(wv[4], wv[5], 0x7632), __byte_perm(wv[6], wv[7], 0x7632));
-      }
-      fence_proxy_async();
-      mbar_arrive(a_full(stage));
-      if (++stage == A.na) {
-        stage = 0;
-        phase ^= 1;
-      }
-    };
-    QGrp qa, qb;
-    const int ngrp = A.n_groups;
-    int lt = blockIdx.x, lg = 0;
-    auto next_q = [&](QGrp& G) {
-      const int ky = lg / p.CB, cb = lg - (lg / p.CB) * p.CB;
-      load_q(G, lt, ky, cb);
-      if (++lg == ngrp) { lg = 0; lt += gridDim.x; }
-    };
-    if (lt < A.n_tiles) next_q(qa);
-    for (;;) {
-      const bool more = lt < A.n_tiles;
-      if (!more && lg == 0 && false) break;
-      if (more) next_q(qb);
-      emit_q(qa);
-      if (!more) break;
-      const bool more2 = lt < A.n_tiles;
-      if (more2) next_q(qa);
-      emit_q(qb);
-      if (!more2) break;
-    }
-  } else if (warp < kProducerWarps) {
+  if (warp < kProducerWarps) {
     // ============ A producers =================================================
     const int r = threadIdx.x & 127;  // slot row in the tile
     const int h = threadIdx.x >> 7;   // channel half
@@ -564,11 +474,8 @@ merit_status launch_conv_tap3(const merit_plan& plan, const void* a, const void*
   A.in = a;
   A.wpk = static_cast<const uint8_t*>(packed_b);
   A.out = static_cast<float*>(out);
-  const bool quad = p.sx == 2 && p.in_bf16 && p.split == 1 && p.W % 8 == 0 && p.Wo % 4 == 0 &&
-                    2 * p.Wo == p.W && (reinterpret_cast<uintptr_t>(a) % 16) == 0 &&
-                    !(getenv("MERIT_TAP3_QUAD") && getenv("MERIT_TAP3_QUAD")[0] == '0');
-  A.padL = quad ? 4 : 1;
-  A.S = quad ? p.Wo + 4 : p.Wo + 1 + (p.sx == 1 ? 1 : 0);
+  A.padL = 1;
+  A.S = p.Wo + 1 + (p.sx == 1 ? 1 : 0);
   A.slots = (long long)p.N * p.Ho * A.S;
   const long long tiles_m = (A.slots + kBM - 1) / kBM;
   A.n_tiles = static_cast<int>(tiles_m * p.n_tiles_n);
@@ -605,18 +512,17 @@ merit_status launch_conv_tap3(const merit_plan& plan, const void* a, const void*
     cudaMemset(A.prof, 0, 8ull * 8 * 16 * grid);
   }
   cudaError_t e;
-#define MERIT_LAUNCH_TAP3(INB, S3, SXV, Q)                                                     \
+#define MERIT_LAUNCH_TAP3(INB, S3, SXV)                                                     \
   do {                                                                                        \
-    auto k = conv_tap3_kernel<INB, S3, SXV, Q>;                                                  \
+    auto k = conv_tap3_kernel<INB, S3, SXV>;                                                  \
     e = set_smem_attr(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);      \
     if (e != cudaSuccess) return cuda_check(e, "set_smem_attr(conv_tap3)");            \
     k<<<grid, kThreads, smem, s>>>(A);                                                        \
   } while (0)
-  if (p.sx == 2 && quad) MERIT_LAUNCH_TAP3(true, false, 2, true);
-  else if (p.sx == 2) MERIT_LAUNCH_TAP3(true, false, 2, false);
-  else if (p.in_bf16) MERIT_LAUNCH_TAP3(true, false, 1, false);
-  else if (split3) MERIT_LAUNCH_TAP3(false, true, 1, false);
-  else MERIT_LAUNCH_TAP3(false, false, 1, false);
+  if (p.sx == 2) MERIT_LAUNCH_TAP3(true, false, 2);
+  else if (p.in_bf16) MERIT_LAUNCH_TAP3(true, false, 1);
+  else if (split3) MERIT_LAUNCH_TAP3(false, true, 1);
+  else MERIT_LAUNCH_TAP3(false, false, 1);
 #undef MERIT_LAUNCH_TAP3
   if (A.debug & 64) {
     cudaStreamSynchronize(s);

@@ -21,6 +21,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "tc_common.cuh"
@@ -45,9 +46,11 @@ struct TmaArgs {
   float* out;
   int tiles_per_img;   // Ho / 4
   int n_tiles;
+  int n_units;         // scheduling units: tiles, or (pair of M tiles, N tile) in pair mode
   int n_groups;        // KH * CB
   uint32_t raw_bytes;  // W * 4 rows * 32 ch * 2 (half a 64-channel k-block)
-  uint32_t b_bytes;
+  uint32_t b_bytes;    // one (k-block, tap) of B: BN rows x 64 ch
+  uint32_t b_slot;     // this CTA's share of it: b_bytes, or b_bytes / 2 in pair mode
   int nr, na, nb;
   uint32_t tmem_cols;
   uint32_t stage_bytes;  // epilogue staging: kEpiCo co x 4 rows x Wo fp32
@@ -74,6 +77,16 @@ __device__ __forceinline__ void twait(uint32_t bar, uint32_t par, unsigned long 
   }
 }
 
+// B tile of one CTA of a pair: completion is signalled on the LEADER's barrier
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap* map, int x, int y,
+                                                 uint32_t leader_bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(leader_bar)
+      : "memory");
+}
+
 __device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, uint32_t src, int x, int y, int c, int n) {
   asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
                    reinterpret_cast<uint64_t>(map)),
@@ -81,9 +94,16 @@ __device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, uint32_t sr
                : "memory");
 }
 
+// PAIR: the kernel runs as clusters of two CTAs that issue cta_group::2 MMAs
+// (M = 256): each CTA gathers and repacks its own 128-slot tile (A) and loads
+// HALF of every weight tile (B rows = output channels), so each weight byte
+// fetched from L2 feeds 256 output slots.  The leader (rank 0) issues the
+// MMAs; operand-ready signals of the peer arrive on the leader's barriers,
+// and the MMA commits multicast back to both CTAs.
+template <bool PAIR>
 __global__ void __maxnreg__(128)  // 15 warps: <= 4 per SM sub-partition x 128 regs
 conv_tma_kernel(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap out_map,
-                TmaArgs A) {
+                const __grid_constant__ CUtensorMap b_map, TmaArgs A) {
   extern __shared__ uint8_t smem_raw[];
   const ConvParams& p = A.p;
   const int warp = threadIdx.x >> 5;
@@ -93,7 +113,7 @@ conv_tma_kernel(const __grid_constant__ CUtensorMap in_map, const __grid_constan
   // which must be a valid shared address (its value only feeds the pad slot
   // of output row 0, which is never stored).
   const uint32_t bring = base;                          // nb x b_bytes
-  const uint32_t aring = bring + A.nb * A.b_bytes;      // na x kASlot
+  const uint32_t aring = bring + A.nb * A.b_slot;       // na x kASlot
   const uint32_t rring = aring + A.na * kASlot;         // nr x raw_bytes
   const uint32_t ering = rring + A.nr * A.raw_bytes;    // 2 x stage_bytes (epilogue)
   const uint32_t bars = (ering + 2 * A.stage_bytes + 7u) & ~7u;
@@ -111,13 +131,19 @@ conv_tma_kernel(const __grid_constant__ CUtensorMap in_map, const __grid_constan
   auto tap2_plane = [&](int s) { return aring + s * kASlot; };
   auto tap1_plane = [&](int s) { return aring + s * kASlot + kPlane; };
 
+  constexpr uint32_t kSplit = PAIR ? 2u : 1u;  // CTAs feeding one MMA
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+  // operand-ready / accumulator-free signals go to the MMA-issuing CTA
+  auto to_leader = [&](uint32_t bar) {
+    if (PAIR) mbar_arrive_cluster(mapa_shared(bar, 0)); else mbar_arrive(bar);
+  };
   if (threadIdx.x == 0) {
     for (int s = 0; s < A.nr; ++s) {
       mbar_init(r_full(s), 1);
       mbar_init(r_empty(s), kRepackers / 2);  // one half of the repack warps
     }
     for (int s = 0; s < A.na; ++s) {
-      mbar_init(a_full(s), kRepackers);
+      mbar_init(a_full(s), kRepackWarps * kSplit);  // one elected lane per repack warp
       mbar_init(a_empty(s), 1);
     }
     for (int s = 0; s < A.nb; ++s) {
@@ -126,18 +152,25 @@ conv_tma_kernel(const __grid_constant__ CUtensorMap in_map, const __grid_constan
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull(a), 1);
-      mbar_init(tempty(a), 128);
+      mbar_init(tempty(a), 4 * kSplit);  // one elected lane per epilogue warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == kWarpB) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot),
-                 "r"(A.tmem_cols)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot),
+                   "r"(A.tmem_cols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot),
+                   "r"(A.tmem_cols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if (PAIR) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot_ptr;
   const int BN = p.BN;
@@ -145,6 +178,12 @@ conv_tma_kernel(const __grid_constant__ CUtensorMap in_map, const __grid_constan
   const bool pon = (A.debug & 64) && lane == 0;
   unsigned long long w1 = 0, w2 = 0, w3 = 0;
   const unsigned long long t_start = clock64();
+  // scheduling unit -> (M tile, N tile); in pair mode the two CTAs of a
+  // cluster take adjacent M tiles (an odd last one reads / writes out of
+  // bounds image N, which TMA zero-fills / clips)
+  const int unit0 = PAIR ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
+  const int ustep = PAIR ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
+  auto m_tile = [&](int u) { return PAIR ? 2 * (u / p.n_tiles_n) + static_cast<int>(rank) : u / p.n_tiles_n; };
 
   if (warp == kWarpTma) {
     // ============ raw-row loader: the MERIT gather on the TMA engine ======
@@ -152,8 +191,8 @@ conv_tma_kernel(const __grid_constant__ CUtensorMap in_map, const __grid_constan
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&in_map)) : "memory");
       int st = 0;
       uint32_t ph = 0;
-      for (int tile = blockIdx.x; tile < A.n_tiles; tile += gridDim.x) {
-        const int mt = tile / p.n_tiles_n;
+      for (int tile = unit0; tile < A.n_units; tile += ustep) {
+        const int mt = m_tile(tile);
         const int n = mt / A.tiles_per_img;
         const int y0 = (mt - n * A.tiles_per_img) * 4;
         for (int g = 0; g < A.n_groups; ++g) {
@@ -191,7 +230,7 @@ conv_tma_kernel(const __grid_constant__ CUtensorMap in_map, const __grid_constan
     const uint32_t roff = static_cast<uint32_t>(8 * (w & 3)) * 4u * rowbytes + (pad ? 0u : 4u * x);
     int rs = w >> 2, as = 0;
     uint32_t rph = 0, aph = 0;
-    for (int tile = blockIdx.x; tile < A.n_tiles; tile += gridDim.x) {
+    for (int tile = unit0; tile < A.n_units; tile += ustep) {
       for (int g = 0; g < A.n_groups; ++g) {
         twait(r_full(rs), rph, w1, pon);
         uint32_t v[4][8];  // [row k][channel c]: (tap1 | tap2 << 16)
@@ -221,7 +260,8 @@ conv_tma_kernel(const __grid_constant__ CUtensorMap in_map, const __grid_constan
                        __byte_perm(wv[4], wv[5], 0x7632), __byte_perm(wv[6], wv[7], 0x7632));
         }
         fence_proxy_async();
-        mbar_arrive(a_full(as));
+        __syncwarp();
+        if (l == 0) to_leader(a_full(as));
         if (++as == A.na) { as = 0; aph ^= 1; }
       }
     }
@@ -230,13 +270,22 @@ conv_tma_kernel(const __grid_constant__ CUtensorMap in_map, const __grid_constan
     if (lane == 0) {
       int st = 0;
       uint32_t ph = 0;
-      for (int tile = blockIdx.x; tile < A.n_tiles; tile += gridDim.x) {
+      for (int tile = unit0; tile < A.n_units; tile += ustep) {
         const int nt = tile % p.n_tiles_n;
         for (int kb = 0; kb < p.n_kb; ++kb) {
           twait(b_empty(st), ph ^ 1, w1, pon);
-          mbar_expect_tx(b_full(st), A.b_bytes);
-          bulk_g2s(bring + st * A.b_bytes, A.wpk + ((long long)nt * p.n_kb + kb) * A.b_bytes, A.b_bytes,
-                   b_full(st));
+          if (PAIR) {
+            // both halves complete on the leader's barrier, which expects the
+            // whole tile
+            if (rank == 0) mbar_expect_tx(b_full(st), A.b_bytes);
+            const long long off = ((long long)nt * p.n_kb + kb) * A.b_bytes + rank * A.b_slot;
+            tma_load_2d_pair(bring + st * A.b_slot, &b_map, 0, static_cast<int>(off >> 8),
+                             mapa_shared(b_full(st), 0));
+          } else {
+            mbar_expect_tx(b_full(st), A.b_bytes);
+            bulk_g2s(bring + st * A.b_bytes, A.wpk + ((long long)nt * p.n_kb + kb) * A.b_bytes, A.b_bytes,
+                     b_full(st));
+          }
           if (++st == A.nb) { st = 0; ph ^= 1; }
         }
       }
@@ -244,11 +293,11 @@ conv_tma_kernel(const __grid_constant__ CUtensorMap in_map, const __grid_constan
     __syncwarp();
   } else if (warp == kWarpMma) {
     // ============ MMA issuer ===================================================
-    if (lane == 0) {
-      const uint32_t idesc = make_idesc(BN);
+    if (lane == 0 && rank == 0) {
+      const uint32_t idesc = PAIR ? make_idesc_pair(BN) : make_idesc(BN);
       int as = 0, bs = 0, acc = 0;
       uint32_t aph = 0, bph = 0, acc_phase = 0;
-      for (int tile = blockIdx.x; tile < A.n_tiles; tile += gridDim.x) {
+      for (int tile = unit0; tile < A.n_units; tile += ustep) {
         twait(tempty(acc), acc_phase ^ 1, w3, pon);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -260,19 +309,22 @@ conv_tma_kernel(const __grid_constant__ CUtensorMap in_map, const __grid_constan
             tc_fence_after();
             // tap 0 = tap-2 plane one slot row earlier; tap 1; tap 2
             const uint32_t a0 = kx == 1 ? tap1_plane(as) : tap2_plane(as) - (kx == 0 ? 128u : 0u);
-            const uint32_t b0 = bring + bs * A.b_bytes;
+            const uint32_t b0 = bring + bs * A.b_slot;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const uint32_t accum = (g > 0 || kx > 0 || k > 0) ? 1u : 0u;
-              tc_mma(d_tmem, sw128_desc(a0 + 32 * k), sw128_desc(b0 + 32 * k), idesc, accum);
+              if (PAIR)
+                tc_mma_pair(d_tmem, sw128_desc(a0 + 32 * k), sw128_desc(b0 + 32 * k), idesc, accum);
+              else
+                tc_mma(d_tmem, sw128_desc(a0 + 32 * k), sw128_desc(b0 + 32 * k), idesc, accum);
             }
-            tc_commit(b_empty(bs));
+            if (PAIR) tc_commit_pair(b_empty(bs), 3); else tc_commit(b_empty(bs));
             if (++bs == A.nb) { bs = 0; bph ^= 1; }
           }
-          tc_commit(a_empty(as));
+          if (PAIR) tc_commit_pair(a_empty(as), 3); else tc_commit(a_empty(as));
           if (++as == A.na) { as = 0; aph ^= 1; }
         }
-        tc_commit(tfull(acc));
+        if (PAIR) tc_commit_pair(tfull(acc), 3); else tc_commit(tfull(acc));
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
@@ -290,8 +342,8 @@ conv_tma_kernel(const __grid_constant__ CUtensorMap in_map, const __grid_constan
     int acc = 0;
     uint32_t acc_phase = 0;
     int sb = 0;  // staging buffer
-    for (int tile = blockIdx.x; tile < A.n_tiles; tile += gridDim.x) {
-      const int mt = tile / p.n_tiles_n, nt = tile % p.n_tiles_n;
+    for (int tile = unit0; tile < A.n_units; tile += ustep) {
+      const int mt = m_tile(tile), nt = tile % p.n_tiles_n;
       const int n = mt / A.tiles_per_img;
       const int y0 = (mt - n * A.tiles_per_img) * 4;
       twait(tfull(acc), acc_phase, w1, pon);
@@ -303,7 +355,8 @@ conv_tma_kernel(const __grid_constant__ CUtensorMap in_map, const __grid_constan
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (c0 + 32 >= BN) {  // accumulator drained: let the MMA reuse it
           tc_fence_before();
-          mbar_arrive(tempty(acc));
+          __syncwarp();
+          if (lane == 0) to_leader(tempty(acc));
         }
 #pragma unroll
         for (int hh = 0; hh < 32 / kEpiCo; ++hh) {
@@ -337,12 +390,17 @@ conv_tma_kernel(const __grid_constant__ CUtensorMap in_map, const __grid_constan
     unsigned long long* pr = A.prof + (blockIdx.x * 16 + warp) * 4;
     pr[0] = clock64() - t_start; pr[1] = w1; pr[2] = w2; pr[3] = w3;
   }
-  __syncthreads();
+  // pair: neither CTA may exit while the other can still signal it or the
+  // leader's MMAs can still read its shared memory
+  if (PAIR) cluster_sync(); else __syncthreads();
   if (warp == kWarpB) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(A.tmem_cols)
-                 : "memory");
+    if (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(A.tmem_cols)
+                   : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(A.tmem_cols)
+                   : "memory");
   }
 }
 
@@ -377,10 +435,17 @@ merit_status launch_conv_tma(const merit_plan& plan, const void* a, const void* 
   A.wpk = static_cast<const uint8_t*>(packed_b);
   A.out = static_cast<float*>(out);
   A.tiles_per_img = p.Ho / 4;
-  A.n_tiles = p.N * A.tiles_per_img * p.n_tiles_n;
+  const int m_tiles = p.N * A.tiles_per_img;
+  A.n_tiles = m_tiles * p.n_tiles_n;
+  // CTA pairs (cta_group::2) unless disabled; BN % 16 == 0 keeps each half of
+  // a weight tile a whole number of 8-row swizzle atoms
+  const char* pe = getenv("MERIT_CONV_PAIR");
+  const bool pair = !(pe && pe[0] == '0') && p.BN % 16 == 0 && num_sms() >= 2;
+  A.n_units = pair ? ((m_tiles + 1) / 2) * p.n_tiles_n : A.n_tiles;
   A.n_groups = p.KH * p.CB;
   A.raw_bytes = static_cast<uint32_t>(p.W) * 4u * 32u * 2u;
   A.b_bytes = static_cast<uint32_t>(p.BN) * 128u;
+  A.b_slot = pair ? A.b_bytes / 2 : A.b_bytes;
   uint32_t cols = 32;
   while (cols < static_cast<uint32_t>(2 * p.BN)) cols <<= 1;
   A.tmem_cols = cols;
@@ -390,17 +455,21 @@ merit_status launch_conv_tma(const merit_plan& plan, const void* a, const void* 
   A.na = 2;
   A.nr = 2;
   A.nb = 2;
-  // grow the rings in the order that hides the most latency: B, raw, A
+  int nb_first = 4;  // weight slots granted before the raw ring grows
+  if (const char* r = getenv("MERIT_TMA_NB_FIRST")) nb_first = atoi(r);
+  auto used_bytes = [&]() {
+    return A.na * (size_t)kASlot + A.nb * (size_t)A.b_slot + A.nr * (size_t)A.raw_bytes + 2 * (size_t)A.stage_bytes;
+  };
+  // grow the rings in the order that hides the most latency: B, raw, B, A
   for (;;) {
-    const size_t used = A.na * (size_t)kASlot + A.nb * (size_t)A.b_bytes + A.nr * (size_t)A.raw_bytes +
-                        2 * (size_t)A.stage_bytes;
-    if (A.nb < 4 && used + A.b_bytes <= budget) { ++A.nb; continue; }
-    if (A.nr < kMaxRing && used + 2 * A.raw_bytes <= budget) { A.nr += 2; continue; }  // even
+    const size_t used = used_bytes();
+    if (A.nb < nb_first && used + A.b_slot <= budget) { ++A.nb; continue; }
+    if (A.nr < 4 && used + 2 * A.raw_bytes <= budget) { A.nr += 2; continue; }  // even
+    if (A.nb < kMaxRing && used + A.b_slot <= budget) { ++A.nb; continue; }
     if (A.na < 3 && used + kASlot <= budget) { ++A.na; continue; }
     break;
   }
-  const size_t used = A.na * (size_t)kASlot + A.nb * (size_t)A.b_bytes + A.nr * (size_t)A.raw_bytes +
-                      2 * (size_t)A.stage_bytes;
+  const size_t used = used_bytes();
   if (used > budget) return fail(MERIT_E_UNSUPPORTED_VIEW, "TMA conv rings exceed shared memory");
   const size_t smem = fixed + used;
   CUtensorMap map;
@@ -422,12 +491,33 @@ merit_status launch_conv_tma(const merit_plan& plan, const void* a, const void* 
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (cr != CUDA_SUCCESS) return fail(MERIT_E_CUDA, "cuTensorMapEncodeTiled failed for the conv output");
+  // packed weights as rows of 256 bytes: one box = this CTA's half tile
+  CUtensorMap bmap;
+  std::memset(&bmap, 0, sizeof(bmap));
+  if (pair) {
+    const cuuint64_t bdims[2] = {256, (cuuint64_t)(p.packed_b_bytes / 256)};
+    const cuuint64_t bstr[1] = {256};
+    const cuuint32_t bbox[2] = {256, A.b_slot / 256};
+    const cuuint32_t bestr[2] = {1, 1};
+    cr = get_encode()(&bmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(packed_b), bdims, bstr, bbox,
+                      bestr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return fail(MERIT_E_CUDA, "cuTensorMapEncodeTiled failed for the conv weights");
+  }
   if (A.n_tiles == 0) return MERIT_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  cudaError_t e = set_smem_attr(conv_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto kfn = pair ? conv_tma_kernel<true> : conv_tma_kernel<false>;
+  cudaError_t e = set_smem_attr(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return cuda_check(e, "set_smem_attr(conv_tma)");
-  int grid = num_sms();
-  if (grid > A.n_tiles) grid = A.n_tiles;
+  int grid;
+  if (pair) {
+    int pairs = num_sms() / 2;
+    if (pairs > A.n_units) pairs = A.n_units;
+    grid = 2 * pairs;
+  } else {
+    grid = num_sms();
+    if (grid > A.n_tiles) grid = A.n_tiles;
+  }
   {
     const char* dbg = getenv("MERIT_CONV_DEBUG");
     A.debug = dbg ? atoi(dbg) : 0;
@@ -437,21 +527,35 @@ merit_status launch_conv_tma(const merit_plan& plan, const void* a, const void* 
     cudaMalloc(&A.prof, 8ull * 4 * 16 * grid);
     cudaMemset(A.prof, 0, 8ull * 4 * 16 * grid);
   }
-  conv_tma_kernel<<<grid, kThreads, smem, s>>>(map, omap, A);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = pair ? 2 : 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  e = cudaLaunchKernelEx(&cfg, kfn, map, omap, bmap, A);
+  if (e != cudaSuccess) return cuda_check(e, "cudaLaunchKernelEx(conv_tma)");
   if (A.debug & 64) {
     cudaStreamSynchronize(s);
     std::vector<unsigned long long> h(4 * 16 * grid);
     cudaMemcpy(h.data(), A.prof, h.size() * 8, cudaMemcpyDeviceToHost);
-    auto frac = [&](int w0, int w1_, int idx) {
+    auto frac = [&](int w0, int w1_, int idx, int bstep) {
       double t = 0, v = 0;
-      for (int b = 0; b < grid; ++b)
+      for (int b = 0; b < grid; b += bstep)
         for (int ww = w0; ww < w1_; ++ww) { t += h[(b * 16 + ww) * 4]; v += h[(b * 16 + ww) * 4 + idx]; }
       return t > 0 ? 100.0 * v / t : 0.0;
     };
-    fprintf(stderr, "[tma prof] rings nr=%d na=%d nb=%d | tma: r_empty-wait %.1f%% | repack: r_full-wait %.1f%% a_empty-wait %.1f%% | B: b_empty-wait %.1f%% | mma: a_full %.1f%% b_full %.1f%% tempty %.1f%% | epi: tfull-wait %.1f%%\n",
-            A.nr, A.na, A.nb, frac(kWarpTma, kWarpTma + 1, 1), frac(0, 8, 1), frac(0, 8, 2), frac(kWarpB, kWarpB + 1, 1),
-            frac(kWarpMma, kWarpMma + 1, 1), frac(kWarpMma, kWarpMma + 1, 2), frac(kWarpMma, kWarpMma + 1, 3),
-            frac(kWarpEpi0, kWarpEpi0 + 4, 1));
+    const int ms = pair ? 2 : 1;  // MMA issuers: leaders only
+    fprintf(stderr, "[tma prof] %s rings nr=%d na=%d nb=%d | tma: r_empty-wait %.1f%% | repack: r_full-wait %.1f%% a_empty-wait %.1f%% | B: b_empty-wait %.1f%% | mma: a_full %.1f%% b_full %.1f%% tempty %.1f%% | epi: tfull-wait %.1f%%\n",
+            pair ? "pair" : "single", A.nr, A.na, A.nb, frac(kWarpTma, kWarpTma + 1, 1, 1), frac(0, 8, 1, 1),
+            frac(0, 8, 2, 1), frac(kWarpB, kWarpB + 1, 1, 1), frac(kWarpMma, kWarpMma + 1, 1, ms),
+            frac(kWarpMma, kWarpMma + 1, 2, ms), frac(kWarpMma, kWarpMma + 1, 3, ms), frac(kWarpEpi0, kWarpEpi0 + 4, 1, 1));
     cudaFree(A.prof);
   }
   return launch_status("conv_tma_kernel");

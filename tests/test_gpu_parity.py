@@ -215,6 +215,36 @@ def test_conv_variants_fp32(cuda, n, cin, h, wd, cout, k, s, pad, dil, relu):
         assert np.all(got >= 0)
 
 
+CONV_VARIANTS = {
+    "default": {},                                  # TMA gather, CTA pairs where eligible
+    "single": {"MERIT_CONV_PAIR": "0"},             # TMA gather, one CTA per tile
+    "tap3": {"MERIT_CONV_TMA": "0"},                # register gather, tap-shared planes
+    "general": {"MERIT_CONV_KERNEL": "general"},    # per-tap gather
+}
+
+
+@pytest.mark.parametrize("variant", sorted(CONV_VARIANTS))
+@pytest.mark.parametrize("n,cin,h,cout", [
+    (2, 128, 16, 256),    # small image: tap3 path, two channel blocks
+    (2, 128, 32, 256),
+    (3, 128, 56, 256),    # C4 geometry, 21 M tiles: odd -> ghost tile in pair mode
+    (1, 192, 56, 96),     # three channel blocks, BN = 96
+    (2, 64, 56, 320),     # two N tiles (BN = 160)
+])
+def test_conv_bf16_stride2_kernel_variants(cuda, monkeypatch, variant, n, cin, h, cout):
+    for k, v in CONV_VARIANTS[variant].items():
+        monkeypatch.setenv(k, v)
+    w = W.conv_nchw_view(n, cin, h, h, cout, 3, 2, 1)
+    x = W.gen_uniform([n, cin, h, h], 31)
+    wt = W.gen_normal([cout, cin, 3, 3], 32, (2.0 / (9 * cin)) ** 0.5)
+    w.src_a, w.src_b = W.to_bf16_bits(x), W.to_bf16_bits(wt)
+    w.dtype_a = w.dtype_b = W.Dtype.BF16
+    got = run_full(w)
+    assert rel_err(got, O.conv2d(x, wt, 2, 1)) <= TOL_BF16
+    want_b = O.conv2d(W.bf16_bits_to_f32(w.src_a), W.bf16_bits_to_f32(w.src_b), 2, 1)
+    assert rel_err(got, want_b) <= 1e-4
+
+
 def test_conv_fast_bf16_flag(cuda):
     w = W.conv_nchw_view(2, 64, 12, 12, 64, 3, 1, 1)
     w.src_a = W.gen_uniform([2, 64, 12, 12], 5)
