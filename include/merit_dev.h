@@ -246,6 +246,9 @@ void merit_f32_to_bf16(const float* in, uint16_t* out, int64_t n);
 /* Counters of kernels launched through this library by the calling process
  * (evidence for the benchmark's gpu_launches claim). */
 int64_t merit_dev_launch_count(void);
+/* Name of the last kernel this library launched (a static string; "" before
+ * the first launch). */
+const char* merit_dev_last_kernel(void);
 
 #ifdef __cplusplus
 }

@@ -83,6 +83,7 @@ PROTOTYPES = {
                                  C.c_int64, C.c_int64, C.c_uint64]),
     "merit_f32_to_bf16": (None, [C.c_void_p, C.c_void_p, C.c_int64]),
     "merit_dev_launch_count": (C.c_int64, []),
+    "merit_dev_last_kernel": (C.c_char_p, []),
 }
 
 _lib = None

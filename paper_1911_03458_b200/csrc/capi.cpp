@@ -8,6 +8,7 @@
 #include <utility>
 #include <vector>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -19,6 +20,7 @@ namespace merit_dev {
 namespace {
 thread_local std::string g_last_error;
 std::atomic<int64_t> g_launches{0};
+std::atomic<const char*> g_last_kernel{""};
 }  // namespace
 
 merit_status fail(merit_status st, const std::string& msg) {
@@ -33,6 +35,14 @@ merit_status cuda_check(int err, const char* what) {
 }
 
 void count_launch(int n) { g_launches += n; }
+void note_kernel(const char* name) { g_last_kernel.store(name); }
+bool pdl_enabled() {
+  static const int on = [] {
+    const char* e = getenv("MERIT_PDL");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  return on != 0;
+}
 
 cudaError_t set_smem_attr_impl(const void* fn, cudaFuncAttribute attr, int bytes) {
   static std::mutex mu;
@@ -96,6 +106,8 @@ const char* merit_dev_build_info(void) {
 const char* merit_dev_last_error(void) { return g_last_error.c_str(); }
 
 int64_t merit_dev_launch_count(void) { return g_launches.load(); }
+
+const char* merit_dev_last_kernel(void) { return g_last_kernel.load(); }
 
 merit_status merit_dev_plan_create(const merit_workload_desc* desc, merit_plan** out_plan) {
   if (!desc || !out_plan) return fail(MERIT_E_INVALID_ARGUMENT, "null argument");

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <utility>
 
 #include "plan.hpp"
 
@@ -12,6 +13,7 @@ inline merit_status launch_status(const char* what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_check(e, what);
   count_launch();
+  note_kernel(what);
   return MERIT_OK;
 }
 
@@ -32,6 +34,52 @@ cudaError_t set_smem_attr_impl(const void* fn, cudaFuncAttribute attr, int bytes
 template <typename K>
 inline cudaError_t set_smem_attr(K kernel, cudaFuncAttribute attr, int bytes) {
   return set_smem_attr_impl(reinterpret_cast<const void*>(kernel), attr, bytes);
+}
+
+// ---------------------------------------------------------------- PDL --
+// Programmatic dependent launch: consecutive MERIT launches on a stream may
+// overlap their prologues.  Every PDL kernel executes pdl_wait() (PTX
+// griddepcontrol.wait: the previous grid has completed and its memory is
+// visible) before its first global load or store, so stream order is kept
+// for any chain of launches; only work that touches no global data (barrier
+// init, TMEM allocation, L2 prefetch hints) runs before it.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+// L2 prefetch hint of global bytes [p, p + bytes): no architectural effect,
+// so it may precede pdl_wait() (L2 is the coherence point).
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+bool pdl_enabled();  // MERIT_PDL=0 disables
+
+// Launch `kernel` with the PDL attribute (and an optional cluster shape).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              unsigned cluster_x, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  unsigned n = 0;
+  if (pdl_enabled()) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  if (cluster_x > 1) {
+    attr[n].id = cudaLaunchAttributeClusterDimension;
+    attr[n].val.clusterDim.x = cluster_x;
+    attr[n].val.clusterDim.y = 1;
+    attr[n].val.clusterDim.z = 1;
+    ++n;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

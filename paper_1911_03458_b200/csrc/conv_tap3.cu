@@ -125,6 +125,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tap3_kernel(Tap3Args A) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot_ptr;
+  pdl_launch_dependents();
+  pdl_wait();  // prologue done: from here on global memory is touched
 
   const long long HW = (long long)p.H * p.W;
   const int BN = p.BN;
@@ -517,7 +519,8 @@ merit_status launch_conv_tap3(const merit_plan& plan, const void* a, const void*
     auto k = conv_tap3_kernel<INB, S3, SXV>;                                                  \
     e = set_smem_attr(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);      \
     if (e != cudaSuccess) return cuda_check(e, "set_smem_attr(conv_tap3)");            \
-    k<<<grid, kThreads, smem, s>>>(A);                                                        \
+    e = launch_pdl(k, dim3(grid), dim3(kThreads), smem, s, 1, A);                              \
+    if (e != cudaSuccess) return cuda_check(e, "launch(conv_tap3)");                         \
   } while (0)
   if (p.sx == 2) MERIT_LAUNCH_TAP3(true, false, 2);
   else if (p.in_bf16) MERIT_LAUNCH_TAP3(true, false, 1);

@@ -102,6 +102,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(ConvArgs A) {
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot_ptr;
+  pdl_launch_dependents();
+  pdl_wait();  // prologue done: from here on global memory is touched
 
   const int HoWo = p.Ho * p.Wo;
   const long long HW = (long long)p.H * p.W;
@@ -735,7 +737,8 @@ merit_status launch_conv(const merit_plan& plan, const void* a, const void* pack
     auto k = conv_tc_kernel<INB, S3, TP>;                                                      \
     e = set_smem_attr(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);       \
     if (e != cudaSuccess) return cuda_check(e, "set_smem_attr(conv)");                  \
-    k<<<grid, kThreads, smem, s>>>(A);                                                         \
+    e = launch_pdl(k, dim3(grid), dim3(kThreads), smem, s, 1, A);                              \
+    if (e != cudaSuccess) return cuda_check(e, "launch(conv_tc)");                           \
   } while (0)
   A.prof = nullptr;
   if (A.debug & 64) cudaMalloc(&A.prof, sizeof(unsigned long long) * 4 * 16 * grid), cudaMemset(A.prof, 0, sizeof(unsigned long long) * 4 * 16 * grid);

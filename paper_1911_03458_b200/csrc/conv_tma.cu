@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "tc_common.cuh"
+#include "tmap.cuh"
 
 namespace merit_dev {
 namespace {
@@ -173,6 +174,8 @@ conv_tma_kernel(const __grid_constant__ CUtensorMap in_map, const __grid_constan
   if (PAIR) cluster_sync(); else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot_ptr;
+  pdl_launch_dependents();
+  pdl_wait();  // prologue done: from here on global memory is touched
   const int BN = p.BN;
   const int W = p.W;
   const bool pon = (A.debug & 64) && lane == 0;
@@ -404,17 +407,7 @@ conv_tma_kernel(const __grid_constant__ CUtensorMap in_map, const __grid_constan
   }
 }
 
-PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
-    void* ptr = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
-  }
-  return fn;
-}
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() { return tensor_map_encoder(); }
 
 }  // namespace
 
@@ -527,20 +520,8 @@ merit_status launch_conv_tma(const merit_plan& plan, const void* a, const void* 
     cudaMalloc(&A.prof, 8ull * 4 * 16 * grid);
     cudaMemset(A.prof, 0, 8ull * 4 * 16 * grid);
   }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = pair ? 2 : 1;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  e = cudaLaunchKernelEx(&cfg, kfn, map, omap, bmap, A);
-  if (e != cudaSuccess) return cuda_check(e, "cudaLaunchKernelEx(conv_tma)");
+  e = launch_pdl(kfn, dim3(grid), dim3(kThreads), smem, s, pair ? 2u : 1u, map, omap, bmap, A);
+  if (e != cudaSuccess) return cuda_check(e, "launch(conv_tma)");
   if (A.debug & 64) {
     cudaStreamSynchronize(s);
     std::vector<unsigned long long> h(4 * 16 * grid);
@@ -558,7 +539,7 @@ merit_status launch_conv_tma(const merit_plan& plan, const void* a, const void* 
             frac(kWarpMma, kWarpMma + 1, 2, ms), frac(kWarpMma, kWarpMma + 1, 3, ms), frac(kWarpEpi0, kWarpEpi0 + 4, 1, 1));
     cudaFree(A.prof);
   }
-  return launch_status("conv_tma_kernel");
+  return launch_status(pair ? "conv_tma_kernel<pair, cta_group::2>" : "conv_tma_kernel<single>");
 }
 
 }  // namespace merit_dev

@@ -112,6 +112,8 @@ __global__ void generic_kernel(GenArgs A) {
   const GenericParams& g = A.g;
   const ProgramImage& P = *A.prog;
   const long long row = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+  pdl_launch_dependents();
+  pdl_wait();
   if (row >= g.rows) return;
   long long k[kMaxK];
   // p index of this row (row-major, tensor.hpp:59-65)
@@ -280,7 +282,9 @@ merit_status launch_generic(const merit_plan& plan, const void* a, const void* b
   const long long blocks = (plan.gen.rows + threads - 1) / threads;
   if (blocks == 0) return MERIT_OK;
   if (blocks > 0x7fffffffLL) return fail(MERIT_E_INVALID_ARGUMENT, "too many rows");
-  generic_kernel<<<static_cast<unsigned>(blocks), threads, 0, static_cast<cudaStream_t>(stream)>>>(args);
+  cudaError_t e = launch_pdl(generic_kernel, dim3(static_cast<unsigned>(blocks)), dim3(threads), 0,
+                             static_cast<cudaStream_t>(stream), 1, args);
+  if (e != cudaSuccess) return cuda_check(e, "launch(generic)");
   return launch_status("generic_kernel");
 }
 

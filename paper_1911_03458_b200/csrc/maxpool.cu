@@ -9,7 +9,10 @@
 // (equivalent to -inf padding for max); ZERO_PAD reads 0 outside.
 //
 // Roofline: HBM.  Algorithmic bytes = input plane bytes + output bytes.
+#include <cstring>
+
 #include "common.cuh"
+#include "tmap.cuh"
 
 namespace merit_dev {
 namespace {
@@ -141,9 +144,7 @@ __device__ __forceinline__ void maxpool3s2_item(const float* __restrict__ in, fl
 // memory, so one cp.async.bulk (TMA engine) per band moves them into a
 // shared-memory ring NS bands deep; warps compute from shared memory.  Bytes
 // in flight no longer cost registers, so HBM stays busy.
-constexpr int kMpStages = 4;
-constexpr int kMpRB = 8;   // output rows per band
-constexpr int kMpThreads = 128;
+constexpr int kMpMaxStages = 16;
 
 __device__ __forceinline__ void mp_mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
@@ -160,22 +161,23 @@ __device__ __forceinline__ void mp_mbar_wait(uint32_t bar, uint32_t parity) {
       : "memory");
 }
 
-__global__ void __launch_bounds__(kMpThreads) maxpool3s2_bulk_kernel(const float* __restrict__ in,
-                                                                     float* __restrict__ out,
-                                                                     MaxpoolParams p, int nband,
-                                                                     long long n_items) {
+template <int NT, int RB, bool TM>
+__global__ void __launch_bounds__(NT) maxpool3s2_bulk_kernel(const float* __restrict__ in,
+                                                             float* __restrict__ out, MaxpoolParams p,
+                                                             int nband, long long n_items, int ns,
+                                                             const __grid_constant__ CUtensorMap rows_map) {
   extern __shared__ __align__(128) float sbuf[];
   const int H = p.H, W = p.W, Ho = p.Ho, Wo = p.Wo;
-  const int rows_max = 2 * kMpRB + 1;
-  const int stage_floats = rows_max * W;
-  __shared__ __align__(8) unsigned long long bars[kMpStages];
+  const int rows_max = 2 * RB + 1;
+  const int stage_floats = ((rows_max * W * 4 + 127) / 128) * 32;  // 128-B aligned stages (TMA)
+  __shared__ __align__(8) unsigned long long bars[kMpMaxStages];
   const uint32_t bar0 = smem_u32(&bars[0]);
   const uint32_t buf0 = smem_u32(sbuf);
   auto rows_of = [&](long long item, int& r0, int& nr) {
     const int band = static_cast<int>(item % nband);
-    const int y0 = band * kMpRB;
+    const int y0 = band * RB;
     const int lo = max(0, 2 * y0 - 1);
-    const int hi = min(H - 1, 2 * (y0 + kMpRB) - 1);
+    const int hi = min(H - 1, 2 * (y0 + RB) - 1);
     r0 = lo;
     nr = hi - lo + 1;
   };
@@ -183,36 +185,58 @@ __global__ void __launch_bounds__(kMpThreads) maxpool3s2_bulk_kernel(const float
     int r0, nr;
     rows_of(item, r0, nr);
     const long long plane = item / nband;
-    const float* src = in + (plane * H + r0) * (long long)W;
-    const uint32_t bytes = static_cast<uint32_t>(nr) * W * 4u;
     const uint32_t bar = bar0 + 8u * st;
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                 ::"r"(buf0 + 4u * st * stage_floats), "l"(src), "r"(bytes), "r"(bar) : "memory");
+    if (TM) {
+      // one tensor-map box of 2 RB + 1 rows of the [planes * H][W] matrix
+      // (rows past the last plane are zero-filled and never read)
+      const uint32_t bytes = static_cast<uint32_t>(2 * RB + 1) * W * 4u;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+          "[%4];" ::"r"(buf0 + 4u * st * stage_floats),
+          "l"(reinterpret_cast<uint64_t>(&rows_map)), "r"(0), "r"(static_cast<int>(plane * H + r0)), "r"(bar)
+          : "memory");
+    } else {
+      const float* src = in + (plane * H + r0) * (long long)W;
+      const uint32_t bytes = static_cast<uint32_t>(nr) * W * 4u;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(buf0 + 4u * st * stage_floats), "l"(src), "r"(bytes), "r"(bar) : "memory");
+    }
   };
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < kMpStages; ++i) mp_mbar_init(bar0 + 8u * i, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
   const long long first = blockIdx.x;
   const long long step = gridDim.x;
+  pdl_launch_dependents();
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < ns; ++i) mp_mbar_init(bar0 + 8u * i, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    // warm L2 with this CTA's first bands while the previous launch drains
+    for (int i = 0; i < ns; ++i) {
+      const long long item = first + i * step;
+      if (item >= n_items) break;
+      int r0, nr;
+      rows_of(item, r0, nr);
+      prefetch_l2(in + ((item / nband) * H + r0) * (long long)W, static_cast<uint32_t>(nr) * W * 4u);
+    }
+  }
+  __syncthreads();
+  pdl_wait();
   if (threadIdx.x == 0)
-    for (int i = 0; i < kMpStages; ++i)
+    for (int i = 0; i < ns; ++i)
       if (first + i * step < n_items) issue(first + i * step, i);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int it = 0;
   for (long long item = first; item < n_items; item += step, ++it) {
-    const int st = it % kMpStages;
-    const uint32_t parity = (it / kMpStages) & 1;
+    const int st = it % ns;
+    const uint32_t parity = (it / ns) & 1;
     mp_mbar_wait(bar0 + 8u * st, parity);
     int r0, nr;
     rows_of(item, r0, nr);
     const long long plane = item / nband;
-    const int y0 = static_cast<int>(item % nband) * kMpRB;
+    const int y0 = static_cast<int>(item % nband) * RB;
     const float* sb = sbuf + st * stage_floats;
-    // warp w computes output rows y0 + w, y0 + w + 4 (RB = 8, 4 warps)
-    for (int yy = warp; yy < kMpRB; yy += kMpThreads / 32) {
+    // warp w computes output rows y0 + w, y0 + w + NT/32, ...
+    for (int yy = warp; yy < RB; yy += NT / 32) {
       const int y = y0 + yy;
       if (y >= Ho) break;
       for (int c4 = lane; c4 * 4 < W; c4 += 32) {
@@ -237,7 +261,7 @@ __global__ void __launch_bounds__(kMpThreads) maxpool3s2_bulk_kernel(const float
       }
     }
     __syncthreads();  // everyone is done with stage st: refill it
-    if (threadIdx.x == 0 && item + kMpStages * step < n_items) issue(item + kMpStages * step, st);
+    if (threadIdx.x == 0 && item + ns * step < n_items) issue(item + ns * step, st);
   }
 }
 
@@ -253,19 +277,48 @@ merit_status launch_maxpool(const merit_plan& plan, const void* a, void* out, vo
   const bool aligned = (reinterpret_cast<uintptr_t>(in) % 16 == 0) &&
                        (reinterpret_cast<uintptr_t>(out) % 8 == 0);
   if (p.fast && aligned && p.W % 4 == 0) {
-    const int nband = (p.Ho + kMpRB - 1) / kMpRB;
+    // bands of RB output rows (2 RB + 1 input rows, one bulk copy each);
+    // 7 four-warp CTAs per SM with a 4..8-band ring keep ~200 KB of copies in
+    // flight per SM, which is what the HBM stream needs at this size
+    int RBv = 8;
+    if (const char* re = getenv("MERIT_MP_RB")) RBv = atoi(re) == 4 ? 4 : 8;
+    const int nband = (p.Ho + RBv - 1) / RBv;
     const long long items = p.planes * nband;
-    const size_t smem = (size_t)kMpStages * (2 * kMpRB + 1) * p.W * 4;
+    int ctas = 7;
+    if (const char* ce = getenv("MERIT_MP_CTAS")) ctas = atoi(ce);
+    const size_t stage = ((size_t)(2 * RBv + 1) * p.W * 4 + 127) / 128 * 128;
+    int ns = RBv == 4 ? 8 : 4;
+    if (const char* se = getenv("MERIT_MP_STAGES")) ns = atoi(se);
+    if (ns > kMpMaxStages) ns = kMpMaxStages;
+    while (ns > 2 && ns * stage > 100 * 1024) --ns;
+    const size_t smem = ns * stage;
     if (smem <= 200 * 1024) {
-      cudaError_t e = set_smem_attr(maxpool3s2_bulk_kernel,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return cuda_check(e, "set_smem_attr(maxpool)");
-      int per_sm = static_cast<int>((220 * 1024) / (smem + 1024));
-      if (per_sm > 8) per_sm = 8;
-      if (per_sm < 1) per_sm = 1;
-      long long grid = (long long)num_sms() * per_sm;
+      long long grid = (long long)num_sms() * ctas;
       if (grid > items) grid = items;
-      maxpool3s2_bulk_kernel<<<static_cast<unsigned>(grid), kMpThreads, smem, s>>>(in, o, p, nband, items);
+      // band loads: a 2-D tensor map over the [planes * H][W] rows (UTMALDG),
+      // or plain bulk copies (MERIT_MP_TMAP=0)
+      CUtensorMap rmap;
+      std::memset(&rmap, 0, sizeof(rmap));
+      const char* te = getenv("MERIT_MP_TMAP");
+      bool tm = !(te && te[0] == '0') && tensor_map_encoder() != nullptr && p.W <= 256 &&
+                p.planes * p.H < (1LL << 31);
+      if (tm) {
+        const cuuint64_t dims[2] = {(cuuint64_t)p.W, (cuuint64_t)(p.planes * p.H)};
+        const cuuint64_t strides[1] = {(cuuint64_t)p.W * 4};
+        const cuuint32_t box[2] = {(cuuint32_t)p.W, (cuuint32_t)(2 * RBv + 1)};
+        const cuuint32_t estr[2] = {1, 1};
+        tm = tensor_map_encoder()(&rmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(in), dims, strides,
+                                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+      }
+      auto k = RBv == 4 ? (tm ? maxpool3s2_bulk_kernel<128, 4, true> : maxpool3s2_bulk_kernel<128, 4, false>)
+                        : (tm ? maxpool3s2_bulk_kernel<128, 8, true> : maxpool3s2_bulk_kernel<128, 8, false>);
+      cudaError_t e = set_smem_attr(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return cuda_check(e, "set_smem_attr(maxpool)");
+      e = launch_pdl(k, dim3(static_cast<unsigned>(grid)), dim3(128), smem, s, 1, in, o, p, nband, items, ns,
+                     rmap);
+      if (e != cudaSuccess) return cuda_check(e, "launch(maxpool3s2_bulk_kernel)");
       return launch_status("maxpool3s2_bulk_kernel");
     }
     constexpr int RB = 4;

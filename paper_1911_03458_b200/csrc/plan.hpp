@@ -150,6 +150,7 @@ merit_status launch_conv(const merit_plan& plan, const void* a, const void* pack
 // Check a CUDA status from C++ host code; returns MERIT_E_CUDA with context.
 merit_status cuda_check(int err, const char* what);
 void count_launch(int n = 1);
+void note_kernel(const char* name);  // static string: last kernel launched
 
 int64_t elem_size(int dtype);
 

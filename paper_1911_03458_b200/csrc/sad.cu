@@ -177,6 +177,8 @@ sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, voi
   }
   long long tile = blockIdx.x;
   int buf = 0;
+  pdl_launch_dependents();
+  pdl_wait();  // first global access follows
   if (tile < L.n_tiles) {
     stage_tile<BLK>(L, cur, ref, tile, smem_u32(raw0), reinterpret_cast<uint8_t*>(raw0),
                     smem_u32(cur0), reinterpret_cast<uint8_t*>(cur0));
@@ -341,7 +343,8 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
   const int threads = (L.items + 31) / 32 * 32;
   long long grid = 2LL * num_sms();
   if (grid > L.n_tiles) grid = L.n_tiles;
-  kern<<<static_cast<unsigned>(grid), threads, smem, s>>>(cur, ref, out, aux, L);
+  e = launch_pdl(kern, dim3(static_cast<unsigned>(grid)), dim3(threads), smem, s, 1, cur, ref, out, aux, L);
+  if (e != cudaSuccess) return cuda_check(e, "launch(sad)");
   return launch_status("sad_kernel");
 }
 
