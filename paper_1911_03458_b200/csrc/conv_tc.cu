@@ -682,6 +682,9 @@ merit_status launch_conv_pack(const merit_plan& plan, const void* b, void* packe
 
 bool conv_tap3_eligible(const ConvParams& p);
 bool conv_tma_eligible(const ConvParams& p, const void* a);
+bool conv_s1_eligible(const ConvParams& p, const void* a);
+merit_status launch_conv_s1(const merit_plan& plan, const void* a, const void* packed_b, void* out,
+                            void* stream);
 merit_status launch_conv_tma(const merit_plan& plan, const void* a, const void* packed_b, void* out,
                              void* stream);
 merit_status launch_conv_tap3(const merit_plan& plan, const void* a, const void* packed_b, void* out,
@@ -695,6 +698,8 @@ merit_status launch_conv(const merit_plan& plan, const void* a, const void* pack
     const bool force_general = kern && kern[0] == 'g';
     if (!force_general && conv_tma_eligible(p, a) && (reinterpret_cast<uintptr_t>(out) % 16) == 0)
       return launch_conv_tma(plan, a, packed_b, out, stream);
+    if (!force_general && conv_s1_eligible(p, a) && (reinterpret_cast<uintptr_t>(out) % 4) == 0)
+      return launch_conv_s1(plan, a, packed_b, out, stream);
     if (!force_general && conv_tap3_eligible(p) &&
         (reinterpret_cast<uintptr_t>(a) % 4) == 0)
       return launch_conv_tap3(plan, a, packed_b, out, stream);

@@ -1,0 +1,493 @@
+// K3d — stride-1, 3-wide convolution with the three horizontal taps stacked
+// along the MMA's N dimension (the C3 shape: NCHW fp32, 3x3, stride 1, pad 1,
+// Cout <= 80).
+//
+// For a fixed kernel row ky and channel block, the tap-kx partial sums
+//   P_kx[x][co] = sum_ci in[ci][y + ky - 1][x] * w[co][ci][ky][kx]
+// are ONE product A x B with A = input columns (M = 128 slots) and
+// B = the three tap matrices stacked (N = 3 * Cout).  The convolution is
+//   out[x] = P_0[x - 1] + P_1[x] + P_2[x + 1],
+// so the epilogue applies the column shifts with warp shuffles.  Compared
+// with three N = Cout MMAs per k-step, each A tile is read by the tensor core
+// once instead of three times, which is what bounds the narrow-Cout case
+// (shared-memory bandwidth, not MMA issue).
+//
+// Gather: one TMA tensor load per (tile, ky, 32-channel half) lands the raw
+// rows [c][rows][W] (zero fill = the view's zero padding in y and c); eight
+// repack warps split fp32 into bf16 hi/lo (3-product split: hi*hi + hi*lo +
+// lo*hi) and write the K-major SW128 A planes.  Slots: `slots` per output
+// row (power of two >= W + 2), input column x at slot x + 1, so every row
+// carries the zero columns x = -1 and x = W the shifts read.
+//
+// Warps: 0-7 repack, 8 B loader + TMEM alloc, 9 MMA, 10-13 and 15-18
+// epilogue (two sets, alternating 8-channel chunks), 14 TMA.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "tc_common.cuh"
+#include "tmap.cuh"
+
+namespace merit_dev {
+namespace {
+
+using namespace tc;
+
+constexpr int kRepackWarps = 8;
+constexpr int kRepackers = kRepackWarps * 32;
+constexpr int kWarpB = 8, kWarpMma = 9, kWarpEpi0 = 10, kWarpTma = 14, kWarpEpi1 = 15;
+constexpr int kThreads = 19 * 32;
+constexpr int kEpiWarps = 8;  // two sets of four (one warp per TMEM lane quadrant each)
+constexpr int kEC = 8;        // output channels per epilogue chunk
+constexpr int kMaxRing = 8;
+constexpr uint32_t kAccCols = 256;  // TMEM columns per accumulator (N <= 240)
+
+struct S1Args {
+  ConvParams p;
+  const uint8_t* wpk;
+  float* out;
+  int slots_log2;      // slots per output row = 1 << slots_log2
+  int rows;            // output rows per tile = 128 / slots
+  int tiles_per_img;   // ceil(Ho / rows)
+  int n_tiles;
+  int n_groups;        // KH * CB
+  uint32_t raw_bytes;  // W * rows * 32 ch * 4 (half a 64-channel k-block)
+  uint32_t a_slot;     // nsplit planes x 16 KB
+  uint32_t b_plane;    // BN * 128: one tap, one split plane
+  uint32_t b_slot;     // 3 taps x nsplit planes
+  int nr, na, nb;
+  unsigned long long* prof;  // MERIT_CONV_DEBUG & 64: per-warp [total, wait1, wait2, wait3]
+  int debug;
+};
+
+__device__ __forceinline__ void tma_load_4d_s1(uint32_t dst, const CUtensorMap* map, int x, int y, int c, int n,
+                                               uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(c), "r"(n), "r"(bar)
+      : "memory");
+}
+
+__device__ __forceinline__ void twait_s1(uint32_t bar, uint32_t par, unsigned long long& acc, bool on) {
+  if (on) {
+    const unsigned long long t0 = clock64();
+    mbar_wait(bar, par);
+    acc += clock64() - t0;
+  } else {
+    mbar_wait(bar, par);
+  }
+}
+
+template <bool SPLIT3>
+__global__ void __maxnreg__(96)  // 19 warps: <= 5 per SM sub-partition x 96 regs
+conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
+  extern __shared__ uint8_t smem_raw[];
+  const ConvParams& p = A.p;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  const uint32_t aring = base;                          // na x a_slot
+  const uint32_t bring = aring + A.na * A.a_slot;       // nb x b_slot
+  const uint32_t rring = bring + A.nb * A.b_slot;       // nr x raw_bytes
+  const uint32_t xring = rring + A.nr * A.raw_bytes;    // epilogue edge exchange
+  const uint32_t bars = xring + 2 * 2 * 4 * 16 * 4;  // [set][parity][warp][8 P0 | 8 P2]
+  auto r_full = [&](int s) { return bars + 8u * s; };
+  auto r_empty = [&](int s) { return bars + 8u * (kMaxRing + s); };
+  auto a_full = [&](int s) { return bars + 8u * (2 * kMaxRing + s); };
+  auto a_empty = [&](int s) { return bars + 8u * (3 * kMaxRing + s); };
+  auto b_full = [&](int s) { return bars + 8u * (4 * kMaxRing + s); };
+  auto b_empty = [&](int s) { return bars + 8u * (5 * kMaxRing + s); };
+  auto tfull = [&](int a) { return bars + 8u * (6 * kMaxRing + a); };
+  auto tempty = [&](int a) { return bars + 8u * (6 * kMaxRing + 2 + a); };
+  const uint32_t tmem_slot = bars + 8u * (6 * kMaxRing + 4);
+  volatile uint32_t* tmem_slot_ptr =
+      reinterpret_cast<volatile uint32_t*>(smem_raw + (tmem_slot - smem_u32(smem_raw)));
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < A.nr; ++s) {
+      mbar_init(r_full(s), 1);
+      mbar_init(r_empty(s), kRepackers / 2);  // one half of the repack warps
+    }
+    for (int s = 0; s < A.na; ++s) {
+      mbar_init(a_full(s), kRepackWarps);  // one elected lane per repack warp
+      mbar_init(a_empty(s), 1);
+    }
+    for (int s = 0; s < A.nb; ++s) {
+      mbar_init(b_full(s), 1);
+      mbar_init(b_empty(s), 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull(a), 1);
+      mbar_init(tempty(a), kEpiWarps);  // one elected lane per epilogue warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == kWarpB) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(tmem_slot),
+                 "r"(2 * kAccCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot_ptr;
+  pdl_launch_dependents();
+  pdl_wait();  // prologue done: from here on global memory is touched
+  const int BN = p.BN;
+  const int W = p.W;
+  const int slots_mask = (1 << A.slots_log2) - 1;
+  const bool pon = (A.debug & 64) && lane == 0 && warp < 16;
+  unsigned long long w1 = 0, w2 = 0, w3 = 0;
+  const unsigned long long t_start = clock64();
+
+  if (warp == kWarpTma) {
+    // ============ raw-row loader: the MERIT gather on the TMA engine ======
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&in_map)) : "memory");
+      int st = 0;
+      uint32_t ph = 0;
+      for (int tile = blockIdx.x; tile < A.n_tiles; tile += gridDim.x) {
+        const int n = tile / A.tiles_per_img;
+        const int y0 = (tile - n * A.tiles_per_img) * A.rows;
+        for (int g = 0; g < A.n_groups; ++g) {
+          const int ky = g / p.CB, cb = g - ky * p.CB;
+          for (int h = 0; h < 2; ++h) {
+            twait_s1(r_empty(st), ph ^ 1, w1, pon);
+            mbar_expect_tx(r_full(st), A.raw_bytes);
+            // input rows y0 + ky*dy + oy + {0 .. rows-1}, all W columns, 32
+            // channels; rows / channels out of range read as zero
+            tma_load_4d_s1(rring + st * A.raw_bytes, &in_map, 0, y0 + ky * p.dy + p.oy, cb * 64 + 32 * h, n,
+                           r_full(st));
+            if (++st == A.nr) { st = 0; ph ^= 1; }
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp < kRepackWarps) {
+    // ============ repack: raw fp32 [c][r][W] -> bf16 hi/lo K-major planes ===
+    // warp w: channels 8w..8w+7 of the k-block (chunk column w of every A
+    // row; warps 0-3 read the even raw entries = channels 0-31, warps 4-7
+    // the odd ones); lane l: A rows 32j + l, j = 0..3, so an STS.128 phase
+    // writes 8 consecutive rows and the 128-B swizzle spreads the banks.
+    const int w = warp;
+    const uint32_t rowf = static_cast<uint32_t>(W);  // floats per raw row
+    const uint32_t cbase = static_cast<uint32_t>(8 * (w & 3)) * A.rows * rowf * 4u;
+    int rs = w >> 2, as = 0;
+    uint32_t rph = 0, aph = 0;
+    for (int tile = blockIdx.x; tile < A.n_tiles; tile += gridDim.x) {
+      for (int g = 0; g < A.n_groups; ++g) {
+        twait_s1(r_full(rs), rph, w1, pon);
+        float v[4][8];
+        const uint32_t src = rring + rs * A.raw_bytes + cbase;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int arow = 32 * j + lane;
+          const int r = arow >> A.slots_log2;
+          const int x = (arow & slots_mask) - 1;
+          const bool ok = x >= 0 && x < W;
+          const uint32_t a0 = src + (static_cast<uint32_t>(r) * rowf + (ok ? x : 0)) * 4u;
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            float t = 0.f;
+            if (ok) asm volatile("ld.shared.f32 %0, [%1];" : "=f"(t) : "r"(a0 + c * A.rows * rowf * 4u));
+            v[j][c] = t;
+          }
+        }
+        mbar_arrive(r_empty(rs));
+        rs += 2;
+        while (rs >= A.nr) { rs -= A.nr; rph ^= 1; }
+        twait_s1(a_empty(as), aph ^ 1, w2, pon);
+        const uint32_t phi = aring + as * A.a_slot;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int row = 32 * j + lane;
+          const uint32_t off = (row >> 3) * 1024u + (row & 7) * 128u + (((uint32_t)w ^ (uint32_t)(row & 7)) << 4);
+          uint32_t hi[4], lo[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) split_bf16x2(v[j][2 * c], v[j][2 * c + 1], hi[c], lo[c]);
+          st_shared_v4(phi + off, hi[0], hi[1], hi[2], hi[3]);
+          if (SPLIT3) st_shared_v4(phi + kAPlane + off, lo[0], lo[1], lo[2], lo[3]);
+        }
+        fence_proxy_async();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(a_full(as));
+        if (++as == A.na) { as = 0; aph ^= 1; }
+      }
+    }
+  } else if (warp == kWarpB) {
+    // ============ B loader: stack the three tap matrices along N ==========
+    // packed (conv_pack_kernel) k-block (ky, cb, kx) = [hi][lo] planes of
+    // BN rows; the slot holds [hi: kx 0 | 1 | 2][lo: kx 0 | 1 | 2], i.e. one
+    // K-major SW128 image of N = 3 BN rows per split plane.
+    if (lane == 0) {
+      constexpr int nsp = SPLIT3 ? 2 : 1;
+      int st = 0;
+      uint32_t ph = 0;
+      for (int tile = blockIdx.x; tile < A.n_tiles; tile += gridDim.x) {
+        for (int g = 0; g < A.n_groups; ++g) {
+          twait_s1(b_empty(st), ph ^ 1, w1, pon);
+          mbar_expect_tx(b_full(st), A.b_slot);
+          for (int kx = 0; kx < 3; ++kx)
+            for (int sp = 0; sp < nsp; ++sp)
+              bulk_g2s(bring + st * A.b_slot + (sp * 3 + kx) * A.b_plane,
+                       A.wpk + ((long long)(g * 3 + kx) * nsp + sp) * A.b_plane, A.b_plane, b_full(st));
+          if (++st == A.nb) { st = 0; ph ^= 1; }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == kWarpMma) {
+    // ============ MMA issuer ===================================================
+    if (lane == 0) {
+      const uint32_t idesc = make_idesc(3 * BN);
+      const uint32_t b_lo = 3 * A.b_plane;
+      int as = 0, bs = 0, acc = 0;
+      uint32_t aph = 0, bph = 0, acc_phase = 0;
+      for (int tile = blockIdx.x; tile < A.n_tiles; tile += gridDim.x) {
+        twait_s1(tempty(acc), acc_phase ^ 1, w3, pon);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * kAccCols;
+        for (int g = 0; g < A.n_groups; ++g) {
+          twait_s1(a_full(as), aph, w1, pon);
+          twait_s1(b_full(bs), bph, w2, pon);
+          tc_fence_after();
+          const uint32_t a0 = aring + as * A.a_slot;
+          const uint32_t b0 = bring + bs * A.b_slot;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            tc_mma(d_tmem, sw128_desc(a0 + 32 * k), sw128_desc(b0 + 32 * k), idesc, (g > 0 || k > 0) ? 1u : 0u);
+            if (SPLIT3) {
+              tc_mma(d_tmem, sw128_desc(a0 + 32 * k), sw128_desc(b0 + b_lo + 32 * k), idesc, 1u);
+              tc_mma(d_tmem, sw128_desc(a0 + kAPlane + 32 * k), sw128_desc(b0 + 32 * k), idesc, 1u);
+            }
+          }
+          tc_commit(b_empty(bs));
+          if (++bs == A.nb) { bs = 0; bph ^= 1; }
+          tc_commit(a_empty(as));
+          if (++as == A.na) { as = 0; aph ^= 1; }
+        }
+        tc_commit(tfull(acc));
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+    __syncwarp();
+  } else if ((warp >= kWarpEpi0 && warp < kWarpEpi0 + 4) || warp >= kWarpEpi1) {
+    // ============ epilogue: out[x] = P0[x-1] + P1[x] + P2[x+1] =============
+    // Warp quadrant q holds A rows 32q..32q+31; set k (0: warps 10-13,
+    // 1: warps 15-18) takes chunks of kEC channels c0 = kEC * (2i + k).  The
+    // x-1 / x+1 neighbours are lane shuffles; across a warp boundary the
+    // edge values go through a small shared exchange (double-buffered by
+    // chunk, one named barrier per set and chunk).
+    const int q = warp & 3;
+    const int set = warp >= kWarpEpi1 ? 1 : 0;
+    const int arow = 32 * q + lane;
+    const int r = arow >> A.slots_log2;
+    const int x = (arow & slots_mask) - 1;
+    const bool relu = p.post == POST_RELU;
+    const bool first = lane == 0, last = lane == 31;
+    const bool has_prev = q > 0, has_next = q < 3;
+    const uint32_t xset = xring + static_cast<uint32_t>(set) * (2 * 4 * 16 * 4);
+    const int n_chunks = BN / kEC;
+    const int my_last = ((n_chunks - 1 - set) / 2) * 2 + set;  // this set's last chunk
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    int par = 0;
+    for (int tile = blockIdx.x; tile < A.n_tiles; tile += gridDim.x) {
+      const int n = tile / A.tiles_per_img;
+      const int y = (tile - n * A.tiles_per_img) * A.rows + r;
+      const bool store = x >= 0 && x < W && y < p.Ho && !(A.debug & 128);
+      float* dst = A.out + ((long long)n * p.Cout * p.Ho + y) * W + x;
+      const long long co_stride = (long long)p.Ho * W;
+      twait_s1(tfull(acc), acc_phase, w1, pon);
+      tc_fence_after();
+      if (A.debug & 1024) {  // timing experiment: release the accumulator unread
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tempty(acc));
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        continue;
+      }
+      const uint32_t t_row = tmem_base + acc * kAccCols + (static_cast<uint32_t>(q * 32) << 16);
+      for (int ch = set; ch < n_chunks; ch += 2) {
+        const int c0 = ch * kEC;
+        uint32_t p0[kEC], p1[kEC], p2[kEC];
+        TMEM_LD8(t_row + c0, p0);
+        TMEM_LD8(t_row + BN + c0, p1);
+        TMEM_LD8(t_row + 2 * BN + c0, p2);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (ch == my_last) {  // accumulator drained by this warp
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(tempty(acc));
+        }
+        // edge values for the neighbouring warps: lane 31's P0, lane 0's P2
+        const uint32_t xb = xset + static_cast<uint32_t>((par * 4 + q) * 16) * 4u;
+        if (last) {
+          st_shared_v4(xb, p0[0], p0[1], p0[2], p0[3]);
+          st_shared_v4(xb + 16u, p0[4], p0[5], p0[6], p0[7]);
+        }
+        if (first) {
+          st_shared_v4(xb + 32u, p2[0], p2[1], p2[2], p2[3]);
+          st_shared_v4(xb + 48u, p2[4], p2[5], p2[6], p2[7]);
+        }
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + set) : "memory");
+        // every lane loads the (warp-uniform, broadcast) neighbour edges and
+        // selects them on lane 0 / 31: no divergent branches in the loop
+        uint32_t xp[kEC], xn[kEC];
+        const uint32_t xpa = xset + static_cast<uint32_t>((par * 4 + ((q + 3) & 3)) * 16) * 4u;
+        const uint32_t xna = xset + static_cast<uint32_t>((par * 4 + ((q + 1) & 3)) * 16 + 8) * 4u;
+#pragma unroll
+        for (int e = 0; e < kEC; e += 4) {
+          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(xp[e]), "=r"(xp[e + 1]), "=r"(xp[e + 2]), "=r"(xp[e + 3])
+                       : "r"(xpa + 4u * e));
+          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(xn[e]), "=r"(xn[e + 1]), "=r"(xn[e + 2]), "=r"(xn[e + 3])
+                       : "r"(xna + 4u * e));
+        }
+        const int cmax = p.Cout - c0;  // channels of this chunk that exist
+        float* ptr = dst + (long long)c0 * co_stride;
+#pragma unroll
+        for (int e = 0; e < kEC; ++e) {
+          float left = __shfl_up_sync(0xffffffffu, __uint_as_float(p0[e]), 1);
+          float right = __shfl_down_sync(0xffffffffu, __uint_as_float(p2[e]), 1);
+          left = first ? (has_prev ? __uint_as_float(xp[e]) : 0.f) : left;
+          right = last ? (has_next ? __uint_as_float(xn[e]) : 0.f) : right;
+          float v = __fadd_rn(__fadd_rn(left, __uint_as_float(p1[e])), right);
+          v = relu ? fmaxf(v, 0.f) : __fadd_rn(v, 0.f);
+          if (store && e < cmax) *ptr = v;
+          ptr += co_stride;
+        }
+        par ^= 1;
+      }
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+  if (pon) {
+    unsigned long long* pr = A.prof + (blockIdx.x * 16 + warp) * 4;
+    pr[0] = clock64() - t_start; pr[1] = w1; pr[2] = w2; pr[3] = w3;
+  }
+  __syncthreads();
+  if (warp == kWarpB) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * kAccCols)
+                 : "memory");
+  }
+}
+
+int slots_log2_for(int W) {
+  for (int l = 5; l <= 7; ++l)
+    if (W + 2 <= (1 << l)) return l;
+  return -1;
+}
+
+}  // namespace
+
+// Geometric eligibility (plan time: decides nothing about packing, which is
+// shared with the other conv kernels).
+bool conv_s1_eligible(const ConvParams& p, const void* a) {
+  const char* e = getenv("MERIT_CONV_S1");
+  if (e && e[0] == '0') return false;
+  return p.KW == 3 && p.dx == 1 && p.ox == -1 && p.sx == 1 && p.sy == 1 && p.Wo == p.W && !p.in_bf16 &&
+         p.n_tiles_n == 1 && 3 * p.BN <= 240 && p.BN % 16 == 0 && slots_log2_for(p.W) > 0 && p.W % 4 == 0 &&
+         (reinterpret_cast<uintptr_t>(a) % 16) == 0 && tensor_map_encoder() != nullptr;
+}
+
+merit_status launch_conv_s1(const merit_plan& plan, const void* a, const void* packed_b, void* out,
+                            void* stream) {
+  const ConvParams& p = plan.conv;
+  S1Args A;
+  A.p = p;
+  A.wpk = static_cast<const uint8_t*>(packed_b);
+  A.out = static_cast<float*>(out);
+  A.slots_log2 = slots_log2_for(p.W);
+  A.rows = 128 >> A.slots_log2;
+  A.tiles_per_img = (p.Ho + A.rows - 1) / A.rows;
+  A.n_tiles = p.N * A.tiles_per_img;
+  A.n_groups = p.KH * p.CB;
+  const bool split3 = p.split == 3;
+  const uint32_t nsp = split3 ? 2u : 1u;
+  A.raw_bytes = static_cast<uint32_t>(p.W) * A.rows * 32u * 4u;
+  A.a_slot = nsp * kAPlane;
+  A.b_plane = static_cast<uint32_t>(p.BN) * 128u;
+  A.b_slot = 3u * nsp * A.b_plane;
+  const size_t fixed = 1024 + 2 * 2 * 4 * 16 * 4 + 8 * (6 * kMaxRing + 4) + 16;
+  const size_t budget = 227 * 1024 - fixed;
+  A.na = 2;
+  A.nb = 2;
+  A.nr = 2;
+  auto used_bytes = [&]() {
+    return A.na * (size_t)A.a_slot + A.nb * (size_t)A.b_slot + A.nr * (size_t)A.raw_bytes;
+  };
+  for (;;) {  // grow: raw (even), A, B
+    const size_t used = used_bytes();
+    if (A.nr < 4 && used + 2 * A.raw_bytes <= budget) { A.nr += 2; continue; }
+    if (A.na < 3 && used + A.a_slot <= budget) { ++A.na; continue; }
+    if (A.nb < 3 && used + A.b_slot <= budget) { ++A.nb; continue; }
+    break;
+  }
+  if (const char* re = getenv("MERIT_S1_RINGS")) {  // "na,nb,nr" (tuning)
+    int na, nb, nr;
+    if (sscanf(re, "%d,%d,%d", &na, &nb, &nr) == 3 && na >= 1 && nb >= 1 && nr >= 2 && nr % 2 == 0 &&
+        na <= kMaxRing && nb <= kMaxRing && nr <= kMaxRing) {
+      A.na = na; A.nb = nb; A.nr = nr;
+    }
+  }
+  if (used_bytes() > budget) return fail(MERIT_E_UNSUPPORTED_VIEW, "stride-1 conv rings exceed shared memory");
+  const size_t smem = fixed + used_bytes();
+  CUtensorMap map;
+  const cuuint64_t dims[4] = {(cuuint64_t)p.W, (cuuint64_t)p.H, (cuuint64_t)p.Cin, (cuuint64_t)p.N};
+  const cuuint64_t strides[3] = {(cuuint64_t)p.W * 4, (cuuint64_t)p.H * p.W * 4,
+                                 (cuuint64_t)p.Cin * p.H * p.W * 4};
+  const cuuint32_t box[4] = {(cuuint32_t)p.W, (cuuint32_t)A.rows, 32, 1};
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult cr = tensor_map_encoder()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(a), dims, strides,
+                                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (cr != CUDA_SUCCESS) return fail(MERIT_E_CUDA, "cuTensorMapEncodeTiled failed for the conv input");
+  if (A.n_tiles == 0) return MERIT_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  auto kfn = split3 ? conv_s1_kernel<true> : conv_s1_kernel<false>;
+  cudaError_t e = set_smem_attr(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return cuda_check(e, "set_smem_attr(conv_s1)");
+  int grid = num_sms();
+  if (grid > A.n_tiles) grid = A.n_tiles;
+  {
+    const char* dbg = getenv("MERIT_CONV_DEBUG");
+    A.debug = dbg ? atoi(dbg) : 0;
+  }
+  A.prof = nullptr;
+  if (A.debug & 64) {
+    cudaMalloc(&A.prof, 8ull * 4 * 16 * grid);
+    cudaMemset(A.prof, 0, 8ull * 4 * 16 * grid);
+  }
+  e = launch_pdl(kfn, dim3(grid), dim3(kThreads), smem, s, 1, map, A);
+  if (e != cudaSuccess) return cuda_check(e, "launch(conv_s1)");
+  if (A.debug & 64) {
+    cudaStreamSynchronize(s);
+    std::vector<unsigned long long> h(4 * 16 * grid);
+    cudaMemcpy(h.data(), A.prof, h.size() * 8, cudaMemcpyDeviceToHost);
+    auto frac = [&](int w0, int w1_, int idx) {
+      double t = 0, v = 0;
+      for (int b = 0; b < grid; ++b)
+        for (int ww = w0; ww < w1_; ++ww) { t += h[(b * 16 + ww) * 4]; v += h[(b * 16 + ww) * 4 + idx]; }
+      return t > 0 ? 100.0 * v / t : 0.0;
+    };
+    fprintf(stderr,
+            "[s1 prof] rings nr=%d na=%d nb=%d | tma: r_empty-wait %.1f%% | repack: r_full-wait %.1f%% a_empty-wait "
+            "%.1f%% | B: b_empty-wait %.1f%% | mma: a_full %.1f%% b_full %.1f%% tempty %.1f%% | epi: tfull-wait "
+            "%.1f%%\n",
+            A.nr, A.na, A.nb, frac(kWarpTma, kWarpTma + 1, 1), frac(0, 8, 1), frac(0, 8, 2), frac(kWarpB, kWarpB + 1, 1),
+            frac(kWarpMma, kWarpMma + 1, 1), frac(kWarpMma, kWarpMma + 1, 2), frac(kWarpMma, kWarpMma + 1, 3),
+            frac(kWarpEpi0, kWarpEpi0 + 4, 1));
+    cudaFree(A.prof);
+  }
+  return launch_status(split3 ? "conv_s1_kernel<split3, taps stacked on N>" : "conv_s1_kernel<bf16, taps stacked on N>");
+}
+
+}  // namespace merit_dev

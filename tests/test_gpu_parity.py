@@ -215,6 +215,25 @@ def test_conv_variants_fp32(cuda, n, cin, h, wd, cout, k, s, pad, dil, relu):
         assert np.all(got >= 0)
 
 
+@pytest.mark.parametrize("variant", ["s1", "no_s1"])
+@pytest.mark.parametrize("n,cin,h,wd,cout,relu", [
+    (2, 64, 56, 56, 64, False),    # C3 geometry, 64 slots / row, 2 rows / tile
+    (1, 3, 20, 20, 16, False),     # Cin < 64, N = 48
+    (2, 64, 28, 28, 80, True),     # Cout = 80 -> N = 240, relu
+    (1, 128, 13, 12, 48, False),   # two channel blocks, 32 slots (4 rows / tile), Ho % 4 != 0
+    (3, 32, 30, 28, 32, False),    # 32 slots
+    (1, 16, 9, 124, 16, False),    # 128 slots, 1 row / tile
+])
+def test_conv_fp32_stride1_tap_stacked(cuda, monkeypatch, variant, n, cin, h, wd, cout, relu):
+    if variant == "no_s1":
+        monkeypatch.setenv("MERIT_CONV_S1", "0")
+    w = W.conv_nchw_view(n, cin, h, wd, cout, 3, 1, 1, 1, relu)
+    w.src_a = W.gen_uniform([n, cin, h, wd], 41)
+    w.src_b = W.gen_normal([cout, cin, 3, 3], 42, (2.0 / (cin * 9)) ** 0.5)
+    got = run_full(w)
+    assert rel_err(got, O.conv2d(w.src_a, w.src_b, 1, 1, 1, relu)) <= TOL_F32
+
+
 CONV_VARIANTS = {
     "default": {},                                  # TMA gather, CTA pairs where eligible
     "single": {"MERIT_CONV_PAIR": "0"},             # TMA gather, one CTA per tile
