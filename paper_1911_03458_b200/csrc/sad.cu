@@ -27,8 +27,10 @@
 //    on the packed key (sad << 16 | dy*WX + dx): lowest SAD, then lowest
 //    raster index — the tie-break BASELINE.json asks for.
 #include <cstdlib>
+#include <cstring>
 
 #include "common.cuh"
+#include "tmap.cuh"
 
 namespace merit_dev {
 namespace {
@@ -58,7 +60,7 @@ struct SadLaunch {
   int TBX;        // blocks per tile
   int G;          // dy groups
   int n_tiles_x;  // ceil(BX / TBX)
-  long long n_tiles;
+  int n_tiles;
   int R;          // staged reference rows = G*D + BH - 1
   int span;       // staged reference columns = TBX*BW + WX - 1
   int Ww;         // words per staged row per copy
@@ -67,17 +69,21 @@ struct SadLaunch {
   int items;      // TBX * WX * G
   int word_path;  // 4-byte aligned reference rows / current blocks
   int vec_path;   // 16-byte aligned reference rows
+  int tma;        // reference window + current blocks staged by TMA (ZERO_PAD)
+  int R_box;      // TMA box rows (= R)
+  int cur_pitch;  // bytes per staged current-frame row: TBX*BW rounded up to 16
+  uint32_t raw_buf, cur_buf;  // bytes per raw / current buffer (128-byte multiples)
 };
 
 template <int BLK>
 __device__ __forceinline__ void stage_tile(const SadLaunch& L, const uint8_t* __restrict__ cur,
-                                           const uint8_t* __restrict__ ref, long long tile,
+                                           const uint8_t* __restrict__ ref, int tile,
                                            uint32_t raw_s, uint8_t* raw, uint32_t cur_s,
                                            uint8_t* curs) {
   const SadParams& p = L.p;
-  const int tx = static_cast<int>(tile % L.n_tiles_x);
-  const long long t2 = tile / L.n_tiles_x;
-  const int by = static_cast<int>(t2 % p.BY);
+  const int tx = tile % L.n_tiles_x;
+  const int t2 = tile / L.n_tiles_x;
+  const int by = t2 % p.BY;
   const long long pair = t2 / p.BY;
   const int bx0 = tx * L.TBX;
   const int nb = min(L.TBX, p.BX - bx0);
@@ -112,7 +118,8 @@ __device__ __forceinline__ void stage_tile(const SadLaunch& L, const uint8_t* __
       if (lane < BWW) {
         const bool in = b < nb;
         const int y = by * BLK + r + p.cy, x = (bx0 + b) * BLK + lane * 4 + p.cx;
-        cp_async4(cur_s + 4u * (rr * BWW + lane), in ? curp + (long long)y * p.Wc + x : curp, in);
+        cp_async4(cur_s + static_cast<uint32_t>(r * L.cur_pitch + b * BLK + 4 * lane),
+                  in ? curp + (long long)y * p.Wc + x : curp, in);
       }
     }
   } else {
@@ -142,28 +149,84 @@ __device__ __forceinline__ void stage_tile(const SadLaunch& L, const uint8_t* __
           const int y = by * BLK + r + p.cy, x = (bx0 + b) * BLK + c + p.cx;
           v = __ldg(curp + (long long)y * p.Wc + x);
         }
-        curs[rr * BLK + c] = v;
+        curs[r * L.cur_pitch + b * BLK + c] = v;
       }
     }
+  }
+}
+
+// TMA boxes of 8-bit tensors must start at a 16-byte multiple in the
+// innermost dimension (measured on sm_100a, tools/microbench/tma_u8.cu: any
+// other start faults with an illegal instruction), so boxes start at
+// floor16(x) and the kernel skips the 0..15 leading bytes.
+__host__ __device__ __forceinline__ int floor16(int x) { return x >= 0 ? (x & ~15) : -((-x + 15) & ~15); }
+
+__device__ __forceinline__ void sad_tma_3d(uint32_t dst, const CUtensorMap* map, int x, int y, int z,
+                                           uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void sad_mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "LAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE;\n\t"
+      "bra LAB_WAIT;\n\t"
+      "DONE:\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+// One tile's staging: TMA (one 3-D box for the reference window, one for the
+// current blocks, completion on the buffer's mbarrier; zero fill outside the
+// frame = ZERO_PAD) or the cp.async / byte paths.
+template <int BLK>
+__device__ __forceinline__ void issue_tile(const SadLaunch& L, const uint8_t* __restrict__ cur,
+                                           const uint8_t* __restrict__ ref, const CUtensorMap* ref_map,
+                                           const CUtensorMap* cur_map, int tile, uint32_t raw_s, uint8_t* raw,
+                                           uint32_t cur_s, uint8_t* curs, uint32_t bar) {
+  if (L.tma) {
+    if (threadIdx.x == 0) {
+      const SadParams& p = L.p;
+      const int tx = tile % L.n_tiles_x;
+      const int t2 = tile / L.n_tiles_x;
+      const int by = t2 % p.BY;
+      const int pair = t2 / p.BY;
+      const int bx0 = tx * L.TBX;
+      const uint32_t bytes = L.R_box * L.rw * 4 + BLK * L.cur_pitch;
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+      sad_tma_3d(raw_s, ref_map, floor16(bx0 * BLK + p.ox), by * BLK + p.oy, pair, bar);
+      sad_tma_3d(cur_s, cur_map, floor16(bx0 * BLK + p.cx), by * BLK + p.cy, pair, bar);
+    }
+  } else {
+    stage_tile<BLK>(L, cur, ref, tile, raw_s, raw, cur_s, curs);
+    cp_async_commit();
   }
 }
 
 template <int BLK, int D>
 __global__ void __launch_bounds__(kSadThreads, 2)
 sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, void* __restrict__ out,
-           int32_t* __restrict__ aux, SadLaunch L) {
-  extern __shared__ __align__(16) uint32_t smem[];
+           int32_t* __restrict__ aux, SadLaunch L, const __grid_constant__ CUtensorMap ref_map,
+           const __grid_constant__ CUtensorMap cur_map) {
+  extern __shared__ __align__(128) uint8_t smem_b[];
   const SadParams& p = L.p;
   constexpr int BWW = BLK / 4;  // words per block row
-  const int raw_words = L.R * L.rw;
-  const int cur_words = L.TBX * BLK * BWW;
-  // --- shared memory carve-up: raw[2] | cur[2] | keys | counters
-  uint32_t* copies = smem;
-  uint32_t* raw0 = copies + 4 * L.CS;
+  const int raw_words = static_cast<int>(L.raw_buf / 4);
+  const int cur_words = static_cast<int>(L.cur_buf / 4);
+  // --- shared memory carve-up: raw[2] | cur[2] | copies[4] | keys | counters | mbarriers
+  uint32_t* raw0 = reinterpret_cast<uint32_t*>(smem_b + ((128u - (smem_u32(smem_b) & 127u)) & 127u));
   uint32_t* cur0 = raw0 + 2 * raw_words;
-  uint32_t* keys = cur0 + 2 * cur_words;   // per block: running argmin key
+  uint32_t* copies = cur0 + 2 * cur_words;
+  uint32_t* keys = copies + 4 * L.CS;       // per block: running argmin key
   uint32_t* cnt = keys + L.TBX;             // per block: contributions so far
+  const uint32_t bar0 = (smem_u32(cnt + L.TBX) + 7u) & ~7u;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  const int cpw = L.cur_pitch / 4;  // words per staged current row
 
   // per-thread item: (block, dx); the thread walks all dy groups
   const int item = threadIdx.x;
@@ -175,56 +238,93 @@ sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, voi
     keys[threadIdx.x] = 0xffffffffu;
     cnt[threadIdx.x] = 0u;
   }
-  long long tile = blockIdx.x;
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0 + 8u) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  int tile = blockIdx.x;
   int buf = 0;
+  uint32_t phase_bits = 0;  // bit b: parity of buffer b's next completion
   pdl_launch_dependents();
   pdl_wait();  // first global access follows
-  if (tile < L.n_tiles) {
-    stage_tile<BLK>(L, cur, ref, tile, smem_u32(raw0), reinterpret_cast<uint8_t*>(raw0),
-                    smem_u32(cur0), reinterpret_cast<uint8_t*>(cur0));
-    cp_async_commit();
-  }
+  if (tile < L.n_tiles)
+    issue_tile<BLK>(L, cur, ref, &ref_map, &cur_map, tile, smem_u32(raw0), reinterpret_cast<uint8_t*>(raw0),
+                    smem_u32(cur0), reinterpret_cast<uint8_t*>(cur0), bar0);
   for (; tile < L.n_tiles; tile += gridDim.x, buf ^= 1) {
     uint32_t* raw = raw0 + buf * raw_words;
     uint32_t* curw = cur0 + buf * cur_words;
-    cp_async_wait_all();
+    if (L.tma) {
+      sad_mbar_wait(bar0 + 8u * buf, (phase_bits >> buf) & 1u);
+      phase_bits ^= 1u << buf;
+    } else {
+      cp_async_wait_all();
+    }
     __syncthreads();  // raw[buf] landed; previous tile's compute finished
-    // four byte-shifted word copies: copy_s[r][w] = bytes (4w+s .. 4w+s+3)
-    for (int r = warp; r < L.R; r += nwarps) {
-      for (int w = lane; w < L.Ww; w += 32) {
-        const uint32_t lo = raw[r * L.rw + w];
-        const uint32_t hi = raw[r * L.rw + w + 1];
-        const int o = r * L.Ww + w;
-        copies[o] = lo;
-        copies[L.CS + o] = __byte_perm(lo, hi, 0x4321);
-        copies[2 * L.CS + o] = __byte_perm(lo, hi, 0x5432);
-        copies[3 * L.CS + o] = __byte_perm(lo, hi, 0x6543);
+    // tile coordinates
+    const int tx = tile % L.n_tiles_x;
+    const int t2 = tile / L.n_tiles_x;
+    const int by = t2 % p.BY;
+    const long long pair = t2 / p.BY;
+    const int bx0 = tx * L.TBX;
+    const int nb = min(L.TBX, p.BX - bx0);
+    // leading bytes of the staged rows before the window (TMA boxes start at
+    // a 16-byte multiple)
+    const int dref = L.tma ? (bx0 * BLK + p.ox) - floor16(bx0 * BLK + p.ox) : 0;
+    const int dcur = L.tma ? (bx0 * BLK + p.cx) - floor16(bx0 * BLK + p.cx) : 0;
+    // four byte-shifted word copies: copy_s[r][w] = window bytes (4w+s .. 4w+s+3)
+    if (dref == 0) {
+      for (int r = warp; r < L.R; r += nwarps) {
+        for (int w = lane; w < L.Ww; w += 32) {
+          const uint32_t lo = raw[r * L.rw + w];
+          const uint32_t hi = raw[r * L.rw + w + 1];
+          const int o = r * L.Ww + w;
+          copies[o] = lo;
+          copies[L.CS + o] = __byte_perm(lo, hi, 0x4321);
+          copies[2 * L.CS + o] = __byte_perm(lo, hi, 0x5432);
+          copies[3 * L.CS + o] = __byte_perm(lo, hi, 0x6543);
+        }
+      }
+    } else {
+      const int dq = dref >> 2, dr = dref & 3;
+      for (int r = warp; r < L.R; r += nwarps) {
+        for (int w = lane; w < L.Ww; w += 32) {
+          const uint32_t* q = raw + r * L.rw + w + dq;
+          const uint32_t a0 = q[0], a1 = q[1], a2 = q[2];
+          const int o = r * L.Ww + w;
+#pragma unroll
+          for (int sft = 0; sft < 4; ++sft) {
+            const int t = sft + dr;  // byte offset within (a0, a1, a2): 1..6
+            copies[sft * L.CS + o] =
+                t < 4 ? __funnelshift_r(a0, a1, 8 * t) : __funnelshift_r(a1, a2, 8 * (t - 4));
+          }
+        }
       }
     }
     __syncthreads();
     // prefetch the next tile into the other buffer while this one computes
-    const long long next = tile + gridDim.x;
-    if (next < L.n_tiles) {
-      stage_tile<BLK>(L, cur, ref, next, smem_u32(raw0 + (buf ^ 1) * raw_words),
+    const int next = tile + gridDim.x;
+    if (next < L.n_tiles)
+      issue_tile<BLK>(L, cur, ref, &ref_map, &cur_map, next, smem_u32(raw0 + (buf ^ 1) * raw_words),
                       reinterpret_cast<uint8_t*>(raw0 + (buf ^ 1) * raw_words),
                       smem_u32(cur0 + (buf ^ 1) * cur_words),
-                      reinterpret_cast<uint8_t*>(cur0 + (buf ^ 1) * cur_words));
-      cp_async_commit();
-    }
-    // tile coordinates
-    const int tx = static_cast<int>(tile % L.n_tiles_x);
-    const long long t2 = tile / L.n_tiles_x;
-    const int by = static_cast<int>(t2 % p.BY);
-    const long long pair = t2 / p.BY;
-    const int bx0 = tx * L.TBX;
-    const int nb = min(L.TBX, p.BX - bx0);
+                      reinterpret_cast<uint8_t*>(cur0 + (buf ^ 1) * cur_words), bar0 + 8u * (buf ^ 1));
     if (has_item && ib < nb) {
       uint32_t cw[BLK][BWW];
-      const uint32_t* cb = curw + ib * BLK * BWW;
+      // rows of cur_pitch bytes, block ib at byte dcur + ib*BLK (dcur % 4 == 0)
+      const uint32_t* cb = curw + (dcur >> 2) + ib * BWW;
+      const bool vec = BWW == 4 && ((dcur & 15) == 0);
 #pragma unroll
-      for (int i = 0; i < BLK; ++i)
+      for (int i = 0; i < BLK; ++i) {
+        if (vec) {
+          const uint4 q4 = *reinterpret_cast<const uint4*>(cb + i * cpw);
+          cw[i][0] = q4.x; cw[i][1 % BWW] = q4.y; cw[i][2 % BWW] = q4.z; cw[i][3 % BWW] = q4.w;
+        } else {
 #pragma unroll
-        for (int j = 0; j < BWW; ++j) cw[i][j] = cb[i * BWW + j];
+          for (int j = 0; j < BWW; ++j) cw[i][j] = cb[i * cpw + j];
+        }
+      }
       const int col = ib * BLK + idx;  // byte column in the staged window
       const uint32_t* cp0 = copies + (col & 3) * L.CS + (col >> 2);
       const long long blk_index = (pair * p.BY + by) * (long long)p.BX + bx0 + ib;
@@ -321,11 +421,19 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
   }
   L.items = L.TBX * per_block;
   L.n_tiles_x = (p.BX + L.TBX - 1) / L.TBX;
-  L.n_tiles = p.pairs * (long long)p.BY * L.n_tiles_x;
+  const long long n_tiles = p.pairs * (long long)p.BY * L.n_tiles_x;
+  if (n_tiles >= (1LL << 31)) return fail(MERIT_E_UNSUPPORTED_VIEW, "too many SAD tiles for one launch");
+  L.n_tiles = static_cast<int>(n_tiles);
   L.R = L.G * D + BLK - 1;
   L.span = L.TBX * BLK + p.WX - 1;
   L.Ww = (L.span + 3) / 4;
-  L.rw = (L.Ww + 1 + 3) / 4 * 4;  // raw rows (+1 word for the shift) padded to 16-byte chunks
+  // TMA staging (see below) lands rows from floor16(x): up to 15 leading
+  // bytes, and the copy builder reads 2 words past the window
+  const char* te = getenv("MERIT_SAD_TMA");
+  bool tma_ok = !(te && te[0] == '0') && p.boundary == MERIT_ZERO_PAD && tensor_map_encoder() != nullptr &&
+                p.Wr % 16 == 0 && p.Wc % 16 == 0 && p.cx % 4 == 0 && (reinterpret_cast<uintptr_t>(ref) % 16) == 0 &&
+                (reinterpret_cast<uintptr_t>(cur) % 16) == 0 && p.pairs < (1LL << 31);
+  L.rw = tma_ok ? (L.Ww + 5 + 3) / 4 * 4 : (L.Ww + 1 + 3) / 4 * 4;  // raw words per row, 16-byte chunks
   L.CS = L.R * L.Ww;
   L.CS += ((8 - (L.CS % 32)) + 32) % 32;
   L.word_path = ((p.ox % 4) == 0 && (p.cx % 4) == 0 && (p.Wr % 4) == 0 && (p.Wc % 4) == 0 &&
@@ -333,7 +441,32 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
                     ? 1 : 0;
   L.vec_path = (L.word_path && (p.ox % 16) == 0 && (p.Wr % 16) == 0 && (BLK % 16) == 0 &&
                 (reinterpret_cast<uintptr_t>(ref) % 16) == 0) ? 1 : 0;
-  const size_t smem = 4ull * (4ull * L.CS + 2ull * L.R * L.rw + 2ull * L.TBX * BLK * (BLK / 4) + 2ull * L.TBX);
+  L.cur_pitch = (L.TBX * BLK + (tma_ok ? 12 : 0) + 15) / 16 * 16;
+  L.R_box = L.R;
+  L.raw_buf = (static_cast<uint32_t>(L.R_box * L.rw * 4) + 127u) & ~127u;
+  L.cur_buf = (static_cast<uint32_t>(BLK * L.cur_pitch) + 127u) & ~127u;
+  // TMA staging: zero fill is the ZERO_PAD rule; row pitches must be 16-byte
+  // multiples and a box row at most 256 elements.
+  L.tma = tma_ok && L.rw * 4 <= 256 && L.R_box <= 256 && L.cur_pitch <= 256;
+  CUtensorMap ref_map, cur_map;
+  std::memset(&ref_map, 0, sizeof(ref_map));
+  std::memset(&cur_map, 0, sizeof(cur_map));
+  if (L.tma) {
+    const cuuint64_t rd[3] = {(cuuint64_t)p.Wr, (cuuint64_t)p.Hr, (cuuint64_t)p.pairs};
+    const cuuint64_t rs[2] = {(cuuint64_t)p.Wr, (cuuint64_t)p.Wr * p.Hr};
+    const cuuint32_t rb[3] = {(cuuint32_t)(L.rw * 4), (cuuint32_t)L.R_box, 1};
+    const cuuint64_t cd[3] = {(cuuint64_t)p.Wc, (cuuint64_t)p.Hc, (cuuint64_t)p.pairs};
+    const cuuint64_t cs[2] = {(cuuint64_t)p.Wc, (cuuint64_t)p.Wc * p.Hc};
+    const cuuint32_t cbx[3] = {(cuuint32_t)L.cur_pitch, (cuuint32_t)BLK, 1};
+    const cuuint32_t es[3] = {1, 1, 1};
+    L.tma = tensor_map_encoder()(&ref_map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(ref), rd, rs, rb,
+                                 es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS &&
+            tensor_map_encoder()(&cur_map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(cur), cd, cs, cbx,
+                                 es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
+  const size_t smem = 128 + 2ull * L.raw_buf + 2ull * L.cur_buf + 4ull * (4ull * L.CS + 2ull * L.TBX) + 8 + 16;
   if (L.n_tiles == 0) return MERIT_OK;
   if (smem > 110 * 1024) return fail(MERIT_E_UNSUPPORTED_VIEW, "SAD footprint exceeds shared memory");
   auto kern = sad_kernel<BLK, D>;
@@ -343,7 +476,8 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
   const int threads = (L.items + 31) / 32 * 32;
   long long grid = 2LL * num_sms();
   if (grid > L.n_tiles) grid = L.n_tiles;
-  e = launch_pdl(kern, dim3(static_cast<unsigned>(grid)), dim3(threads), smem, s, 1, cur, ref, out, aux, L);
+  e = launch_pdl(kern, dim3(static_cast<unsigned>(grid)), dim3(threads), smem, s, 1, cur, ref, out, aux, L, ref_map,
+                 cur_map);
   if (e != cudaSuccess) return cuda_check(e, "launch(sad)");
   return launch_status("sad_kernel");
 }

@@ -116,6 +116,22 @@ def test_sad_small_bit_exact(cuda, h, wd, blk, r, boundary):
     assert np.array_equal(mv, O.me_argmin(want, r))
 
 
+@pytest.mark.parametrize("mode", ["1", "0"])  # staging: TMA boxes / cp.async
+@pytest.mark.parametrize("blk", [8, 16])
+def test_sad_staging_modes_unaligned_windows(cuda, monkeypatch, mode, blk):
+    # windows that start at every byte offset mod 16 (radius r: x0 = bx*blk - r),
+    # the case TMA boxes cannot start at (tools/microbench/tma_u8.cu)
+    monkeypatch.setenv("MERIT_SAD_TMA", mode)
+    for (h, wd, r) in [(64, 96, 2), (48, 128, 5), (80, 160, 7), (64, 112, 12), (96, 80, 23)]:
+        cur, ref = W.gen_me_pair(h, wd, 17, blk, min(r, 16), 4)
+        w = W.me_view(h, wd, blk, r)
+        w.src_a, w.src_b = cur, ref
+        sad, mv = run_full_argmin(w)
+        want = O.me_sad(cur, ref, blk, r)
+        assert np.array_equal(sad, want), (h, wd, r)
+        assert np.array_equal(mv, O.me_argmin(want, r)), (h, wd, r)
+
+
 def test_sad_ties_lowest_raster(cuda):
     # Flat frames: every displacement that stays inside the frame ties at 0;
     # the lowest raster index (dy*WX + dx) must win.
