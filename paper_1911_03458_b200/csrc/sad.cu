@@ -274,31 +274,36 @@ sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, voi
     const int dref = L.tma ? (bx0 * BLK + p.ox) - floor16(bx0 * BLK + p.ox) : 0;
     const int dcur = L.tma ? (bx0 * BLK + p.cx) - floor16(bx0 * BLK + p.cx) : 0;
     // four byte-shifted word copies: copy_s[r][w] = window bytes (4w+s .. 4w+s+3)
-    if (dref == 0) {
-      for (int r = warp; r < L.R; r += nwarps) {
-        for (int w = lane; w < L.Ww; w += 32) {
-          const uint32_t lo = raw[r * L.rw + w];
-          const uint32_t hi = raw[r * L.rw + w + 1];
-          const int o = r * L.Ww + w;
-          copies[o] = lo;
-          copies[L.CS + o] = __byte_perm(lo, hi, 0x4321);
-          copies[2 * L.CS + o] = __byte_perm(lo, hi, 0x5432);
-          copies[3 * L.CS + o] = __byte_perm(lo, hi, 0x6543);
-        }
-      }
-    } else {
-      const int dq = dref >> 2, dr = dref & 3;
-      for (int r = warp; r < L.R; r += nwarps) {
-        for (int w = lane; w < L.Ww; w += 32) {
-          const uint32_t* q = raw + r * L.rw + w + dq;
-          const uint32_t a0 = q[0], a1 = q[1], a2 = q[2];
-          const int o = r * L.Ww + w;
-#pragma unroll
-          for (int sft = 0; sft < 4; ++sft) {
-            const int t = sft + dr;  // byte offset within (a0, a1, a2): 1..6
-            copies[sft * L.CS + o] =
-                t < 4 ? __funnelshift_r(a0, a1, 8 * t) : __funnelshift_r(a1, a2, 8 * (t - 4));
+    {
+      // 32-bit shared addresses, bumped per row (no generic-pointer math)
+      const uint32_t cs4 = static_cast<uint32_t>(L.CS) * 4u;
+      const uint32_t rstep = static_cast<uint32_t>(nwarps * L.rw) * 4u;
+      const uint32_t cstep = static_cast<uint32_t>(nwarps * L.Ww) * 4u;
+      uint32_t ra = smem_u32(raw) + static_cast<uint32_t>(warp * L.rw + lane + (dref >> 2)) * 4u;
+      uint32_t ca = smem_u32(copies) + static_cast<uint32_t>(warp * L.Ww + lane) * 4u;
+      const int dr = dref & 3;
+      for (int r = warp; r < L.R; r += nwarps, ra += rstep, ca += cstep) {
+        for (int w = lane, k = 0; w < L.Ww; w += 32, k += 128) {
+          uint32_t a0, a1, a2;
+          asm volatile("ld.shared.u32 %0, [%1];" : "=r"(a0) : "r"(ra + k));
+          asm volatile("ld.shared.u32 %0, [%1];" : "=r"(a1) : "r"(ra + k + 4));
+          uint32_t c0, c1, c2, c3;
+          if (dr == 0) {
+            c0 = a0;
+            c1 = __byte_perm(a0, a1, 0x4321);
+            c2 = __byte_perm(a0, a1, 0x5432);
+            c3 = __byte_perm(a0, a1, 0x6543);
+          } else {
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(a2) : "r"(ra + k + 8));
+            c0 = __funnelshift_r(a0, a1, 8 * dr);
+            c1 = dr + 1 < 4 ? __funnelshift_r(a0, a1, 8 * (dr + 1)) : a1;
+            c2 = dr + 2 < 4 ? __funnelshift_r(a0, a1, 8 * (dr + 2)) : __funnelshift_r(a1, a2, 8 * (dr - 2));
+            c3 = __funnelshift_r(a1, a2, 8 * (dr - 1));
           }
+          asm volatile("st.shared.u32 [%0], %1;" ::"r"(ca + k), "r"(c0) : "memory");
+          asm volatile("st.shared.u32 [%0], %1;" ::"r"(ca + cs4 + k), "r"(c1) : "memory");
+          asm volatile("st.shared.u32 [%0], %1;" ::"r"(ca + 2 * cs4 + k), "r"(c2) : "memory");
+          asm volatile("st.shared.u32 [%0], %1;" ::"r"(ca + 3 * cs4 + k), "r"(c3) : "memory");
         }
       }
     }
@@ -368,8 +373,8 @@ sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, voi
           } else {
             int32_t* o = static_cast<int32_t*>(out) + obase;
 #pragma unroll
-            for (int d = 0; d < D; ++d)
-              if (d < nd) __stcs(o + d * p.WX, static_cast<int32_t>(acc[d]));
+            for (int d = 0; d < D; ++d, o += p.WX)
+              if (d < nd) __stcs(o, static_cast<int32_t>(acc[d]));
           }
         }
       }
