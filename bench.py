@@ -432,7 +432,7 @@ def run_ours(args):
 
 def cpu_baseline(config, budget_s=20.0, steps=1, warmup=0):
     from oracle.cpu_baseline import CpuBaseline, unit_cost_s
-    cfg = config if config in ("C1", "C2", "C5") else "C2"
+    cfg = config
     cb = CpuBaseline(cfg)
     try:
         per_proc = max(1, int(budget_s / max(steps + warmup, 1) / unit_cost_s(cfg, cb.kind)))
@@ -449,7 +449,8 @@ def cpu_baseline(config, budget_s=20.0, steps=1, warmup=0):
     finally:
         cb.close()
     unit_name = {"C2": "16x16 blocks of the 1080p pair", "C5": "16x16 blocks of a 4K pair",
-                 "C1": "images (64 channels)"}[cfg]
+                 "C1": "images (64 channels)", "C3": "output channels of one 56x56 image (fp32)",
+                 "C4": "output channels of one image (bf16-rounded values in REAL32)"}[cfg]
     return {"value": round(n / wall / 1e9, 9), "unit": UNIT, "cores": cb.procs, "kind": cb.kind,
             "sample": f"{cfg}: {cb.procs} processes x {per_proc} {unit_name} per step, {steps} step(s), "
                       f"{n} outputs in {wall:.2f} s through merit::run_full"

@@ -49,7 +49,17 @@ def _init(config, seed):
     elif config == "C1":
         _state["x"] = W.gen_uniform([1, 64, 112, 112], 1 + seed)
     elif config in ("C3", "C4"):
-        pass
+        cin, h, cout = CONV_GEOM[config][1:4]
+        x = W.gen_uniform([1, cin, h, h], 3 + seed)
+        wt = W.gen_normal([cout, cin, 3, 3], 4 + seed, (2.0 / (9 * cin)) ** 0.5)
+        if config == "C4":  # the engine has no bf16: bf16-rounded values in REAL32
+            x = W.bf16_bits_to_f32(W.to_bf16_bits(x))
+            wt = W.bf16_bits_to_f32(W.to_bf16_bits(wt))
+        _state["x"], _state["wt"] = x, wt
+
+
+# (N, Cin, H=W, Cout, stride) of the conv configs
+CONV_GEOM = {"C3": (32, 64, 56, 64, 1), "C4": (256, 128, 56, 256, 2)}
 
 
 def strip_workload(config, shard, units):
@@ -78,6 +88,16 @@ def strip_workload(config, shard, units):
         w = W.maxpool_nchw_view(1, 64, 112, 112)
         w.src_a = _state["x"]
         return w, 64 * 56 * 56
+    if config in ("C3", "C4"):
+        # `units` output channels of one image (all output pixels)
+        _, cin, h, cout, s = CONV_GEOM[config]
+        co0 = (shard * units) % cout
+        units = min(units, cout - co0)
+        w = W.conv_nchw_view(1, cin, h, h, units, 3, s, 1)
+        w.src_a = _state["x"]
+        w.src_b = np.ascontiguousarray(_state["wt"][co0:co0 + units])
+        ho = (h + 2 - 3) // s + 1
+        return w, units * ho * ho
     raise ValueError(config)
 
 
@@ -122,9 +142,15 @@ def unit_cost_s(config, kind):
         per = 1089 * 256
     elif config == "C5":
         per = 4225 * 256
+    elif config in ("C3", "C4"):
+        _, cin, h, _, s = CONV_GEOM[config]
+        ho = (h + 2 - 3) // s + 1
+        per = ho * ho * cin * 9  # MACs per output channel of one image
     else:
         per = 64 * 56 * 56 * 9
     rate = 1.1e6 if kind == "reference" else 3.0e8  # measured: 4 blocks/proc in 5.5 s
+    if config in ("C3", "C4") and kind == "reference":
+        rate = 6.0e6  # measured: one C4 output channel (0.9 M MAC) in 0.13 s, warm
     return per / rate
 
 
