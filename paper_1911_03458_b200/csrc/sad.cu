@@ -71,6 +71,8 @@ struct SadLaunch {
   int vec_path;   // 16-byte aligned reference rows
   int tma;        // reference window + current blocks staged by TMA (ZERO_PAD)
   int R_box;      // TMA box rows (= R)
+  int nby;        // block rows per tile / per thread (1, or 2 for 8x8 blocks on the TMA path)
+  int BYT;        // tile rows = ceil(BY / nby)
   int cur_pitch;  // bytes per staged current-frame row: TBX*BW rounded up to 16
   uint32_t raw_buf, cur_buf;  // bytes per raw / current buffer (128-byte multiples)
 };
@@ -83,8 +85,8 @@ __device__ __forceinline__ void stage_tile(const SadLaunch& L, const uint8_t* __
   const SadParams& p = L.p;
   const int tx = tile % L.n_tiles_x;
   const int t2 = tile / L.n_tiles_x;
-  const int by = t2 % p.BY;
-  const long long pair = t2 / p.BY;
+  const int by = t2 % L.BYT;  // nby == 1 on this path
+  const long long pair = t2 / L.BYT;
   const int bx0 = tx * L.TBX;
   const int nb = min(L.TBX, p.BX - bx0);
   const uint8_t* refp = ref + pair * (long long)p.Hr * p.Wr;
@@ -194,10 +196,10 @@ __device__ __forceinline__ void issue_tile(const SadLaunch& L, const uint8_t* __
       const SadParams& p = L.p;
       const int tx = tile % L.n_tiles_x;
       const int t2 = tile / L.n_tiles_x;
-      const int by = t2 % p.BY;
-      const int pair = t2 / p.BY;
+      const int by = (t2 % L.BYT) * L.nby;
+      const int pair = t2 / L.BYT;
       const int bx0 = tx * L.TBX;
-      const uint32_t bytes = L.R_box * L.rw * 4 + BLK * L.cur_pitch;
+      const uint32_t bytes = L.R_box * L.rw * 4 + L.nby * BLK * L.cur_pitch;
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
       sad_tma_3d(raw_s, ref_map, floor16(bx0 * BLK + p.ox), by * BLK + p.oy, pair, bar);
       sad_tma_3d(cur_s, cur_map, floor16(bx0 * BLK + p.cx), by * BLK + p.cy, pair, bar);
@@ -208,7 +210,7 @@ __device__ __forceinline__ void issue_tile(const SadLaunch& L, const uint8_t* __
   }
 }
 
-template <int BLK, int D>
+template <int BLK, int D, int NBY>
 __global__ void __launch_bounds__(kSadThreads, 2)
 sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, void* __restrict__ out,
            int32_t* __restrict__ aux, SadLaunch L, const __grid_constant__ CUtensorMap ref_map,
@@ -223,8 +225,8 @@ sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, voi
   uint32_t* cur0 = raw0 + 2 * raw_words;
   uint32_t* copies = cur0 + 2 * cur_words;
   uint32_t* keys = copies + 4 * L.CS;       // per block: running argmin key
-  uint32_t* cnt = keys + L.TBX;             // per block: contributions so far
-  const uint32_t bar0 = (smem_u32(cnt + L.TBX) + 7u) & ~7u;
+  uint32_t* cnt = keys + NBY * L.TBX;       // per block: contributions so far
+  const uint32_t bar0 = (smem_u32(cnt + NBY * L.TBX) + 7u) & ~7u;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   const int cpw = L.cur_pitch / 4;  // words per staged current row
 
@@ -234,7 +236,7 @@ sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, voi
   const int idx = item - ib * p.WX;
   const bool has_item = item < L.items;
 
-  if (threadIdx.x < L.TBX) {
+  if (threadIdx.x < NBY * L.TBX) {
     keys[threadIdx.x] = 0xffffffffu;
     cnt[threadIdx.x] = 0u;
   }
@@ -265,8 +267,8 @@ sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, voi
     // tile coordinates
     const int tx = tile % L.n_tiles_x;
     const int t2 = tile / L.n_tiles_x;
-    const int by = t2 % p.BY;
-    const long long pair = t2 / p.BY;
+    const int by = (t2 % L.BYT) * NBY;  // first block row of the tile
+    const long long pair = t2 / L.BYT;
     const int bx0 = tx * L.TBX;
     const int nb = min(L.TBX, p.BX - bx0);
     // leading bytes of the staged rows before the window (TMA boxes start at
@@ -316,65 +318,80 @@ sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, voi
                       smem_u32(cur0 + (buf ^ 1) * cur_words),
                       reinterpret_cast<uint8_t*>(cur0 + (buf ^ 1) * cur_words), bar0 + 8u * (buf ^ 1));
     if (has_item && ib < nb) {
-      uint32_t cw[BLK][BWW];
-      // rows of cur_pitch bytes, block ib at byte dcur + ib*BLK (dcur % 4 == 0)
+      // current blocks (NBY block rows) in registers: rows of cur_pitch bytes,
+      // block ib at byte dcur + ib*BLK (dcur % 4 == 0), block row n at row n*BLK
+      uint32_t cw[NBY][BLK][BWW];
       const uint32_t* cb = curw + (dcur >> 2) + ib * BWW;
       const bool vec = BWW == 4 && ((dcur & 15) == 0);
 #pragma unroll
-      for (int i = 0; i < BLK; ++i) {
-        if (vec) {
-          const uint4 q4 = *reinterpret_cast<const uint4*>(cb + i * cpw);
-          cw[i][0] = q4.x; cw[i][1 % BWW] = q4.y; cw[i][2 % BWW] = q4.z; cw[i][3 % BWW] = q4.w;
-        } else {
+      for (int n = 0; n < NBY; ++n)
 #pragma unroll
-          for (int j = 0; j < BWW; ++j) cw[i][j] = cb[i * cpw + j];
+        for (int i = 0; i < BLK; ++i) {
+          const uint32_t* src = cb + (n * BLK + i) * cpw;
+          if (vec) {
+            const uint4 q4 = *reinterpret_cast<const uint4*>(src);
+            cw[n][i][0] = q4.x; cw[n][i][1 % BWW] = q4.y; cw[n][i][2 % BWW] = q4.z; cw[n][i][3 % BWW] = q4.w;
+          } else {
+#pragma unroll
+            for (int j = 0; j < BWW; ++j) cw[n][i][j] = src[j];
+          }
         }
-      }
       const int col = ib * BLK + idx;  // byte column in the staged window
       const uint32_t* cp0 = copies + (col & 3) * L.CS + (col >> 2);
       const long long blk_index = (pair * p.BY + by) * (long long)p.BX + bx0 + ib;
-      uint32_t best = 0xffffffffu;
+      uint32_t best[NBY];
+#pragma unroll
+      for (int n = 0; n < NBY; ++n) best[n] = 0xffffffffu;
       for (int ig = 0; ig < L.G; ++ig) {
         const uint32_t* cp = cp0 + ig * D * L.Ww;
-        uint32_t acc[D];
+        uint32_t acc[NBY][D];
 #pragma unroll
-        for (int d = 0; d < D; ++d) acc[d] = 0;
+        for (int n = 0; n < NBY; ++n)
 #pragma unroll
-        for (int r = 0; r < D + BLK - 1; ++r) {
+          for (int d = 0; d < D; ++d) acc[n][d] = 0;
+        // block row n at displacement d reads staged row r = n*BLK + d + i:
+        // every loaded reference word feeds all NBY block rows
+#pragma unroll
+        for (int r = 0; r < D + NBY * BLK - 1; ++r) {
           uint32_t rwv[BWW];
 #pragma unroll
           for (int j = 0; j < BWW; ++j) rwv[j] = cp[j];
           cp += L.Ww;
 #pragma unroll
-          for (int d = 0; d < D; ++d) {
-            const int i = r - d;
-            if (i >= 0 && i < BLK) {
+          for (int n = 0; n < NBY; ++n)
 #pragma unroll
-              for (int j = 0; j < BWW; ++j) acc[d] = vabsdiff4_acc(cw[i][j], rwv[j], acc[d]);
+            for (int d = 0; d < D; ++d) {
+              const int i = r - d - n * BLK;
+              if (i >= 0 && i < BLK) {
+#pragma unroll
+                for (int j = 0; j < BWW; ++j) acc[n][d] = vabsdiff4_acc(cw[n][i][j], rwv[j], acc[n][d]);
+              }
             }
-          }
         }
         const int dy0 = ig * D;
         const int nd = min(D, p.WY - dy0);
         uint32_t key = (static_cast<uint32_t>(dy0) * p.WX + idx);
         const uint32_t kstep = static_cast<uint32_t>(p.WX);
 #pragma unroll
-        for (int d = 0; d < D; ++d) {
-          const uint32_t k = (acc[d] << 16) | (key + d * kstep);
-          if (d < nd) best = k < best ? k : best;
-        }
-        if (p.write_map) {
-          const long long obase = (blk_index * p.WY + dy0) * p.WX + idx;
-          if (p.out_f32) {
-            float* o = static_cast<float*>(out) + obase;
+        for (int n = 0; n < NBY; ++n) {
 #pragma unroll
-            for (int d = 0; d < D; ++d)
-              if (d < nd) __stcs(o + d * p.WX, static_cast<float>(acc[d]));
-          } else {
-            int32_t* o = static_cast<int32_t*>(out) + obase;
+          for (int d = 0; d < D; ++d) {
+            const uint32_t k = (acc[n][d] << 16) | (key + d * kstep);
+            if (d < nd) best[n] = k < best[n] ? k : best[n];
+          }
+          if (p.write_map && by + n < p.BY) {
+            const long long obase = ((blk_index + n * (long long)p.BX) * p.WY + dy0) * p.WX + idx;
+            if (p.out_f32) {
+              float* o = static_cast<float*>(out) + obase;
 #pragma unroll
-            for (int d = 0; d < D; ++d, o += p.WX)
-              if (d < nd) __stcs(o, static_cast<int32_t>(acc[d]));
+              for (int d = 0; d < D; ++d, o += p.WX)
+                if (d < nd) __stcs(o, static_cast<float>(acc[n][d]));
+            } else {
+              int32_t* o = static_cast<int32_t*>(out) + obase;
+#pragma unroll
+              for (int d = 0; d < D; ++d, o += p.WX)
+                if (d < nd) __stcs(o, static_cast<int32_t>(acc[n][d]));
+            }
           }
         }
       }
@@ -383,18 +400,23 @@ sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, voi
         // in; the thread that arrives last writes the record and re-arms the
         // slot for the next tile (the next tile's atomics follow the barrier at
         // the top of the loop).
-        atomicMin(&keys[ib], best);
-        __threadfence_block();
-        if (atomicAdd(&cnt[ib], 1u) == static_cast<uint32_t>(p.WX - 1)) {
+#pragma unroll
+        for (int n = 0; n < NBY; ++n) {
+          if (by + n >= p.BY) break;
+          const int slot = n * L.TBX + ib;
+          atomicMin(&keys[slot], best[n]);
           __threadfence_block();
-          const uint32_t key = atomicExch(&keys[ib], 0xffffffffu);
-          cnt[ib] = 0u;
-          const int k = static_cast<int>(key & 0xffffu);
-          const int dy = k / p.WX, dx = k - (k / p.WX) * p.WX;
-          int32_t* a = aux + blk_index * 3;
-          a[0] = dy + p.oy - p.cy;
-          a[1] = dx + p.ox - p.cx;
-          a[2] = static_cast<int32_t>(key >> 16);
+          if (atomicAdd(&cnt[slot], 1u) == static_cast<uint32_t>(p.WX - 1)) {
+            __threadfence_block();
+            const uint32_t key = atomicExch(&keys[slot], 0xffffffffu);
+            cnt[slot] = 0u;
+            const int k = static_cast<int>(key & 0xffffu);
+            const int dy = k / p.WX, dx = k - (k / p.WX) * p.WX;
+            int32_t* a = aux + (blk_index + n * (long long)p.BX) * 3;
+            a[0] = dy + p.oy - p.cy;
+            a[1] = dx + p.ox - p.cx;
+            a[2] = static_cast<int32_t>(key >> 16);
+          }
         }
       }
     }
@@ -426,33 +448,44 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
   }
   L.items = L.TBX * per_block;
   L.n_tiles_x = (p.BX + L.TBX - 1) / L.TBX;
-  const long long n_tiles = p.pairs * (long long)p.BY * L.n_tiles_x;
-  if (n_tiles >= (1LL << 31)) return fail(MERIT_E_UNSUPPORTED_VIEW, "too many SAD tiles for one launch");
-  L.n_tiles = static_cast<int>(n_tiles);
-  L.R = L.G * D + BLK - 1;
   L.span = L.TBX * BLK + p.WX - 1;
   L.Ww = (L.span + 3) / 4;
-  // TMA staging (see below) lands rows from floor16(x): up to 15 leading
-  // bytes, and the copy builder reads 2 words past the window
+  // TMA staging lands rows from floor16(x): up to 15 leading bytes, and the
+  // copy builder reads 2 words past the window
   const char* te = getenv("MERIT_SAD_TMA");
-  bool tma_ok = !(te && te[0] == '0') && p.boundary == MERIT_ZERO_PAD && tensor_map_encoder() != nullptr &&
-                p.Wr % 16 == 0 && p.Wc % 16 == 0 && p.cx % 4 == 0 && (reinterpret_cast<uintptr_t>(ref) % 16) == 0 &&
-                (reinterpret_cast<uintptr_t>(cur) % 16) == 0 && p.pairs < (1LL << 31);
-  L.rw = tma_ok ? (L.Ww + 5 + 3) / 4 * 4 : (L.Ww + 1 + 3) / 4 * 4;  // raw words per row, 16-byte chunks
-  L.CS = L.R * L.Ww;
-  L.CS += ((8 - (L.CS % 32)) + 32) % 32;
+  const bool tma_ok = !(te && te[0] == '0') && p.boundary == MERIT_ZERO_PAD && tensor_map_encoder() != nullptr &&
+                      p.Wr % 16 == 0 && p.Wc % 16 == 0 && p.cx % 4 == 0 &&
+                      (reinterpret_cast<uintptr_t>(ref) % 16) == 0 && (reinterpret_cast<uintptr_t>(cur) % 16) == 0 &&
+                      p.pairs < (1LL << 31);
   L.word_path = ((p.ox % 4) == 0 && (p.cx % 4) == 0 && (p.Wr % 4) == 0 && (p.Wc % 4) == 0 &&
                  (reinterpret_cast<uintptr_t>(cur) % 4) == 0 && (reinterpret_cast<uintptr_t>(ref) % 4) == 0)
                     ? 1 : 0;
   L.vec_path = (L.word_path && (p.ox % 16) == 0 && (p.Wr % 16) == 0 && (BLK % 16) == 0 &&
                 (reinterpret_cast<uintptr_t>(ref) % 16) == 0) ? 1 : 0;
-  L.cur_pitch = (L.TBX * BLK + (tma_ok ? 12 : 0) + 15) / 16 * 16;
-  L.R_box = L.R;
-  L.raw_buf = (static_cast<uint32_t>(L.R_box * L.rw * 4) + 127u) & ~127u;
-  L.cur_buf = (static_cast<uint32_t>(BLK * L.cur_pitch) + 127u) & ~127u;
-  // TMA staging: zero fill is the ZERO_PAD rule; row pitches must be 16-byte
-  // multiples and a box row at most 256 elements.
-  L.tma = tma_ok && L.rw * 4 <= 256 && L.R_box <= 256 && L.cur_pitch <= 256;
+  // geometry for nby block rows per tile; TMA staging only where the boxes fit
+  auto geometry = [&](int nby, bool tma) {
+    L.nby = nby;
+    L.BYT = (p.BY + nby - 1) / nby;
+    L.R = L.G * D + nby * BLK - 1;
+    L.rw = tma ? (L.Ww + 5 + 3) / 4 * 4 : (L.Ww + 1 + 3) / 4 * 4;  // raw words per row, 16-byte chunks
+    L.CS = L.R * L.Ww;
+    L.CS += ((8 - (L.CS % 32)) + 32) % 32;
+    L.cur_pitch = (L.TBX * BLK + (tma ? 12 : 0) + 15) / 16 * 16;
+    L.R_box = L.R;
+    L.raw_buf = (static_cast<uint32_t>(L.R_box * L.rw * 4) + 127u) & ~127u;
+    L.cur_buf = (static_cast<uint32_t>(nby * BLK * L.cur_pitch) + 127u) & ~127u;
+    return tma && L.rw * 4 <= 256 && L.R_box <= 256 && L.cur_pitch <= 256 && nby * BLK <= 256;
+  };
+  // 8x8 blocks: two block rows per thread (every loaded reference word feeds
+  // both), on the TMA staging path
+  const char* ne = getenv("MERIT_SAD_NBY");
+  const int nby_want = (BLK == 8 && !(ne && ne[0] == '1')) ? 2 : 1;
+  L.tma = geometry(nby_want, tma_ok);
+  if (!L.tma && nby_want != 1) L.tma = geometry(1, tma_ok);
+  if (!L.tma) geometry(1, false);
+  const long long n_tiles = p.pairs * (long long)L.BYT * L.n_tiles_x;
+  if (n_tiles >= (1LL << 31)) return fail(MERIT_E_UNSUPPORTED_VIEW, "too many SAD tiles for one launch");
+  L.n_tiles = static_cast<int>(n_tiles);
   CUtensorMap ref_map, cur_map;
   std::memset(&ref_map, 0, sizeof(ref_map));
   std::memset(&cur_map, 0, sizeof(cur_map));
@@ -462,7 +495,7 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
     const cuuint32_t rb[3] = {(cuuint32_t)(L.rw * 4), (cuuint32_t)L.R_box, 1};
     const cuuint64_t cd[3] = {(cuuint64_t)p.Wc, (cuuint64_t)p.Hc, (cuuint64_t)p.pairs};
     const cuuint64_t cs[2] = {(cuuint64_t)p.Wc, (cuuint64_t)p.Wc * p.Hc};
-    const cuuint32_t cbx[3] = {(cuuint32_t)L.cur_pitch, (cuuint32_t)BLK, 1};
+    const cuuint32_t cbx[3] = {(cuuint32_t)L.cur_pitch, (cuuint32_t)(L.nby * BLK), 1};
     const cuuint32_t es[3] = {1, 1, 1};
     L.tma = tensor_map_encoder()(&ref_map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(ref), rd, rs, rb,
                                  es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -470,11 +503,16 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
             tensor_map_encoder()(&cur_map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t*>(cur), cd, cs, cbx,
                                  es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                                  CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    if (!L.tma) return fail(MERIT_E_CUDA, "cuTensorMapEncodeTiled failed for the SAD frames");
   }
-  const size_t smem = 128 + 2ull * L.raw_buf + 2ull * L.cur_buf + 4ull * (4ull * L.CS + 2ull * L.TBX) + 8 + 16;
+  const size_t smem =
+      128 + 2ull * L.raw_buf + 2ull * L.cur_buf + 4ull * (4ull * L.CS + 2ull * L.nby * L.TBX) + 8 + 16;
   if (L.n_tiles == 0) return MERIT_OK;
   if (smem > 110 * 1024) return fail(MERIT_E_UNSUPPORTED_VIEW, "SAD footprint exceeds shared memory");
-  auto kern = sad_kernel<BLK, D>;
+  auto kern = sad_kernel<BLK, D, 1>;
+  if constexpr (BLK == 8) {
+    if (L.nby == 2) kern = sad_kernel<BLK, D, 2>;
+  }
   cudaError_t e = set_smem_attr(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return cuda_check(e, "set_smem_attr(sad)");

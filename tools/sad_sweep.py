@@ -6,7 +6,7 @@ from paper_1911_03458_b200.merit import run_full_argmin
 import oracle.binding as O
 blk = int(sys.argv[1])
 bad = 0
-for (h, wd) in [(48, 64), (64, 96), (80, 160), (96, 112), (112, 192), (128, 256), (144, 80)]:
+for (h, wd) in [(48, 64), (64, 96), (72, 96), (80, 160), (88, 128), (96, 112), (112, 192), (128, 256), (144, 80)]:
     for r in [2, 4, 7, 8, 12, 16, 20, 24, 32]:
         cur, ref = W.gen_me_pair(h, wd, 9, blk, min(r, 16), 4)
         w = W.me_view(h, wd, blk, r)
