@@ -531,12 +531,14 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
 // fits the thread budget.  Used by the lowering to decide eligibility.
 int sad_rows_per_thread(int BH, int WY, int WX) {
   if (WX > kSadMaxThreads || WY > 256) return 0;
+  const char* e = getenv("MERIT_SAD_D");  // tuning override
+  const int want = e ? atoi(e) : 0;
   if (BH == 16) {
-    const char* e = getenv("MERIT_SAD_D");  // tuning override: 11 or 33
-    if (WY <= 33) return (e && atoi(e) == 11) ? 11 : 33;
-    return 17;
+    if (want == 11 || want == 17 || want == 33) return want;
+    return WY <= 66 ? 33 : 17;
   }
-  return WY <= 33 ? 11 : 22;
+  if (want == 11 || want == 22 || want == 33) return want;
+  return WY <= 33 ? 11 : (WY <= 66 ? 33 : 22);  // measured on C5 (+/-32): 33 beats 22 by 3%
 }
 
 merit_status launch_sad(const merit_plan& plan, const void* a, const void* b, void* out, void* aux,
@@ -554,6 +556,7 @@ merit_status launch_sad(const merit_plan& plan, const void* a, const void* b, vo
   } else {
     if (D == 11) return launch_sad_t<8, 11>(p, cur, ref, out, ax, s);
     if (D == 22) return launch_sad_t<8, 22>(p, cur, ref, out, ax, s);
+    if (D == 33) return launch_sad_t<8, 33>(p, cur, ref, out, ax, s);
   }
   return fail(MERIT_E_UNSUPPORTED_VIEW, "no SAD kernel variant for this window");
 }
