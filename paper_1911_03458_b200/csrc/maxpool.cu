@@ -164,7 +164,7 @@ __device__ __forceinline__ void mp_mbar_wait(uint32_t bar, uint32_t parity) {
 template <int NT, int RB, bool TM>
 __global__ void __launch_bounds__(NT) maxpool3s2_bulk_kernel(const float* __restrict__ in,
                                                              float* __restrict__ out, MaxpoolParams p,
-                                                             int nband, long long n_items, int ns,
+                                                             int nband, int n_items, int ns,
                                                              const __grid_constant__ CUtensorMap rows_map) {
   extern __shared__ __align__(128) float sbuf[];
   const int H = p.H, W = p.W, Ho = p.Ho, Wo = p.Wo;
@@ -173,19 +173,25 @@ __global__ void __launch_bounds__(NT) maxpool3s2_bulk_kernel(const float* __rest
   __shared__ __align__(8) unsigned long long bars[kMpMaxStages];
   const uint32_t bar0 = smem_u32(&bars[0]);
   const uint32_t buf0 = smem_u32(sbuf);
-  auto rows_of = [&](long long item, int& r0, int& nr) {
-    const int band = static_cast<int>(item % nband);
+  // item -> (plane, band) with one 32-bit divide (64-bit div/mod is a long
+  // emulated sequence: it dominated the per-item cost)
+  auto rows_of = [&](int item, int& plane, int& r0, int& nr) {
+    plane = item / nband;
+    const int band = item - plane * nband;
     const int y0 = band * RB;
     const int lo = max(0, 2 * y0 - 1);
     const int hi = min(H - 1, 2 * (y0 + RB) - 1);
     r0 = lo;
     nr = hi - lo + 1;
   };
-  auto issue = [&](long long item, int st) {
-    int r0, nr;
-    rows_of(item, r0, nr);
-    const long long plane = item / nband;
+  auto issue = [&](int item, int st) {
+    int plane, r0, nr;
+    rows_of(item, plane, r0, nr);
     const uint32_t bar = bar0 + 8u * st;
+    if (p.dbg & 2) {  // timing experiment: no loads
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+      return;
+    }
     if (TM) {
       // one tensor-map box of 2 RB + 1 rows of the [planes * H][W] matrix
       // (rows past the last plane are zero-filled and never read)
@@ -194,29 +200,30 @@ __global__ void __launch_bounds__(NT) maxpool3s2_bulk_kernel(const float* __rest
       asm volatile(
           "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
           "[%4];" ::"r"(buf0 + 4u * st * stage_floats),
-          "l"(reinterpret_cast<uint64_t>(&rows_map)), "r"(0), "r"(static_cast<int>(plane * H + r0)), "r"(bar)
+          "l"(reinterpret_cast<uint64_t>(&rows_map)), "r"(0), "r"(plane * H + r0), "r"(bar)
           : "memory");
     } else {
-      const float* src = in + (plane * H + r0) * (long long)W;
+      const float* src = in + ((long long)plane * H + r0) * W;
       const uint32_t bytes = static_cast<uint32_t>(nr) * W * 4u;
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
       asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                    ::"r"(buf0 + 4u * st * stage_floats), "l"(src), "r"(bytes), "r"(bar) : "memory");
     }
   };
-  const long long first = blockIdx.x;
-  const long long step = gridDim.x;
+  const int first = blockIdx.x;
+  const int step = gridDim.x;
   pdl_launch_dependents();
   if (threadIdx.x == 0) {
     for (int i = 0; i < ns; ++i) mp_mbar_init(bar0 + 8u * i, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     // warm L2 with this CTA's first bands while the previous launch drains
     for (int i = 0; i < ns; ++i) {
-      const long long item = first + i * step;
+      const int item = first + i * step;
       if (item >= n_items) break;
-      int r0, nr;
-      rows_of(item, r0, nr);
-      prefetch_l2(in + ((item / nband) * H + r0) * (long long)W, static_cast<uint32_t>(nr) * W * 4u);
+      int plane, r0, nr;
+      rows_of(item, plane, r0, nr);
+      if (!(p.dbg & 4))
+        prefetch_l2(in + ((long long)plane * H + r0) * W, static_cast<uint32_t>(nr) * W * 4u);
     }
   }
   __syncthreads();
@@ -226,42 +233,76 @@ __global__ void __launch_bounds__(NT) maxpool3s2_bulk_kernel(const float* __rest
       if (first + i * step < n_items) issue(first + i * step, i);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int it = 0;
-  for (long long item = first; item < n_items; item += step, ++it) {
-    const int st = it % ns;
-    const uint32_t parity = (it / ns) & 1;
+  int st = 0;
+  uint32_t parity = 0;
+  for (int item = first; item < n_items; item += step, ++it) {
     mp_mbar_wait(bar0 + 8u * st, parity);
-    int r0, nr;
-    rows_of(item, r0, nr);
-    const long long plane = item / nband;
-    const int y0 = static_cast<int>(item % nband) * RB;
+    int plane, r0, nr;
+    rows_of(item, plane, r0, nr);
+    const int y0 = (item - plane * nband) * RB;
+    float* orow = out + (long long)plane * Ho * Wo;
     const float* sb = sbuf + st * stage_floats;
-    // warp w computes output rows y0 + w, y0 + w + NT/32, ...
-    for (int yy = warp; yy < RB; yy += NT / 32) {
-      const int y = y0 + yy;
-      if (y >= Ho) break;
-      for (int c4 = lane; c4 * 4 < W; c4 += 32) {
-        const int col0 = c4 * 4;
-        float r0v = p.init, r1v = p.init;
+    if (p.vec_out) {
+      // The band's output rows are contiguous (RB * Wo floats): thread t
+      // writes outputs 4t .. 4t+3 of the band with one 16-byte store, so a
+      // warp store covers whole 128-byte lines (a partial-line store per
+      // row measured ~2x slower for the output stream).
+      const int q = Wo / 4;  // 16-byte groups per output row
+      const int rows = min(RB, Ho - y0);
+      for (int t = threadIdx.x; t < rows * q; t += NT) {
+        const int yy = t / q;
+        const int x0 = (t - yy * q) * 4;  // first output column
+        const int y = y0 + yy;
+        const int c0 = 2 * x0;            // input columns c0 - 1 .. c0 + 7
+        float r[4] = {p.init, p.init, p.init, p.init};
 #pragma unroll
         for (int ky = 0; ky < 3; ++ky) {
           int iy = 2 * y - 1 + ky;
           iy = iy < 0 ? 0 : (iy > H - 1 ? H - 1 : iy);
           const float* row = sb + (iy - r0) * W;
-          const float4 q = *reinterpret_cast<const float4*>(row + col0);
-          const float l = col0 == 0 ? q.x : row[col0 - 1];
-          r0v = fold_max(r0v, l);
-          r0v = fold_max(r0v, q.x);
-          r0v = fold_max(r0v, q.y);
-          r1v = fold_max(r1v, q.y);
-          r1v = fold_max(r1v, q.z);
-          r1v = fold_max(r1v, q.w);
+          const float4 a4 = *reinterpret_cast<const float4*>(row + c0);
+          const float4 b4 = *reinterpret_cast<const float4*>(row + c0 + 4);
+          const float l = c0 == 0 ? a4.x : row[c0 - 1];
+          r[0] = fold_max(fold_max(fold_max(r[0], l), a4.x), a4.y);
+          r[1] = fold_max(fold_max(fold_max(r[1], a4.y), a4.z), a4.w);
+          r[2] = fold_max(fold_max(fold_max(r[2], a4.w), b4.x), b4.y);
+          r[3] = fold_max(fold_max(fold_max(r[3], b4.y), b4.z), b4.w);
         }
-        *reinterpret_cast<float2*>(out + (plane * Ho + y) * (long long)Wo + col0 / 2) =
-            make_float2(post_op(r0v, p.post), post_op(r1v, p.post));
+        if (!(p.dbg & 1))
+          *reinterpret_cast<float4*>(orow + y * Wo + x0) =
+              make_float4(post_op(r[0], p.post), post_op(r[1], p.post), post_op(r[2], p.post), post_op(r[3], p.post));
+      }
+    } else {
+      // warp w computes output rows y0 + w, y0 + w + NT/32, ...
+      for (int yy = warp; yy < RB; yy += NT / 32) {
+        const int y = y0 + yy;
+        if (y >= Ho) break;
+        for (int c4 = lane; c4 * 4 < W; c4 += 32) {
+          const int col0 = c4 * 4;
+          float r0v = p.init, r1v = p.init;
+#pragma unroll
+          for (int ky = 0; ky < 3; ++ky) {
+            int iy = 2 * y - 1 + ky;
+            iy = iy < 0 ? 0 : (iy > H - 1 ? H - 1 : iy);
+            const float* row = sb + (iy - r0) * W;
+            const float4 qv = *reinterpret_cast<const float4*>(row + col0);
+            const float l = col0 == 0 ? qv.x : row[col0 - 1];
+            r0v = fold_max(r0v, l);
+            r0v = fold_max(r0v, qv.x);
+            r0v = fold_max(r0v, qv.y);
+            r1v = fold_max(r1v, qv.y);
+            r1v = fold_max(r1v, qv.z);
+            r1v = fold_max(r1v, qv.w);
+          }
+          if (!(p.dbg & 1))
+            *reinterpret_cast<float2*>(orow + y * Wo + col0 / 2) =
+                make_float2(post_op(r0v, p.post), post_op(r1v, p.post));
+        }
       }
     }
     __syncthreads();  // everyone is done with stage st: refill it
     if (threadIdx.x == 0 && item + ns * step < n_items) issue(item + ns * step, st);
+    if (++st == ns) { st = 0; parity ^= 1; }
   }
 }
 
@@ -281,16 +322,20 @@ merit_status launch_maxpool(const merit_plan& plan, const void* a, void* out, vo
     // 7 four-warp CTAs per SM with a 4..8-band ring keep ~200 KB of copies in
     // flight per SM, which is what the HBM stream needs at this size
     int RBv = 8;
-    if (const char* re = getenv("MERIT_MP_RB")) RBv = atoi(re) == 4 ? 4 : 8;
+    if (const char* re = getenv("MERIT_MP_RB")) {
+      const int v = atoi(re);
+      RBv = (v == 4 || v == 16 || v == 28) ? v : 8;
+    }
     const int nband = (p.Ho + RBv - 1) / RBv;
     const long long items = p.planes * nband;
+    if (items >= (1LL << 31)) return fail(MERIT_E_UNSUPPORTED_VIEW, "too many max-pool bands for one launch");
     int ctas = 7;
     if (const char* ce = getenv("MERIT_MP_CTAS")) ctas = atoi(ce);
     const size_t stage = ((size_t)(2 * RBv + 1) * p.W * 4 + 127) / 128 * 128;
-    int ns = RBv == 4 ? 8 : 4;
+    int ns = RBv == 4 ? 8 : (RBv == 8 ? 4 : (RBv == 16 ? 2 : 1));
     if (const char* se = getenv("MERIT_MP_STAGES")) ns = atoi(se);
     if (ns > kMpMaxStages) ns = kMpMaxStages;
-    while (ns > 2 && ns * stage > 100 * 1024) --ns;
+    while (ns > 1 && ns * stage > 100 * 1024) --ns;
     const size_t smem = ns * stage;
     if (smem <= 200 * 1024) {
       long long grid = (long long)num_sms() * ctas;
@@ -312,11 +357,17 @@ merit_status launch_maxpool(const merit_plan& plan, const void* a, void* out, vo
                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
       }
-      auto k = RBv == 4 ? (tm ? maxpool3s2_bulk_kernel<128, 4, true> : maxpool3s2_bulk_kernel<128, 4, false>)
-                        : (tm ? maxpool3s2_bulk_kernel<128, 8, true> : maxpool3s2_bulk_kernel<128, 8, false>);
+      auto k = tm ? maxpool3s2_bulk_kernel<128, 8, true> : maxpool3s2_bulk_kernel<128, 8, false>;
+      if (RBv == 4) k = tm ? maxpool3s2_bulk_kernel<128, 4, true> : maxpool3s2_bulk_kernel<128, 4, false>;
+      if (RBv == 16) k = tm ? maxpool3s2_bulk_kernel<128, 16, true> : maxpool3s2_bulk_kernel<128, 16, false>;
+      if (RBv == 28) k = tm ? maxpool3s2_bulk_kernel<128, 28, true> : maxpool3s2_bulk_kernel<128, 28, false>;
       cudaError_t e = set_smem_attr(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return cuda_check(e, "set_smem_attr(maxpool)");
-      e = launch_pdl(k, dim3(static_cast<unsigned>(grid)), dim3(128), smem, s, 1, in, o, p, nband, items, ns,
+      MaxpoolParams pp = p;
+      if (const char* de = getenv("MERIT_MP_DEBUG")) pp.dbg = atoi(de);
+      pp.vec_out = (p.Wo % 4 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+      e = launch_pdl(k, dim3(static_cast<unsigned>(grid)), dim3(128), smem, s, 1, in, o, pp, nband,
+                     static_cast<int>(items), ns,
                      rmap);
       if (e != cudaSuccess) return cuda_check(e, "launch(maxpool3s2_bulk_kernel)");
       return launch_status("maxpool3s2_bulk_kernel");

@@ -71,6 +71,8 @@ struct MaxpoolParams {
   int32_t post = POST_ADD_ZERO;
   float init = -3.0e38f;           // MOVC constant of Pre_1
   int32_t fast = 0;                // 3x3 / stride 2 / offset -1 warp-row path
+  int32_t vec_out = 0;             // launch-time: Wo % 4 == 0 and 16-byte aligned output
+  int32_t dbg = 0;                 // launch-time timing experiments (MERIT_MP_DEBUG)
 };
 
 // K2: L1 block matching (motion estimation, workloads.hpp:255-279).
