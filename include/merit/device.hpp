@@ -17,6 +17,7 @@
 
 #include <cstdint>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "merit/engine.hpp"
@@ -128,6 +129,38 @@ inline Tensor run_full(const Workload& w, uint32_t flags = 0) {
   st = merit_dev_run_host(g.p, a, b, o, nullptr, nullptr);
   if (st != MERIT_OK) detail::raise(st);
   return out;
+}
+
+/// engine.hpp:289-295 on the device.  The plan is validated by the reference's
+/// own TilingPlan::validate (BadParams); the result is run_full's (the device
+/// executes its own footprint-staged tiling) and the report is
+/// the reference's TrafficReport for the plan (Eq. 6 words per pass, computed
+/// by merit_dev_tiled_traffic).  EngineConfig's scratchpad capacities are
+/// accepted and not enforced.
+inline std::pair<Tensor, TrafficReport> run_tiled(const Workload& w, const TilingPlan& plan,
+                                                  const EngineConfig& cfg = {}, uint32_t flags = 0) {
+  (void)cfg;
+  w.validate();
+  plan.validate(w.p_shape(), w.a_shape());
+  TrafficReport rep;
+  {
+    detail::Desc D;
+    detail::fill(D, w, flags);
+    detail::PlanGuard g;
+    merit_status st = merit_dev_plan_create(&D.d, &g.p);
+    if (st != MERIT_OK) detail::raise(st);
+    merit_traffic_report r{};
+    st = merit_dev_tiled_traffic(g.p, plan.t_p.data(), plan.t_a.data(), &r);
+    if (st != MERIT_OK) detail::raise(st);
+    rep.dram_read_words_a = r.dram_read_words_a;
+    rep.dram_read_words_b = r.dram_read_words_b;
+    rep.dram_write_words = r.dram_write_words;
+    rep.scratchpad_peak_words_a = r.scratchpad_peak_words_a;
+    rep.scratchpad_peak_words_b = r.scratchpad_peak_words_b;
+    rep.passes = r.passes;
+    rep.macs = r.macs;
+  }
+  return {run_full(w, flags), rep};
 }
 
 /// Which device kernel a workload lowers to (MERIT_KERNEL_*), without running it.

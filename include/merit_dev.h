@@ -233,6 +233,26 @@ merit_status merit_dev_run(const merit_plan* plan, const void* d_src_a, const vo
 merit_status merit_dev_run_host(const merit_plan* plan, const void* h_src_a, const void* h_src_b,
                                 void* h_out, void* h_aux, void* cuda_stream);
 
+/* merit::run_tiled's traffic report (engine.hpp:72-80, :189-278) for a
+ * TilingPlan {t_p, t_a} over this plan's workload: the plan is validated like
+ * TilingPlan::validate (engine.hpp:50-63; MERIT_E_BAD_PARAMS) and every pass
+ * is charged its Eq. 6 footprint box (view.hpp:121-149; negative strides ->
+ * MERIT_E_NEGATIVE_STRIDE), exactly as the reference counts words.  The
+ * device executes its own tiling, so the scratchpad
+ * capacities of EngineConfig are not enforced.  Host-only: no
+ * device needed.  t_p / t_a hold p_rank / a_rank extents. */
+typedef struct merit_traffic_report {
+  uint64_t dram_read_words_a;
+  uint64_t dram_read_words_b;
+  uint64_t dram_write_words;
+  uint64_t scratchpad_peak_words_a;
+  uint64_t scratchpad_peak_words_b;
+  uint64_t passes;
+  uint64_t macs;
+} merit_traffic_report;
+merit_status merit_dev_tiled_traffic(const merit_plan* plan, const int64_t* t_p, const int64_t* t_a,
+                                     merit_traffic_report* report);
+
 /* Deterministic input synthesis shared by tests and the benchmark
  * (workloads.hpp:74-105 SplitMix64 / fill_random, and the seeded frame
  * generator of SURVEY §8(d)).  Host-only. */

@@ -7,10 +7,10 @@ BASELINE configurations (``workloads.py``).
 """
 from .merit import (AluInstr, Boundary, Dst, Dtype, Error, ErrorCode, Kernel, LookupTable, Op,
                     Operand, Plan, StrategyProgram, ViewSpec, ViewTerm, Workload, run_full,
-                    run_full_argmin, FLAG_ARGMIN, FLAG_EXACT, FLAG_FAST_BF16, FLAG_NO_MAP)
+                    run_full_argmin, run_tiled, FLAG_ARGMIN, FLAG_EXACT, FLAG_FAST_BF16, FLAG_NO_MAP)
 from . import workloads
 
 __all__ = ["AluInstr", "Boundary", "Dst", "Dtype", "Error", "ErrorCode", "Kernel", "LookupTable",
            "Op", "Operand", "Plan", "StrategyProgram", "ViewSpec", "ViewTerm", "Workload",
-           "run_full", "run_full_argmin", "workloads", "FLAG_ARGMIN", "FLAG_EXACT",
+           "run_full", "run_full_argmin", "run_tiled", "workloads", "FLAG_ARGMIN", "FLAG_EXACT",
            "FLAG_FAST_BF16", "FLAG_NO_MAP"]

@@ -62,6 +62,12 @@ class PlanInfoC(C.Structure):
                 ("description", C.c_char * 256)]
 
 
+class TrafficReportC(C.Structure):  # merit_traffic_report (engine.hpp:72-80)
+    _fields_ = [("dram_read_words_a", C.c_uint64), ("dram_read_words_b", C.c_uint64),
+                ("dram_write_words", C.c_uint64), ("scratchpad_peak_words_a", C.c_uint64),
+                ("scratchpad_peak_words_b", C.c_uint64), ("passes", C.c_uint64), ("macs", C.c_uint64)]
+
+
 # Exported symbols and their prototypes (kept in sync with include/merit_dev.h;
 # tests/test_capi_symbols.py checks every declared symbol is exported).
 PROTOTYPES = {
@@ -84,6 +90,7 @@ PROTOTYPES = {
     "merit_f32_to_bf16": (None, [C.c_void_p, C.c_void_p, C.c_int64]),
     "merit_dev_launch_count": (C.c_int64, []),
     "merit_dev_last_kernel": (C.c_char_p, []),
+    "merit_dev_tiled_traffic": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(TrafficReportC)]),
 }
 
 _lib = None

@@ -372,6 +372,18 @@ class Plan:
         _check(self.lib.merit_dev_run(self.handle, self._ptr(d_src_a), self._ptr(d_src_b),
                                       self._ptr(d_out), self._ptr(d_aux), C.c_void_p(stream or 0)))
 
+    def tiled_traffic(self, t_p, t_a) -> dict:
+        """merit::run_tiled's TrafficReport (engine.hpp:72-80) for the tiling plan
+        {t_p, t_a}: validated like TilingPlan::validate, Eq. 6 words per pass."""
+        tp = np.ascontiguousarray(t_p, np.int64)
+        ta = np.ascontiguousarray(t_a, np.int64)
+        if tp.size != self._holder.desc.view_a.p_rank or ta.size != self._holder.desc.view_a.a_rank:
+            raise Error(ErrorCode.BadParams, "tile rank mismatch")
+        r = _capi.TrafficReportC()
+        _check(self.lib.merit_dev_tiled_traffic(self.handle, tp.ctypes.data_as(C.c_void_p),
+                                                ta.ctypes.data_as(C.c_void_p), C.byref(r)))
+        return {k: int(getattr(r, k)) for k, _ in r._fields_}
+
     # -- host buffers: the reference's run_full convention --------------------
     def run_host(self, src_a, src_b, out: Optional[np.ndarray] = None,
                  aux: Optional[np.ndarray] = None, stream=None):
@@ -402,6 +414,17 @@ def run_full(w: Workload, flags: int = 0):
     plan = Plan(w, flags)
     out, _ = plan.run_host(_host(w.src_a), _host(w.src_b))
     return out
+
+
+def run_tiled(w: Workload, t_p, t_a, flags: int = 0):
+    """engine.hpp:289-295 on the device: the output of run_full (the device
+    executes its own footprint-staged tiling) and the TilingPlan's
+    TrafficReport as a dict (scratchpad capacities are not enforced)."""
+    _check_sources(w)
+    plan = Plan(w, flags)
+    rep = plan.tiled_traffic(t_p, t_a)
+    out, _ = plan.run_host(_host(w.src_a), _host(w.src_b))
+    return out, rep
 
 
 def run_full_argmin(w: Workload, with_map: bool = True):

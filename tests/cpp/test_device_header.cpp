@@ -78,6 +78,40 @@ int main() {
     std::printf("%s reject-error-code ref=%d dev=%d\n", ok ? "PASS" : "FAIL", int(rc), int(dc));
     if (!ok) ++failures;
   }
+  // run_tiled (engine.hpp:289-295): same output as the reference's tiled run
+  // and the identical TrafficReport (tests/test_engine.cpp:91-107's KAT plan)
+  {
+    Workload w = build_template("conv2d", {{"h", 68}, {"w", 68}, {"k", 5}, {"pad", 0}});
+    fill_random(w.src_a, 1);
+    fill_random(w.src_b, 2);
+    TilingPlan plan{{16, 8}, {5, 5}};
+    EngineConfig cfg;
+    auto [want, wrep] = run_tiled(w, plan, cfg);
+    auto [got, grep] = device::run_tiled(w, plan, cfg);
+    double worst = 0;
+    for (size_t i = 0; i < got.fdata.size(); ++i)
+      worst = std::max(worst, std::abs(double(got.fdata[i]) - want.fdata[i]) / (1.0 + std::abs(want.fdata[i])));
+    const bool same = wrep.dram_read_words_a == grep.dram_read_words_a &&
+                      wrep.dram_read_words_b == grep.dram_read_words_b &&
+                      wrep.dram_write_words == grep.dram_write_words &&
+                      wrep.scratchpad_peak_words_a == grep.scratchpad_peak_words_a &&
+                      wrep.scratchpad_peak_words_b == grep.scratchpad_peak_words_b &&
+                      wrep.passes == grep.passes && wrep.macs == grep.macs;
+    const bool ok = same && got.shape == want.shape && worst <= 1e-4 && grep.scratchpad_peak_words_a == 240;
+    std::printf("%s run_tiled conv2d 5x5 plan {16,8}x{5,5}: peak_a=%llu passes=%llu worst=%.3g\n",
+                ok ? "PASS" : "FAIL", (unsigned long long)grep.scratchpad_peak_words_a,
+                (unsigned long long)grep.passes, worst);
+    if (!ok) ++failures;
+    // an invalid plan fails with the reference's error code
+    TilingPlan bad{{16, 8}, {5, 4}};
+    bool rt = false, dt = false;
+    ErrorCode rc{}, dc{};
+    try { run_tiled(w, bad, cfg); } catch (const Error& e) { rt = true; rc = e.code; }
+    try { device::run_tiled(w, bad, cfg); } catch (const Error& e) { dt = true; dc = e.code; }
+    const bool ok2 = rt && dt && rc == dc;
+    std::printf("%s run_tiled-bad-plan ref=%d dev=%d\n", ok2 ? "PASS" : "FAIL", int(rc), int(dc));
+    if (!ok2) ++failures;
+  }
   std::printf("%d failure(s)\n", failures);
   return failures == 0 ? 0 : 1;
 }

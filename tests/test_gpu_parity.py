@@ -375,3 +375,15 @@ def test_generic_errors_raise_like_reference(cuda):
     with pytest.raises(Error) as ei:
         run_full(w)
     assert ei.value.code == ErrorCode.DivByZero
+
+
+# ------------------------------------------------------------ run_tiled --
+def test_run_tiled_output_and_report(cuda):
+    # engine.hpp:289-295: the device result equals run_full's, the report is
+    # the plan's (pinned on CPU in tests/test_tiled_traffic.py)
+    from paper_1911_03458_b200 import run_tiled
+    w = W.maxpool_nchw_view(2, 4, 16, 16)
+    w.src_a = W.gen_uniform([2, 4, 16, 16], 91)
+    out, rep = run_tiled(w, [1, 2, 4, 8], [3, 3])
+    assert np.array_equal(out.view(np.uint32), run_full(w).view(np.uint32))
+    assert rep["passes"] == 2 * 2 * 2 * 1 and rep["macs"] == 2 * 4 * 8 * 8 * 9
