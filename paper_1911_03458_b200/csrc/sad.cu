@@ -433,16 +433,21 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
   const int per_block = p.WX;
   if (per_block > kSadMaxThreads)
     return fail(MERIT_E_UNSUPPORTED_VIEW, "search window too wide for the SAD kernel");
-  // Blocks per tile: least idle-lane fraction within the thread budget.
+  // Blocks per tile: the most busy lanes per SM sub-partition.  Warps of a
+  // CTA are spread warp % 4 over the four sub-partitions, so a CTA of w
+  // warps costs ceil(w / 4) * 4 warp slots of VABSDIFF4 time (7 warps load
+  // three sub-partitions with two warps and one with one: profiled as 12% of
+  // all stall samples at the tile barrier).
   L.TBX = 1;
-  double best_waste = 2.0;
+  double best_eff = -1.0;
   for (int t = 1; t <= 16 && t <= p.BX; ++t) {
     const int items = t * per_block;
-    const int threads = (items + 31) / 32 * 32;
-    if (threads > kSadMaxThreads) break;
-    const double waste = double(threads - items) / threads;
-    if (waste < best_waste - 0.02) {
-      best_waste = waste;
+    const int warps = (items + 31) / 32;
+    if (warps * 32 > kSadMaxThreads) break;
+    const int tiles = (p.BX + t - 1) / t;  // the last tile of a row may be partial
+    const double eff = double(items) / (((warps + 3) / 4) * 4 * 32) * double(p.BX) / (tiles * t);
+    if (eff > best_eff + 1e-9) {
+      best_eff = eff;
       L.TBX = t;
     }
   }
