@@ -58,6 +58,11 @@ def ref():
         L.ref_run_full.restype = C.c_int
         L.ref_run_tiled.argtypes = [C.c_void_p] * 3 + [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.ref_run_tiled.restype = C.c_int
+        L.ref_mrt1_write.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int64]
+        L.ref_mrt1_write.restype = C.c_int64
+        L.ref_mrt1_read.argtypes = [C.c_void_p, C.c_int64, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                    C.POINTER(C.c_int), C.c_void_p, C.c_void_p, C.c_int64]
+        L.ref_mrt1_read.restype = C.c_int
         L.ref_fill_random_f32.argtypes = [C.c_void_p, C.c_int64, C.c_uint64, C.c_double, C.c_double]
         L.ref_fill_random_i16.argtypes = [C.c_void_p, C.c_int64, C.c_uint64]
         L.ref_template_case.argtypes = [C.c_char_p, C.c_char_p, C.c_uint64, C.c_void_p,
@@ -174,6 +179,36 @@ def ref_run_tiled(w, t_p, t_a):
     if st:
         raise Error(st, ref().ref_last_error().decode())
     return out, traffic
+
+
+def ref_mrt1_bytes(arr, frac_bits=0) -> bytes:
+    """merit::Tensor::write of a float32 / int16 array (the reference's bytes)."""
+    a = np.ascontiguousarray(arr)
+    shape = np.asarray(a.shape, np.int64)
+    cap = 8 + 4 * a.ndim + a.nbytes
+    buf = np.empty(cap, np.uint8)
+    n = ref().ref_mrt1_write(0 if a.dtype == np.float32 else 1, frac_bits, _p(shape), a.ndim, _p(a), _p(buf), cap)
+    if n < 0:
+        raise RuntimeError(ref().ref_last_error().decode())
+    return buf[:n].tobytes()
+
+
+def ref_mrt1_parse(data: bytes):
+    """merit::Tensor::read: (array, frac_bits) or raises Error(code)."""
+    from paper_1911_03458_b200.merit import Error
+    raw = np.frombuffer(data, np.uint8)
+    dt, fb, rk = C.c_int(), C.c_int(), C.c_int()
+    shape = np.zeros(16, np.int64)
+    cap = max(len(data), 16)
+    payload = np.empty(cap, np.uint8)
+    st = ref().ref_mrt1_read(_p(np.ascontiguousarray(raw)), len(data), C.byref(dt), C.byref(fb), C.byref(rk),
+                             _p(shape), _p(payload), cap)
+    if st:
+        raise Error(st, ref().ref_last_error().decode())
+    shp = tuple(int(x) for x in shape[:rk.value])
+    n = int(np.prod(shp))
+    arr = payload[:n * (4 if dt.value == 0 else 2)].view(np.float32 if dt.value == 0 else np.int16).reshape(shp)
+    return arr.copy(), fb.value
 
 
 def ref_template_case(name, params: dict, seed: int, cap=1 << 22):

@@ -10,6 +10,7 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <sstream>
 #include <string>
 
 #include "merit/engine.hpp"
@@ -192,6 +193,52 @@ static merit::Params parse_params(const char* s) {
     pos = comma + 1;
   }
   return p;
+}
+
+// merit::Tensor::write (tensor.hpp:123-139): MRT1 bytes of a REAL32 (dtype 0)
+// or FIX16 (dtype 1) tensor.  Returns the byte count, or -1 if cap is short.
+int64_t ref_mrt1_write(int dtype, int frac_bits, const int64_t* shape, int rank, const void* data, void* out,
+                       int64_t cap) {
+  try {
+    merit::Shape sh(shape, shape + rank);
+    merit::Tensor t = dtype == 0 ? merit::Tensor::real(sh) : merit::Tensor::fix(sh, frac_bits);
+    if (dtype == 0)
+      std::memcpy(t.fdata.data(), data, t.fdata.size() * 4);
+    else
+      std::memcpy(t.qdata.data(), data, t.qdata.size() * 2);
+    std::ostringstream os;
+    t.write(os);
+    const std::string b = os.str();
+    if (static_cast<int64_t>(b.size()) > cap) return -1;
+    std::memcpy(out, b.data(), b.size());
+    return static_cast<int64_t>(b.size());
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -2;
+  }
+}
+
+// merit::Tensor::read (tensor.hpp:141-163) of `n` bytes: 0 and the tensor's
+// dtype / rank / shape / payload (cap bytes), or the ErrorCode + 1 it throws.
+int ref_mrt1_read(const void* bytes, int64_t n, int* dtype, int* frac_bits, int* rank, int64_t* shape,
+                  void* payload, int64_t cap) {
+  try {
+    std::istringstream is(std::string(static_cast<const char*>(bytes), static_cast<size_t>(n)));
+    merit::Tensor t = merit::Tensor::read(is);
+    *dtype = t.dtype == merit::Dtype::Real32 ? 0 : 1;
+    *frac_bits = t.frac_bits;
+    *rank = static_cast<int>(t.shape.size());
+    for (size_t i = 0; i < t.shape.size(); ++i) shape[i] = t.shape[i];
+    const int64_t bytes_out = t.dtype == merit::Dtype::Real32 ? int64_t(t.fdata.size()) * 4 : int64_t(t.qdata.size()) * 2;
+    if (bytes_out > cap) return -1;
+    std::memcpy(payload, t.dtype == merit::Dtype::Real32 ? static_cast<const void*>(t.fdata.data())
+                                                         : static_cast<const void*>(t.qdata.data()),
+                static_cast<size_t>(bytes_out));
+    return 0;
+  } catch (const merit::Error& e) {
+    g_err = e.what();
+    return code_of(e);
+  }
 }
 
 int ref_template_case(const char* name, const char* params, uint64_t seed, void* src_a,

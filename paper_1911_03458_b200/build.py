@@ -66,7 +66,26 @@ def build(verbose: bool = False, force: bool = False) -> Path:
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
+    build_cli(verbose, force)
     return LIB
+
+
+CLI_SRC = PKG / "cli" / "merit_dev.cpp"
+CLI = PKG / "bin" / "merit-dev"
+
+
+def build_cli(verbose: bool = False, force: bool = False) -> Path:
+    """bin/merit-dev: the reference CLI's `run --manifest` path over the C ABI
+    (host C++, linked to libmerit_dev.so through an $ORIGIN rpath)."""
+    CLI.parent.mkdir(exist_ok=True)
+    if force or _stale(CLI, [CLI_SRC, LIB, INCLUDE / "merit_dev.h"]):
+        cxx = shutil.which("g++") or "g++"
+        cmd = [cxx, "-O2", "-std=c++17", "-Wall", f"-I{INCLUDE}", str(CLI_SRC), "-o", str(CLI),
+               f"-L{PKG}", "-l:libmerit_dev.so", "-Wl,-rpath,$ORIGIN/.."]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+    return CLI
 
 
 if __name__ == "__main__":
