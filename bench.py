@@ -149,21 +149,29 @@ class Case:
             self.rotation = f"{nsets} rotating input/output sets ({nsets * 39.3:.0f} MB > 126 MB L2)"
             self.dtype = "u8 (int32 SAD)"
         elif config == "C1":
-            w = W.config_workload("C1", with_inputs=False)
+            # batch-sharded: 8 / world images per rank
+            w = W.config_workload("C1", scale=world, with_inputs=False)
+            n_img = w.view_a.p_shape[0]
             self.plan = Plan(w)
-            nsets = 6
+            nsets = 6 * max(1, 8 // n_img)
             for s in range(nsets):
-                x = W.gen_uniform([8, 64, 112, 112], 1 + rank * 1000 + s)
+                x = W.gen_uniform([n_img, 64, 112, 112], 1 + rank * 1000 + s)
                 self.sets.append(self._bufs(x, np.zeros(1, np.float32)))
             self.cpu_inputs = (x, np.zeros(1, np.float32))
-            self.units = "8 images (8,64,112,112) per rank per step"
+            self.units = f"{n_img} of the 8 images (N,64,112,112) per rank per step"
             self.workload = "C1 maxpool 3x3 s2 p1 fp32 NCHW (8,64,112,112)"
-            self.rotation = f"{nsets} rotating input/output sets ({nsets * 32.1:.0f} MB > 126 MB L2)"
+            self.rotation = f"{nsets} rotating input/output sets ({nsets * 4.0 * n_img:.0f} MB > 126 MB L2)"
             self.dtype = "f32"
         elif config in ("C3", "C4"):
-            w = W.config_workload(config, with_inputs=True, seed_offset=rank * 1000)
+            # C4 is batch-sharded over the GPUs (BASELINE configs[3]): 256 / world
+            # images per rank; C3 runs its 32 images on every rank
+            w = W.config_workload(config, scale=world if config == "C4" else 1, with_inputs=True,
+                                  seed_offset=rank * 1000)
+            n_img = w.view_a.p_shape[0]
             self.plan = Plan(w)
-            nsets = 4 if config == "C3" else 1
+            # rotating device copies so the sets together exceed 2x L2 (C4
+            # shards at 8 GPUs are 51 MB)
+            nsets = 4 if config == "C3" else max(1, -(-300 // int(1.6 * n_img)))
             a0, b0 = w.src_a, w.src_b
             for s in range(nsets):
                 a = a0 if s == 0 else (W.gen_uniform(list(a0.shape), 3 + rank * 1000 + s)
@@ -172,11 +180,11 @@ class Case:
             self.plan.pack_b(self.sets[0][1])
             torch.cuda.synchronize()
             self.cpu_inputs = (a0, b0)
-            self.units = ("32 images (32,64,56,56) fp32" if config == "C3"
-                          else "256 images (256,128,56,56) bf16") + " per rank per step"
+            self.units = ("32 images (32,64,56,56) fp32 per rank per step" if config == "C3"
+                          else f"{n_img} of the 256 images (N,128,56,56) bf16 per rank per step")
             self.workload = W.CONFIGS[config]
             self.rotation = (f"{nsets} rotating sets ({nsets * 51.5:.0f} MB > 126 MB L2)" if config == "C3"
-                             else "single set, 411 MB working set > 126 MB L2")
+                             else f"{nsets} rotating set(s) of {1.6 * n_img:.0f} MB (> 126 MB L2 in total)")
             self.dtype = "f32 (3-term bf16 split, fp32 accumulate)" if config == "C3" else "bf16 (fp32 accumulate)"
         elif config == "C5":
             pairs = max(1, 64 // world)
@@ -405,7 +413,7 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 5), "higher_is_better": True,
-        "scaling": "strong" if args.config == "C5" else "weak", "vs_baseline": None,
+        "scaling": "strong" if args.config in ("C1", "C4", "C5") else "weak", "vs_baseline": None,
         "dtype": case.dtype, "data": "synthetic (seeded SplitMix64 generators, SURVEY §8(d))",
         "config": {"workload": case.workload, "units": case.units,
                    "outputs_per_step_per_rank": case.outputs_per_step,
