@@ -210,8 +210,8 @@ __device__ __forceinline__ void issue_tile(const SadLaunch& L, const uint8_t* __
   }
 }
 
-template <int BLK, int D, int NBY>
-__global__ void __launch_bounds__(kSadThreads, 2)
+template <int BLK, int D, int NBY, int NT>
+__global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1)
 sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, void* __restrict__ out,
            int32_t* __restrict__ aux, SadLaunch L, const __grid_constant__ CUtensorMap ref_map,
            const __grid_constant__ CUtensorMap cur_map) {
@@ -438,19 +438,34 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
   // warps costs ceil(w / 4) * 4 warp slots of VABSDIFF4 time (7 warps load
   // three sub-partitions with two warps and one with one: profiled as 12% of
   // all stall samples at the tile barrier).
-  L.TBX = 1;
-  double best_eff = -1.0;
-  for (int t = 1; t <= 16 && t <= p.BX; ++t) {
-    const int items = t * per_block;
-    const int warps = (items + 31) / 32;
-    if (warps * 32 > kSadMaxThreads) break;
-    const int tiles = (p.BX + t - 1) / t;  // the last tile of a row may be partial
-    const double eff = double(items) / (((warps + 3) / 4) * 4 * 32) * double(p.BX) / (tiles * t);
-    if (eff > best_eff + 1e-9) {
-      best_eff = eff;
-      L.TBX = t;
+  auto best_tbx = [&](int budget, double& eff_out) {
+    int tbx = 1;
+    double best_eff = -1.0;
+    for (int t = 1; t <= 16 && t <= p.BX; ++t) {
+      const int items = t * per_block;
+      const int warps = (items + 31) / 32;
+      if (warps * 32 > budget) break;
+      const int tiles = (p.BX + t - 1) / t;  // the last tile of a row may be partial
+      const double eff = double(items) / (((warps + 3) / 4) * 4 * 32) * double(p.BX) / (tiles * t);
+      if (eff > best_eff + 1e-9) {
+        best_eff = eff;
+        tbx = t;
+      }
     }
-  }
+    eff_out = best_eff;
+    return tbx;
+  };
+  // 256-thread CTAs, two per SM; or one 512-thread CTA per SM when a wide
+  // window leaves many lanes idle in 256 threads (C5 +/-32: 3 blocks = 76%
+  // of lanes busy, 7 blocks in 512 threads = 89%)
+  double eff256 = 0, eff512 = 0;
+  const int tbx256 = best_tbx(256, eff256);
+  const int tbx512 = best_tbx(512, eff512);
+  // measured: C5 (eff 0.76 -> 0.87) 120 -> 99 ms; C2 (0.86 -> 0.97) 64 -> 67 us,
+  // the single CTA per SM exposes the tile barriers
+  int nt = (eff256 < 0.80 && eff512 > 1.08 * eff256) ? 512 : 256;
+  if (const char* te = getenv("MERIT_SAD_THREADS")) nt = atoi(te) == 512 ? 512 : 256;
+  L.TBX = nt == 512 ? tbx512 : tbx256;
   L.items = L.TBX * per_block;
   L.n_tiles_x = (p.BX + L.TBX - 1) / L.TBX;
   L.span = L.TBX * BLK + p.WX - 1;
@@ -513,16 +528,17 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
   const size_t smem =
       128 + 2ull * L.raw_buf + 2ull * L.cur_buf + 4ull * (4ull * L.CS + 2ull * L.nby * L.TBX) + 8 + 16;
   if (L.n_tiles == 0) return MERIT_OK;
-  if (smem > 110 * 1024) return fail(MERIT_E_UNSUPPORTED_VIEW, "SAD footprint exceeds shared memory");
-  auto kern = sad_kernel<BLK, D, 1>;
+  if (smem > (nt == 512 ? 220 : 110) * 1024)
+    return fail(MERIT_E_UNSUPPORTED_VIEW, "SAD footprint exceeds shared memory");
+  auto kern = nt == 512 ? sad_kernel<BLK, D, 1, 512> : sad_kernel<BLK, D, 1, 256>;
   if constexpr (BLK == 8) {
-    if (L.nby == 2) kern = sad_kernel<BLK, D, 2>;
+    if (L.nby == 2) kern = nt == 512 ? sad_kernel<BLK, D, 2, 512> : sad_kernel<BLK, D, 2, 256>;
   }
   cudaError_t e = set_smem_attr(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return cuda_check(e, "set_smem_attr(sad)");
   const int threads = (L.items + 31) / 32 * 32;
-  long long grid = 2LL * num_sms();
+  long long grid = (nt == 512 ? 1LL : 2LL) * num_sms();
   if (grid > L.n_tiles) grid = L.n_tiles;
   e = launch_pdl(kern, dim3(static_cast<unsigned>(grid)), dim3(threads), smem, s, 1, cur, ref, out, aux, L, ref_map,
                  cur_map);
