@@ -387,3 +387,13 @@ def test_run_tiled_output_and_report(cuda):
     out, rep = run_tiled(w, [1, 2, 4, 8], [3, 3])
     assert np.array_equal(out.view(np.uint32), run_full(w).view(np.uint32))
     assert rep["passes"] == 2 * 2 * 2 * 1 and rep["macs"] == 2 * 4 * 8 * 8 * 9
+
+
+def test_conv_random_shapes_all_dispatch_paths(cuda):
+    # a compact run of tools/conv_sweep.py (1,250 case x variant runs clean at
+    # seed 11): random shapes / strides / dtypes / Cout through every kernel
+    import subprocess, sys
+    r = subprocess.run([sys.executable, "tools/conv_sweep.py", "24", "5"], capture_output=True, text=True,
+                       cwd=str(__import__("pathlib").Path(__file__).resolve().parents[1]))
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert r.stdout.strip().endswith("bad 0"), r.stdout[-2000:]
