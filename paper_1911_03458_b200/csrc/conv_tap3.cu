@@ -463,6 +463,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tap3_kernel(Tap3Args A) {
 }  // namespace
 
 bool conv_tap3_eligible(const ConvParams& p) {
+  if (p.gemm) return false;
   return p.KW == 3 && p.dx == 1 && p.ox == -1 &&
          ((p.sx == 2 && p.in_bf16 && p.split == 1 && p.W % 2 == 0) ||
           (p.sx == 1 && p.Wo == p.W && (p.split == 1 ? p.in_bf16 : !p.in_bf16)));

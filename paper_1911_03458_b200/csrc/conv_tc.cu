@@ -419,7 +419,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(ConvArgs A) {
           const bool inb = valid && iy >= 0 && iy < p.H && ix >= 0 && ix < p.W;
           const int c0 = cb * 64 + h * 32;
           const int nc = inb ? min(32, p.Cin - c0) : 0;
-          const long long off = ((long long)n * p.Cin + c0) * HW + (long long)iy * p.W + ix;
+          const long long off = (long long)n * p.a_sn + (long long)c0 * p.a_sc + (long long)iy * p.a_sy +
+                                (long long)ix * p.a_sx;
+          const long long cs = p.a_sc;
           mbar_wait(empty_bar(stage), phase ^ 1);
           const uint32_t a_hi = ring + stage * A.stage_bytes;
           float v[32];
@@ -427,11 +429,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(ConvArgs A) {
             const uint16_t* src = static_cast<const uint16_t*>(A.in) + off;
 #pragma unroll
             for (int c = 0; c < 32; ++c)
-              v[c] = c < nc ? __uint_as_float(static_cast<uint32_t>(__ldg(src + c * HW)) << 16) : 0.f;
+              v[c] = c < nc ? __uint_as_float(static_cast<uint32_t>(__ldg(src + c * cs)) << 16) : 0.f;
           } else {
             const float* src = static_cast<const float*>(A.in) + off;
 #pragma unroll
-            for (int c = 0; c < 32; ++c) v[c] = c < nc ? __ldg(src + c * HW) : 0.f;
+            for (int c = 0; c < 32; ++c) v[c] = c < nc ? __ldg(src + c * cs) : 0.f;
           }
 #pragma unroll
           for (int j4 = 0; j4 < 4; ++j4) put8(a_hi, h * 4 + j4, v + j4 * 8);
@@ -543,11 +545,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(ConvArgs A) {
       if (valid) {
         const long long n = m / HoWo;
         const long long rem = m % HoWo;
-        obase = n * (long long)p.Cout * HoWo + rem;
+        obase = n * p.o_sn + rem * p.o_sp;
       }
       // Warm L2 with the input footprint of the tile two steps ahead (the
       // gather's loads then hit L2 instead of paying DRAM latency).
-      if (!(A.debug & 8)) {
+      if (!(A.debug & 8) && !p.gemm) {
         const int ahead = tile + 2 * gridDim.x;
         if (ahead < A.n_tiles) {
           const long long m0 = (long long)(ahead / p.n_tiles_n) * kBM;
@@ -586,7 +588,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(ConvArgs A) {
             if (co < p.Cout) {
               float v = __uint_as_float(r[j]);
               v = p.post == POST_RELU ? ((v < 0.f) ? 0.f : v) : __fadd_rn(v, 0.f);
-              __stcs(A.out + obase + (long long)co * HoWo, v);
+              __stcs(A.out + obase + (long long)co * p.o_sc, v);
             }
           }
         }
@@ -638,7 +640,7 @@ __global__ void conv_pack_kernel(const void* __restrict__ w, uint8_t* __restrict
       const int ci = cb * 64 + j * 8 + e8;
       float v = 0.f;
       if (co < p.Cout && ci < p.Cin) {
-        const long long idx = (((long long)co * p.Cin + ci) * p.KH + ky) * p.KW + kx;
+        const long long idx = (long long)co * p.w_so + (long long)ci * p.w_si + ky * p.KW + kx;
         if (W_BF16)
           v = __uint_as_float(static_cast<uint32_t>(static_cast<const uint16_t*>(w)[idx]) << 16);
         else
@@ -722,7 +724,7 @@ merit_status launch_conv(const merit_plan& plan, const void* a, const void* pack
     const char* dbg = getenv("MERIT_CONV_DEBUG");
     A.debug = dbg ? atoi(dbg) : 0;
   }
-  A.tap3 = (p.KW == 3 && p.dx == 1 && p.ox == -1 &&
+  A.tap3 = (!p.gemm && p.KW == 3 && p.dx == 1 && p.ox == -1 &&
             ((p.sx == 1 && p.Wo == p.W) || (p.sx == 2 && p.in_bf16 && p.W % 2 == 0 &&
                            (reinterpret_cast<uintptr_t>(a) % 4) == 0)))
                ? 1 : 0;

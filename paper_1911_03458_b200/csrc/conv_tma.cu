@@ -412,6 +412,7 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() { return tensor_map_encoder(); }
 }  // namespace
 
 bool conv_tma_eligible(const ConvParams& p, const void* a) {
+  if (p.gemm) return false;
   const char* e = getenv("MERIT_CONV_TMA");
   if (e && e[0] == '0') return false;
   return p.KW == 3 && p.dx == 1 && p.ox == -1 && p.sx == 2 && p.in_bf16 && p.split == 1 &&

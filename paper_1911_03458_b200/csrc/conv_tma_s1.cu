@@ -391,6 +391,7 @@ int slots_log2_for(int W) {
 // Geometric eligibility (plan time: decides nothing about packing, which is
 // shared with the other conv kernels).
 bool conv_s1_eligible(const ConvParams& p, const void* a) {
+  if (p.gemm) return false;
   const char* e = getenv("MERIT_CONV_S1");
   if (e && e[0] == '0') return false;
   return p.KW == 3 && p.dx == 1 && p.ox == -1 && p.sx == 1 && p.sy == 1 && p.Wo == p.W && !p.in_bf16 &&

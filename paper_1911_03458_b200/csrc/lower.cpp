@@ -322,6 +322,8 @@ bool lower_sad(const merit_workload_desc& d, const ViewAffine& fa, const ViewAff
 // Input view:  [N]: n; C: ci; H: y*sy + ky*dy + oy; W: x*sx + kx*dx + ox
 // Weight view: (Cout, Cin, KH, KW) <- (co, ci, ky, kx)
 // p = ([n,] co, y, x), a = (ci, ky, kx).
+bool finish_conv(const merit_workload_desc& d, int32_t post, ConvParams& cp);
+
 bool lower_conv(const merit_workload_desc& d, const ViewAffine& fa, const ViewAffine& fb,
                 int32_t post, ConvParams& cp, bool& swapped) {
   if (d.dtype_out != MERIT_F32) return false;
@@ -377,6 +379,17 @@ bool lower_conv(const merit_workload_desc& d, const ViewAffine& fa, const ViewAf
     cp.ox = (int32_t)fi.off[lead + 2];
     cp.in_bf16 = dti == MERIT_BF16;
     cp.w_bf16 = dtw == MERIT_BF16;
+    // NCHW input / OIHW weights / NCHW output
+    cp.a_sx = 1;
+    cp.a_sy = cp.W;
+    cp.a_sc = (int64_t)cp.H * cp.W;
+    cp.a_sn = (int64_t)cp.Cin * cp.a_sc;
+    cp.o_sp = 1;
+    cp.o_sc = (int64_t)cp.Ho * cp.Wo;
+    cp.o_sn = (int64_t)cp.Cout * cp.o_sc;
+    cp.w_si = (int64_t)cp.KH * cp.KW;
+    cp.w_so = (int64_t)cp.Cin * cp.w_si;
+    cp.gemm = 0;
     return true;
   };
   swapped = false;
@@ -384,6 +397,55 @@ bool lower_conv(const merit_workload_desc& d, const ViewAffine& fa, const ViewAf
     if (!try_one(d.view_b, fb, d.dtype_b, d.view_a, fa, d.dtype_a)) return false;
     swapped = true;
   }
+  return finish_conv(d, post, cp);
+}
+
+// GEMM view (workloads.hpp:122-136): C[i,j] = sum_t A[i,t] B[t,j], p = (m, n),
+// a = (k).  It runs on the general tensor-core kernel as a 1x1 "convolution"
+// of one image of M x 1 pixels with K input and N output channels, through
+// operand strides: A rows are pixels (channel stride 1, row stride K), B is
+// [K][N] (output-channel stride 1, input-channel stride N), C is [M][N].
+bool lower_gemm(const merit_workload_desc& d, const ViewAffine& fa, const ViewAffine& fb, int32_t post,
+                ConvParams& cp, bool& swapped) {
+  if (d.dtype_out != MERIT_F32) return false;
+  auto try_one = [&](const merit_view_spec& va, const ViewAffine& xa, int dta, const merit_view_spec& vb,
+                     const ViewAffine& xb, int dtb) -> bool {
+    if ((dta != MERIT_F32 && dta != MERIT_BF16) || (dtb != MERIT_F32 && dtb != MERIT_BF16)) return false;
+    if (va.src_rank != 2 || vb.src_rank != 2 || va.p_rank != 2 || va.a_rank != 1) return false;
+    // A[i, t]: axis 0 <- p0, axis 1 <- a0;  B[t, j]: axis 0 <- a0, axis 1 <- p1
+    if (!axis_single(xa, 0, 0, 1) || !axis_single(xa, 1, 2, 1) || !comp_unused(xa, 1)) return false;
+    if (!axis_single(xb, 0, 2, 1) || !axis_single(xb, 1, 1, 1) || !comp_unused(xb, 0)) return false;
+    if (xa.off[0] || xa.off[1] || xb.off[0] || xb.off[1]) return false;
+    const int64_t M = va.p_shape[0], N = va.p_shape[1], K = va.a_shape[0];
+    if (va.src_shape[0] != M || va.src_shape[1] != K || vb.src_shape[0] != K || vb.src_shape[1] != N)
+      return false;
+    cp = ConvParams{};
+    cp.N = 1;
+    cp.Cin = (int32_t)K;
+    cp.H = cp.Ho = (int32_t)M;
+    cp.W = cp.Wo = 1;
+    cp.Cout = (int32_t)N;
+    cp.KH = cp.KW = 1;
+    cp.in_bf16 = dta == MERIT_BF16;
+    cp.w_bf16 = dtb == MERIT_BF16;
+    cp.a_sc = 1;
+    cp.a_sy = K;
+    cp.o_sc = 1;
+    cp.o_sp = N;
+    cp.w_so = 1;
+    cp.w_si = N;
+    cp.gemm = 1;
+    return true;
+  };
+  swapped = false;
+  if (!try_one(d.view_a, fa, d.dtype_a, d.view_b, fb, d.dtype_b)) {
+    if (!try_one(d.view_b, fb, d.dtype_b, d.view_a, fa, d.dtype_a)) return false;
+    swapped = true;
+  }
+  return finish_conv(d, post, cp);
+}
+
+bool finish_conv(const merit_workload_desc& d, int32_t post, ConvParams& cp) {
   const bool both_bf16 = cp.in_bf16 && cp.w_bf16;
   cp.split = (both_bf16 || (d.flags & MERIT_FLAG_FAST_BF16)) ? 1 : 3;
   cp.post = post;
@@ -547,19 +609,24 @@ merit_status lower(const merit_workload_desc& d, merit_plan& plan) {
                   sp.argmin ? " +argmin" : "", sp.write_map ? "" : " (no map)");
   } else if (sk == SK_MAC) {
     bool swapped = false;
-    if (lower_conv(d, fa, fb, post, plan.conv, swapped)) {
+    if (lower_conv(d, fa, fb, post, plan.conv, swapped) || lower_gemm(d, fa, fb, post, plan.conv, swapped)) {
       plan.kernel = MERIT_KERNEL_CONV_TC;
       const auto& cp = plan.conv;
       info.algorithmic_ops = (double)info.n_outputs * avol;  // MACs
       const int64_t in_bytes = swapped ? info.src_b_bytes : info.src_a_bytes;
       const int64_t w_bytes = swapped ? info.src_a_bytes : info.src_b_bytes;
       info.algorithmic_bytes = (double)in_bytes + (double)w_bytes + (double)info.out_elems * 4;
-      std::snprintf(info.description, sizeof(info.description),
-                    "conv_tc N=%d Cin=%d %dx%d -> Cout=%d %dx%d k=%dx%d s=%d,%d d=%d,%d o=%d,%d "
-                    "%s split=%d BN=%d kb=%d%s",
-                    cp.N, cp.Cin, cp.H, cp.W, cp.Cout, cp.Ho, cp.Wo, cp.KH, cp.KW, cp.sy, cp.sx,
-                    cp.dy, cp.dx, cp.oy, cp.ox, cp.in_bf16 ? "bf16" : "f32", cp.split, cp.BN,
-                    cp.n_kb, cp.post == POST_RELU ? " relu" : "");
+      if (cp.gemm)
+        std::snprintf(info.description, sizeof(info.description),
+                      "conv_tc gemm M=%d N=%d K=%d %s split=%d BN=%d kb=%d%s", cp.H, cp.Cout, cp.Cin,
+                      cp.in_bf16 ? "bf16" : "f32", cp.split, cp.BN, cp.n_kb, cp.post == POST_RELU ? " relu" : "");
+      else
+        std::snprintf(info.description, sizeof(info.description),
+                      "conv_tc N=%d Cin=%d %dx%d -> Cout=%d %dx%d k=%dx%d s=%d,%d d=%d,%d o=%d,%d "
+                      "%s split=%d BN=%d kb=%d%s",
+                      cp.N, cp.Cin, cp.H, cp.W, cp.Cout, cp.Ho, cp.Wo, cp.KH, cp.KW, cp.sy, cp.sx,
+                      cp.dy, cp.dx, cp.oy, cp.ox, cp.in_bf16 ? "bf16" : "f32", cp.split, cp.BN,
+                      cp.n_kb, cp.post == POST_RELU ? " relu" : "");
       plan.conv_swapped = swapped;
     }
   }

@@ -107,6 +107,13 @@ struct ConvParams {
   int32_t n_kb = 0;         // k-blocks per tile = KH*KW*CB
   int64_t npix = 0;         // N*Ho*Wo
   int64_t packed_b_bytes = 0;
+  // Element strides of the operands (NCHW / OIHW / NCHW by default; a GEMM
+  // view maps onto the same kernel with A rows as pixels and K as channels,
+  // workloads.hpp:122-136).  Only the general kernel K3a reads them.
+  int64_t a_sn = 0, a_sc = 0, a_sy = 0, a_sx = 0;  // input: image, channel, row, column
+  int64_t o_sn = 0, o_sc = 0, o_sp = 0;            // output: image, channel, pixel (y*Wo + x)
+  int64_t w_so = 0, w_si = 0;                      // weights: output channel, input channel
+  int32_t gemm = 0;                                // not NCHW: general kernel only
 };
 
 }  // namespace merit_dev

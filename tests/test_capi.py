@@ -87,7 +87,8 @@ def test_templates_lower():
     kinds = {t: Plan(W.build_template(t, {})).kernel for t in W.TEMPLATES}
     assert kinds["maxpool"] == Kernel.MAXPOOL
     assert kinds["alexnet_conv1"] == Kernel.CONV_TC
-    for t in ("gemm", "correlation", "bilateral", "motion_estimation", "conv2d", "dilated"):
+    assert kinds["gemm"] == Kernel.CONV_TC  # through operand strides on the general kernel
+    for t in ("correlation", "bilateral", "motion_estimation", "conv2d", "dilated"):
         assert kinds[t] == Kernel.GENERIC
     assert Plan(W.build_template("conv2d", {"cin": 4, "cout": 8})).kernel == Kernel.CONV_TC
     assert Plan(W.build_template("relu_fused_conv", {"cin": 4, "cout": 8})).description.endswith("relu")
@@ -170,3 +171,15 @@ def test_device_entry_points_fail_loudly_without_a_gpu():
     with pytest.raises(Error) as e:
         Plan(w).run_host(w.src_a, w.src_b)
     assert e.value.code == ErrorCode.Cuda
+
+
+def test_gemm_lowers_to_tensor_core_kernel_real32_only():
+    from paper_1911_03458_b200 import Kernel, Plan
+    from paper_1911_03458_b200 import workloads as W
+    w = W.build_template("gemm", {"m": 33, "n": 40, "k": 70})
+    W.fill_random(w, 1, 2)
+    p = Plan(w)
+    assert p.kernel == Kernel.CONV_TC and "gemm M=33 N=40 K=70" in p.description
+    wf = W.build_template("gemm", {"m": 5, "n": 6, "k": 7, "fix": 1, "frac": 6})
+    W.fill_random(wf, 1, 2)
+    assert Plan(wf).kernel == Kernel.GENERIC  # FIX16: exact interpreter

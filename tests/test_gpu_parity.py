@@ -397,3 +397,17 @@ def test_conv_random_shapes_all_dispatch_paths(cuda):
                        cwd=str(__import__("pathlib").Path(__file__).resolve().parents[1]))
     assert r.returncode == 0, r.stderr[-2000:]
     assert r.stdout.strip().endswith("bad 0"), r.stdout[-2000:]
+
+
+@pytest.mark.parametrize("m,n,k", [(9, 7, 11), (300, 70, 129), (128, 300, 64), (1, 1, 1), (517, 256, 200)])
+def test_gemm_template_on_tensor_cores(cuda, m, n, k):
+    # workloads.hpp:122-136 lowered onto the general tcgen05 kernel through
+    # operand strides; fp32 data: 3-term split, tol 1e-4
+    w = W.build_template("gemm", {"m": m, "n": n, "k": k})
+    W.fill_random(w, 2 * m + 1, 2 * n + 2)
+    plan = Plan(w)
+    assert plan.kernel == Kernel.CONV_TC and "gemm" in plan.description
+    got = run_full(w)
+    want = (np.asarray(w.src_a, np.float64) @ np.asarray(w.src_b, np.float64)).astype(np.float32)
+    assert got.shape == (m, n)
+    assert rel_err(got, want) <= TOL_F32
