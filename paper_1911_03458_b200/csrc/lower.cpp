@@ -630,11 +630,11 @@ merit_status lower(const merit_workload_desc& d, merit_plan& plan) {
       plan.conv_swapped = swapped;
     }
   }
+  if (plan.kernel != MERIT_KERNEL_SAD && (d.flags & (MERIT_FLAG_ARGMIN | MERIT_FLAG_NO_MAP)))
+    return fail(MERIT_E_UNSUPPORTED_PROGRAM,
+                "argmin is only available for L1 block-matching workloads on the SAD kernel");
   if (plan.kernel == MERIT_KERNEL_GENERIC) {
     // Exact interpreter.  Any storage dtype widens to the mode's value type.
-    if (d.flags & (MERIT_FLAG_ARGMIN | MERIT_FLAG_NO_MAP))
-      return fail(MERIT_E_UNSUPPORTED_PROGRAM,
-                  "argmin is only available for L1 block-matching workloads on the SAD kernel");
     if (!fix16 && d.dtype_out != MERIT_F32)
       return fail(MERIT_E_UNSUPPORTED_PROGRAM, "REAL32 generic execution writes f32 outputs");
     GenericParams& g = plan.gen;
