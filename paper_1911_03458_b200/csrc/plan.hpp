@@ -135,6 +135,12 @@ struct merit_plan {
   mutable void* d_packed_b = nullptr;  // K3 packed weights
   mutable bool packed_valid = false;
   mutable int device = -1;
+  // Device staging of merit_dev_run_host (a, b, out, aux), kept across calls
+  // on the device they were made on; host_mu serialises host-buffer calls.
+  mutable std::mutex host_mu;
+  mutable void* stage[4] = {nullptr, nullptr, nullptr, nullptr};
+  mutable size_t stage_bytes[4] = {0, 0, 0, 0};
+  mutable int stage_dev = -1;
 };
 
 namespace merit_dev {
