@@ -39,7 +39,7 @@ constexpr int kThreads = 15 * 32;
 constexpr int kMaxRing = 8;
 constexpr uint32_t kPlane = kAPlane;           // 16 KB
 constexpr uint32_t kASlot = 2 * kPlane;        // [tap2][tap1]
-constexpr int kEpiCo = 32;                     // output channels per TMA store
+constexpr int kEpiCo = 16;                     // output channels per TMA store
 
 struct TmaArgs {
   ConvParams p;
