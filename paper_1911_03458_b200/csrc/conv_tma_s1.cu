@@ -53,6 +53,8 @@ struct S1Args {
   int rows;            // output rows per tile = 128 / slots
   int tiles_per_img;   // ceil(Ho / rows)
   int n_tiles;
+  int n_full;          // units below n_full are whole tiles; the last (n_tiles - n_full)
+  int n_units;         // tiles run as two half-N units each (the final, partial wave)
   int n_groups;        // KH * CB
   uint32_t raw_bytes;  // W * rows * 32 ch * 4 (half a 64-channel k-block)
   uint32_t a_slot;     // nsplit planes x 16 KB
@@ -140,6 +142,17 @@ conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
   pdl_wait();  // prologue done: from here on global memory is touched
   const int BN = p.BN;
   const int W = p.W;
+  // scheduling unit -> (tile, half): half = -1 for a whole tile, 0 / 1 for the
+  // lower / upper half of the output channels of a tail tile
+  auto unit_of = [&](int u, int& tile, int& half) {
+    if (u < A.n_full) {
+      tile = u;
+      half = -1;
+    } else {
+      tile = A.n_full + ((u - A.n_full) >> 1);
+      half = (u - A.n_full) & 1;
+    }
+  };
   const int slots_mask = (1 << A.slots_log2) - 1;
   const bool pon = (A.debug & 64) && lane == 0 && warp < 16;
   unsigned long long w1 = 0, w2 = 0, w3 = 0;
@@ -151,7 +164,9 @@ conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&in_map)) : "memory");
       int st = 0;
       uint32_t ph = 0;
-      for (int tile = blockIdx.x; tile < A.n_tiles; tile += gridDim.x) {
+      for (int u = blockIdx.x; u < A.n_units; u += gridDim.x) {
+        int tile, half;
+        unit_of(u, tile, half);
         const int n = tile / A.tiles_per_img;
         const int y0 = (tile - n * A.tiles_per_img) * A.rows;
         for (int g = 0; g < A.n_groups; ++g) {
@@ -180,7 +195,9 @@ conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
     const uint32_t cbase = static_cast<uint32_t>(8 * (w & 3)) * A.rows * rowf * 4u;
     int rs = w >> 2, as = 0;
     uint32_t rph = 0, aph = 0;
-    for (int tile = blockIdx.x; tile < A.n_tiles; tile += gridDim.x) {
+    for (int u = blockIdx.x; u < A.n_units; u += gridDim.x) {
+        int tile, half;
+        unit_of(u, tile, half);
       for (int g = 0; g < A.n_groups; ++g) {
         twait_s1(r_full(rs), rph, w1, pon);
         float v[4][8];
@@ -229,14 +246,19 @@ conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
       constexpr int nsp = SPLIT3 ? 2 : 1;
       int st = 0;
       uint32_t ph = 0;
-      for (int tile = blockIdx.x; tile < A.n_tiles; tile += gridDim.x) {
+      for (int u = blockIdx.x; u < A.n_units; u += gridDim.x) {
+        int tile, half;
+        unit_of(u, tile, half);
         for (int g = 0; g < A.n_groups; ++g) {
           twait_s1(b_empty(st), ph ^ 1, w1, pon);
-          mbar_expect_tx(b_full(st), A.b_slot);
+          // a half unit stacks the taps' rows of its 32-channel half: N = 3 BN / 2
+          const uint32_t rows = half < 0 ? A.b_plane : A.b_plane / 2;
+          const uint32_t src_off = half < 0 ? 0u : static_cast<uint32_t>(half) * (A.b_plane / 2);
+          mbar_expect_tx(b_full(st), 3u * nsp * rows);
           for (int kx = 0; kx < 3; ++kx)
             for (int sp = 0; sp < nsp; ++sp)
-              bulk_g2s(bring + st * A.b_slot + (sp * 3 + kx) * A.b_plane,
-                       A.wpk + ((long long)(g * 3 + kx) * nsp + sp) * A.b_plane, A.b_plane, b_full(st));
+              bulk_g2s(bring + st * A.b_slot + (sp * 3 + kx) * rows,
+                       A.wpk + ((long long)(g * 3 + kx) * nsp + sp) * A.b_plane + src_off, rows, b_full(st));
           if (++st == A.nb) { st = 0; ph ^= 1; }
         }
       }
@@ -245,11 +267,15 @@ conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
   } else if (warp == kWarpMma) {
     // ============ MMA issuer ===================================================
     if (lane == 0) {
-      const uint32_t idesc = make_idesc(3 * BN);
-      const uint32_t b_lo = 3 * A.b_plane;
+      const uint32_t idesc_full = make_idesc(3 * BN);
+      const uint32_t idesc_half = make_idesc(3 * (BN / 2));
       int as = 0, bs = 0, acc = 0;
       uint32_t aph = 0, bph = 0, acc_phase = 0;
-      for (int tile = blockIdx.x; tile < A.n_tiles; tile += gridDim.x) {
+      for (int u = blockIdx.x; u < A.n_units; u += gridDim.x) {
+        int tile, half;
+        unit_of(u, tile, half);
+        const uint32_t idesc = half < 0 ? idesc_full : idesc_half;
+        const uint32_t b_lo = 3 * (half < 0 ? A.b_plane : A.b_plane / 2);
         twait_s1(tempty(acc), acc_phase ^ 1, w3, pon);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * kAccCols;
@@ -293,16 +319,21 @@ conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
     const bool first = lane == 0, last = lane == 31;
     const bool has_prev = q > 0, has_next = q < 3;
     const uint32_t xset = xring + static_cast<uint32_t>(set) * (2 * 4 * 16 * 4);
-    const int n_chunks = BN / kEC;
-    const int my_last = ((n_chunks - 1 - set) / 2) * 2 + set;  // this set's last chunk
     int acc = 0;
     uint32_t acc_phase = 0;
     int par = 0;
-    for (int tile = blockIdx.x; tile < A.n_tiles; tile += gridDim.x) {
+    for (int u = blockIdx.x; u < A.n_units; u += gridDim.x) {
+        int tile, half;
+        unit_of(u, tile, half);
       const int n = tile / A.tiles_per_img;
       const int y = (tile - n * A.tiles_per_img) * A.rows + r;
       const bool store = x >= 0 && x < W && y < p.Ho && !(A.debug & 128);
-      float* dst = A.out + ((long long)n * p.Cout * p.Ho + y) * W + x;
+      // a half unit holds 32 channels: P_kx at columns kx * bn
+      const int bn = half < 0 ? BN : BN / 2;
+      const int co_off = half < 0 ? 0 : half * bn;
+      const int n_chunks = bn / kEC;
+      const int my_last = ((n_chunks - 1 - set) / 2) * 2 + set;  // this set's last chunk
+      float* dst = A.out + ((long long)n * p.Cout * p.Ho + y) * W + x + (long long)co_off * p.Ho * W;
       const long long co_stride = (long long)p.Ho * W;
       twait_s1(tfull(acc), acc_phase, w1, pon);
       tc_fence_after();
@@ -317,8 +348,8 @@ conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
         const int c0 = ch * kEC;
         uint32_t p0[kEC], p1[kEC], p2[kEC];
         TMEM_LD8(t_row + c0, p0);
-        TMEM_LD8(t_row + BN + c0, p1);
-        TMEM_LD8(t_row + 2 * BN + c0, p2);
+        TMEM_LD8(t_row + bn + c0, p1);
+        TMEM_LD8(t_row + 2 * bn + c0, p2);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (ch == my_last) {  // accumulator drained by this warp
           tc_fence_before();
@@ -350,7 +381,7 @@ conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
                        : "=r"(xn[e]), "=r"(xn[e + 1]), "=r"(xn[e + 2]), "=r"(xn[e + 3])
                        : "r"(xna + 4u * e));
         }
-        const int cmax = p.Cout - c0;  // channels of this chunk that exist
+        const int cmax = p.Cout - co_off - c0;  // channels of this chunk that exist
         float* ptr = dst + (long long)c0 * co_stride;
 #pragma unroll
         for (int e = 0; e < kEC; ++e) {
@@ -458,6 +489,16 @@ merit_status launch_conv_s1(const merit_plan& plan, const void* a, const void* p
   if (e != cudaSuccess) return cuda_check(e, "set_smem_attr(conv_s1)");
   int grid = num_sms();
   if (grid > A.n_tiles) grid = A.n_tiles;
+  // Tail split: the final partial wave of r = n_tiles % grid tiles runs as 2r
+  // half-N units, so it costs half a tile instead of a whole one (C3: 896
+  // tiles on 148 SMs).  Needs N / 2 = 3 BN / 2 to stay a multiple of 16.
+  {
+    const int r = A.n_tiles % grid;
+    const char* se = getenv("MERIT_S1_SPLIT");
+    const bool split = !(se && se[0] == '0') && r > 0 && 2 * r <= grid && p.BN % 32 == 0;
+    A.n_full = split ? A.n_tiles - r : A.n_tiles;
+    A.n_units = A.n_full + 2 * (A.n_tiles - A.n_full);
+  }
   {
     const char* dbg = getenv("MERIT_CONV_DEBUG");
     A.debug = dbg ? atoi(dbg) : 0;
