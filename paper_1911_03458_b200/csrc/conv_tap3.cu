@@ -9,8 +9,9 @@
 // every output row (and one after it for stride 1), these identities hold at
 // row boundaries too (the padding slot reads only padding).  So the A-operand
 // tile of the shifted tap is the SAME shared-memory tile, read one row earlier
-// or later: the UMMA descriptor's start address moves by +-128 B and its
-// base_offset field carries the swizzle phase.  The producers write two
+// or later: the UMMA descriptor's start address moves by +-128 B (the
+// hardware applies the 128-B swizzle from physical address bits, so the
+// descriptor's base_offset field stays 0 — measured).  The producers write two
 // tiles per (ky, channel-block) group for stride 2 and ONE for stride 1,
 // instead of three, with no shuffles: the view's kx term is executed by the
 // tensor core's operand addressing.
@@ -59,16 +60,9 @@ struct Tap3Args {
   uint32_t b_bytes; // per k-block
   int na, nb;
   uint32_t tmem_cols;
-  int base_offset_mode;  // 1: set descriptor base_offset = (addr >> 7) & 7 (verified wrong: keep 0)
   unsigned long long* prof;  // MERIT_CONV_DEBUG & 64: per-role cycle counters
   int debug;
 };
-
-__device__ __forceinline__ uint64_t sw128_desc_off(uint32_t saddr, int mode) {
-  uint64_t d = sw128_desc(saddr);
-  if (mode) d |= static_cast<uint64_t>((saddr >> 7) & 7u) << 49;
-  return d;
-}
 
 __device__ __forceinline__ void st_shared_u16(uint32_t addr, uint32_t v) {
   asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"(static_cast<unsigned short>(v)) : "memory");
@@ -348,7 +342,6 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tap3_kernel(Tap3Args A) {
     // ============ MMA issuer ===================================================
     if (lane == 0) {
       const uint32_t idesc = make_idesc(BN);
-      const int bom = A.base_offset_mode;
       const bool mprof = (A.debug & 64) != 0;
       unsigned long long m_a = 0, m_b = 0, m_t = 0;
       const unsigned long long m_start = clock64();
@@ -374,10 +367,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tap3_kernel(Tap3Args A) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const uint32_t accum = (g > 0 || kx > 0 || k > 0) ? 1u : 0u;
-              tc_mma(d_tmem, sw128_desc_off(a_hi + 32 * k, bom), sw128_desc(b_hi + 32 * k), idesc, accum);
+              tc_mma(d_tmem, sw128_desc(a_hi + 32 * k), sw128_desc(b_hi + 32 * k), idesc, accum);
               if (SPLIT3) {
-                tc_mma(d_tmem, sw128_desc_off(a_hi + 32 * k, bom), sw128_desc(b_lo + 32 * k), idesc, 1u);
-                tc_mma(d_tmem, sw128_desc_off(a_lo + 32 * k, bom), sw128_desc(b_hi + 32 * k), idesc, 1u);
+                tc_mma(d_tmem, sw128_desc(a_hi + 32 * k), sw128_desc(b_lo + 32 * k), idesc, 1u);
+                tc_mma(d_tmem, sw128_desc(a_lo + 32 * k), sw128_desc(b_hi + 32 * k), idesc, 1u);
               }
             }
             tc_commit(b_empty(bs));
@@ -490,8 +483,6 @@ merit_status launch_conv_tap3(const merit_plan& plan, const void* a, const void*
   uint32_t cols = 32;
   while (cols < static_cast<uint32_t>(2 * p.BN)) cols <<= 1;
   A.tmem_cols = cols;
-  const char* bo = getenv("MERIT_TAP3_BASE_OFFSET");
-  A.base_offset_mode = bo ? atoi(bo) : 0;  // hardware swizzles by address bits: field stays 0
   // ring depths: 3 A slots (one group each) if possible, B fills the rest
   const size_t fixed = 1024 + 8 * (4 * kMaxRing + 4) + 16;
   const size_t budget = 227 * 1024 - fixed;
