@@ -364,11 +364,33 @@ class Plan:
             return C.c_void_p(x)
         return C.c_void_p(x.data_ptr())
 
+    packed = False  # weights pre-packed on the device (src_b may then be omitted)
+
     def pack_b(self, d_src_b, stream=None):
+        self._check_buf(d_src_b, self.info.src_b_bytes, "src_b")
         _check(self.lib.merit_dev_plan_pack_b(self.handle, self._ptr(d_src_b),
                                               C.c_void_p(stream or 0)))
+        self.packed = True
+
+    def _check_buf(self, x, need: int, what: str):
+        """Device buffers given as tensors must be CUDA tensors of at least
+        `need` bytes (raw integer pointers are the caller's responsibility)."""
+        if x is None or isinstance(x, int) or need <= 0:
+            return
+        if not getattr(x, "is_cuda", False):
+            raise Error(ErrorCode.BadParams, f"{what} must be a CUDA tensor (device buffers)")
+        if not x.is_contiguous():
+            raise Error(ErrorCode.BadParams, f"{what} must be contiguous")
+        if x.numel() * x.element_size() < need:
+            raise Error(ErrorCode.BadParams, f"{what} holds {x.numel() * x.element_size()} bytes, needs {need}")
 
     def run(self, d_src_a, d_src_b, d_out, d_aux=None, stream=None):
+        """merit_dev_run on device buffers (torch CUDA tensors or raw pointers)."""
+        i = self.info
+        self._check_buf(d_src_a, i.src_a_bytes, "src_a")
+        self._check_buf(d_src_b, i.src_b_bytes if not self.packed else 0, "src_b")
+        self._check_buf(d_out, i.out_bytes, "out")
+        self._check_buf(d_aux, i.aux_elems * 4, "aux")
         _check(self.lib.merit_dev_run(self.handle, self._ptr(d_src_a), self._ptr(d_src_b),
                                       self._ptr(d_out), self._ptr(d_aux), C.c_void_p(stream or 0)))
 

@@ -411,3 +411,16 @@ def test_gemm_template_on_tensor_cores(cuda, m, n, k):
     want = (np.asarray(w.src_a, np.float64) @ np.asarray(w.src_b, np.float64)).astype(np.float32)
     assert got.shape == (m, n)
     assert rel_err(got, want) <= TOL_F32
+
+
+def test_device_buffer_checks(cuda):
+    import torch
+    w = W.maxpool_nchw_view(1, 2, 8, 8)
+    plan = Plan(w)
+    a = torch.zeros(2 * 8 * 8, device="cuda")
+    out = torch.zeros(2 * 4 * 4, device="cuda")
+    plan.run(a, None, out)
+    with pytest.raises(Error):
+        plan.run(a[:10], None, out)                      # too small
+    with pytest.raises(Error):
+        plan.run(a.cpu(), None, out)                     # host tensor
