@@ -75,7 +75,22 @@ struct SadLaunch {
   int BYT;        // tile rows = ceil(BY / nby)
   int cur_pitch;  // bytes per staged current-frame row: TBX*BW rounded up to 16
   uint32_t raw_buf, cur_buf;  // bytes per raw / current buffer (128-byte multiples)
+  uint32_t ntx_m, ntx_s;      // n / n_tiles_x as a multiply-high (fast_div)
+  uint32_t byt_m, byt_s;      // n / BYT
+  int cp_sr, cp_sw;           // copy builder: blockDim.x = cp_sr * Ww + cp_sw
 };
+
+// n / d for n < 2^31 by multiply-high (Granlund-Montgomery): s = ceil(log2 d),
+// m = floor(2^32 (2^s - d) / d) + 1.  Replaces the ~25-instruction signed
+// division the compiler emits per tile.
+inline void fast_div_init(uint32_t d, uint32_t& m, uint32_t& s) {
+  s = 0;
+  while ((1ull << s) < d) ++s;
+  m = static_cast<uint32_t>(((1ull << 32) * ((1ull << s) - d)) / d + 1);
+}
+__device__ __forceinline__ uint32_t fast_div(uint32_t n, uint32_t m, uint32_t s) {
+  return (__umulhi(n, m) + n) >> s;
+}
 
 template <int BLK>
 __device__ __forceinline__ void stage_tile(const SadLaunch& L, const uint8_t* __restrict__ cur,
@@ -83,10 +98,10 @@ __device__ __forceinline__ void stage_tile(const SadLaunch& L, const uint8_t* __
                                            uint32_t raw_s, uint8_t* raw, uint32_t cur_s,
                                            uint8_t* curs) {
   const SadParams& p = L.p;
-  const int tx = tile % L.n_tiles_x;
-  const int t2 = tile / L.n_tiles_x;
-  const int by = t2 % L.BYT;  // nby == 1 on this path
-  const long long pair = t2 / L.BYT;
+  const int t2 = static_cast<int>(fast_div(tile, L.ntx_m, L.ntx_s));
+  const int tx = tile - t2 * L.n_tiles_x;
+  const long long pair = fast_div(t2, L.byt_m, L.byt_s);
+  const int by = t2 - static_cast<int>(pair) * L.BYT;  // nby == 1 on this path
   const int bx0 = tx * L.TBX;
   const int nb = min(L.TBX, p.BX - bx0);
   const uint8_t* refp = ref + pair * (long long)p.Hr * p.Wr;
@@ -194,10 +209,10 @@ __device__ __forceinline__ void issue_tile(const SadLaunch& L, const uint8_t* __
   if (L.tma) {
     if (threadIdx.x == 0) {
       const SadParams& p = L.p;
-      const int tx = tile % L.n_tiles_x;
-      const int t2 = tile / L.n_tiles_x;
-      const int by = (t2 % L.BYT) * L.nby;
-      const int pair = t2 / L.BYT;
+      const int t2 = static_cast<int>(fast_div(tile, L.ntx_m, L.ntx_s));
+      const int tx = tile - t2 * L.n_tiles_x;
+      const int pair = static_cast<int>(fast_div(t2, L.byt_m, L.byt_s));
+      const int by = (t2 - pair * L.BYT) * L.nby;
       const int bx0 = tx * L.TBX;
       const uint32_t bytes = L.R_box * L.rw * 4 + L.nby * BLK * L.cur_pitch;
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
@@ -210,13 +225,17 @@ __device__ __forceinline__ void issue_tile(const SadLaunch& L, const uint8_t* __
   }
 }
 
-template <int BLK, int D, int NBY, int NT>
+// WXC: the displacement-window width as a compile-time constant (0 = runtime
+// p.WX).  A constant width turns the per-displacement key and SAD-map store
+// offsets into immediates (the epilogue was ~8% of the issued instructions).
+template <int BLK, int D, int NBY, int NT, int WXC>
 __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1)
 sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, void* __restrict__ out,
            int32_t* __restrict__ aux, SadLaunch L, const __grid_constant__ CUtensorMap ref_map,
            const __grid_constant__ CUtensorMap cur_map) {
   extern __shared__ __align__(128) uint8_t smem_b[];
   const SadParams& p = L.p;
+  const int WX = WXC ? WXC : p.WX;
   constexpr int BWW = BLK / 4;  // words per block row
   const int raw_words = static_cast<int>(L.raw_buf / 4);
   const int cur_words = static_cast<int>(L.cur_buf / 4);
@@ -227,14 +246,16 @@ sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, voi
   uint32_t* keys = copies + 4 * L.CS;       // per block: running argmin key
   uint32_t* cnt = keys + NBY * L.TBX;       // per block: contributions so far
   const uint32_t bar0 = (smem_u32(cnt + NBY * L.TBX) + 7u) & ~7u;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   const int cpw = L.cur_pitch / 4;  // words per staged current row
 
   // per-thread item: (block, dx); the thread walks all dy groups
   const int item = threadIdx.x;
-  const int ib = item / p.WX;
-  const int idx = item - ib * p.WX;
+  const int ib = item / WX;
+  const int idx = item - ib * WX;
   const bool has_item = item < L.items;
+  // copy-builder start (row, word) of this thread in the flattened R x Ww walk
+  const int cp_r0 = static_cast<int>(threadIdx.x) / L.Ww;
+  const int cp_w0 = static_cast<int>(threadIdx.x) - cp_r0 * L.Ww;
 
   if (threadIdx.x < NBY * L.TBX) {
     keys[threadIdx.x] = 0xffffffffu;
@@ -265,47 +286,53 @@ sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, voi
     }
     __syncthreads();  // raw[buf] landed; previous tile's compute finished
     // tile coordinates
-    const int tx = tile % L.n_tiles_x;
-    const int t2 = tile / L.n_tiles_x;
-    const int by = (t2 % L.BYT) * NBY;  // first block row of the tile
-    const long long pair = t2 / L.BYT;
+    const int t2 = static_cast<int>(fast_div(tile, L.ntx_m, L.ntx_s));
+    const int tx = tile - t2 * L.n_tiles_x;
+    const int pair_i = static_cast<int>(fast_div(t2, L.byt_m, L.byt_s));
+    const int by = (t2 - pair_i * L.BYT) * NBY;  // first block row of the tile
+    const long long pair = pair_i;
     const int bx0 = tx * L.TBX;
     const int nb = min(L.TBX, p.BX - bx0);
     // leading bytes of the staged rows before the window (TMA boxes start at
     // a 16-byte multiple)
     const int dref = L.tma ? (bx0 * BLK + p.ox) - floor16(bx0 * BLK + p.ox) : 0;
     const int dcur = L.tma ? (bx0 * BLK + p.cx) - floor16(bx0 * BLK + p.cx) : 0;
-    // four byte-shifted word copies: copy_s[r][w] = window bytes (4w+s .. 4w+s+3)
+    // four byte-shifted word copies: copy_s[r][w] = window bytes (4w+s .. 4w+s+3),
+    // one (row, word) per thread per step over the flattened R x Ww range
     {
-      // 32-bit shared addresses, bumped per row (no generic-pointer math)
       const uint32_t cs4 = static_cast<uint32_t>(L.CS) * 4u;
-      const uint32_t rstep = static_cast<uint32_t>(nwarps * L.rw) * 4u;
-      const uint32_t cstep = static_cast<uint32_t>(nwarps * L.Ww) * 4u;
-      uint32_t ra = smem_u32(raw) + static_cast<uint32_t>(warp * L.rw + lane + (dref >> 2)) * 4u;
-      uint32_t ca = smem_u32(copies) + static_cast<uint32_t>(warp * L.Ww + lane) * 4u;
+      const uint32_t raw_s = smem_u32(raw) + static_cast<uint32_t>(dref >> 2) * 4u;
+      const uint32_t cop_s = smem_u32(copies);
       const int dr = dref & 3;
-      for (int r = warp; r < L.R; r += nwarps, ra += rstep, ca += cstep) {
-        for (int w = lane, k = 0; w < L.Ww; w += 32, k += 128) {
-          uint32_t a0, a1, a2;
-          asm volatile("ld.shared.u32 %0, [%1];" : "=r"(a0) : "r"(ra + k));
-          asm volatile("ld.shared.u32 %0, [%1];" : "=r"(a1) : "r"(ra + k + 4));
-          uint32_t c0, c1, c2, c3;
-          if (dr == 0) {
-            c0 = a0;
-            c1 = __byte_perm(a0, a1, 0x4321);
-            c2 = __byte_perm(a0, a1, 0x5432);
-            c3 = __byte_perm(a0, a1, 0x6543);
-          } else {
-            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(a2) : "r"(ra + k + 8));
-            c0 = __funnelshift_r(a0, a1, 8 * dr);
-            c1 = dr + 1 < 4 ? __funnelshift_r(a0, a1, 8 * (dr + 1)) : a1;
-            c2 = dr + 2 < 4 ? __funnelshift_r(a0, a1, 8 * (dr + 2)) : __funnelshift_r(a1, a2, 8 * (dr - 2));
-            c3 = __funnelshift_r(a1, a2, 8 * (dr - 1));
-          }
-          asm volatile("st.shared.u32 [%0], %1;" ::"r"(ca + k), "r"(c0) : "memory");
-          asm volatile("st.shared.u32 [%0], %1;" ::"r"(ca + cs4 + k), "r"(c1) : "memory");
-          asm volatile("st.shared.u32 [%0], %1;" ::"r"(ca + 2 * cs4 + k), "r"(c2) : "memory");
-          asm volatile("st.shared.u32 [%0], %1;" ::"r"(ca + 3 * cs4 + k), "r"(c3) : "memory");
+      int r = cp_r0, w = cp_w0;
+      while (r < L.R) {
+        const uint32_t ra = raw_s + static_cast<uint32_t>(r * L.rw + w) * 4u;
+        const uint32_t ca = cop_s + static_cast<uint32_t>(r * L.Ww + w) * 4u;
+        uint32_t a0, a1, a2;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(a0) : "r"(ra));
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(a1) : "r"(ra + 4));
+        uint32_t c0, c1, c2, c3;
+        if (dr == 0) {
+          c0 = a0;
+          c1 = __byte_perm(a0, a1, 0x4321);
+          c2 = __byte_perm(a0, a1, 0x5432);
+          c3 = __byte_perm(a0, a1, 0x6543);
+        } else {
+          asm volatile("ld.shared.u32 %0, [%1];" : "=r"(a2) : "r"(ra + 8));
+          c0 = __funnelshift_r(a0, a1, 8 * dr);
+          c1 = dr + 1 < 4 ? __funnelshift_r(a0, a1, 8 * (dr + 1)) : a1;
+          c2 = dr + 2 < 4 ? __funnelshift_r(a0, a1, 8 * (dr + 2)) : __funnelshift_r(a1, a2, 8 * (dr - 2));
+          c3 = __funnelshift_r(a1, a2, 8 * (dr - 1));
+        }
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(ca), "r"(c0) : "memory");
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(ca + cs4), "r"(c1) : "memory");
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(ca + 2 * cs4), "r"(c2) : "memory");
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(ca + 3 * cs4), "r"(c3) : "memory");
+        w += L.cp_sw;
+        r += L.cp_sr;
+        if (w >= L.Ww) {
+          w -= L.Ww;
+          ++r;
         }
       }
     }
@@ -322,20 +349,22 @@ sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, voi
       // block ib at byte dcur + ib*BLK (dcur % 4 == 0), block row n at row n*BLK
       uint32_t cw[NBY][BLK][BWW];
       const uint32_t* cb = curw + (dcur >> 2) + ib * BWW;
-      const bool vec = BWW == 4 && ((dcur & 15) == 0);
+      if (BWW == 4 && ((dcur & 15) == 0)) {
 #pragma unroll
-      for (int n = 0; n < NBY; ++n)
+        for (int n = 0; n < NBY; ++n)
 #pragma unroll
-        for (int i = 0; i < BLK; ++i) {
-          const uint32_t* src = cb + (n * BLK + i) * cpw;
-          if (vec) {
-            const uint4 q4 = *reinterpret_cast<const uint4*>(src);
+          for (int i = 0; i < BLK; ++i) {
+            const uint4 q4 = *reinterpret_cast<const uint4*>(cb + (n * BLK + i) * cpw);
             cw[n][i][0] = q4.x; cw[n][i][1 % BWW] = q4.y; cw[n][i][2 % BWW] = q4.z; cw[n][i][3 % BWW] = q4.w;
-          } else {
-#pragma unroll
-            for (int j = 0; j < BWW; ++j) cw[n][i][j] = src[j];
           }
-        }
+      } else {
+#pragma unroll
+        for (int n = 0; n < NBY; ++n)
+#pragma unroll
+          for (int i = 0; i < BLK; ++i)
+#pragma unroll
+            for (int j = 0; j < BWW; ++j) cw[n][i][j] = cb[(n * BLK + i) * cpw + j];
+      }
       const int col = ib * BLK + idx;  // byte column in the staged window
       const uint32_t* cp0 = copies + (col & 3) * L.CS + (col >> 2);
       const long long blk_index = (pair * p.BY + by) * (long long)p.BX + bx0 + ib;
@@ -370,29 +399,47 @@ sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, voi
         }
         const int dy0 = ig * D;
         const int nd = min(D, p.WY - dy0);
-        uint32_t key = (static_cast<uint32_t>(dy0) * p.WX + idx);
-        const uint32_t kstep = static_cast<uint32_t>(p.WX);
+        // argmin key = sad << 16 | (dy * WX + dx): the per-thread part
+        // dy0 * WX + idx is added after the min (it does not change the order)
+        const uint32_t key0 = static_cast<uint32_t>(dy0 * WX + idx);
 #pragma unroll
         for (int n = 0; n < NBY; ++n) {
+          uint32_t bn = 0xffffffffu;
+          const bool store = p.write_map && by + n < p.BY;
+          const long long obase = ((blk_index + n * (long long)p.BX) * p.WY + dy0) * WX + idx;
+          if (nd == D) {  // full group: no per-displacement predicates
 #pragma unroll
-          for (int d = 0; d < D; ++d) {
-            const uint32_t k = (acc[n][d] << 16) | (key + d * kstep);
-            if (d < nd) best[n] = k < best[n] ? k : best[n];
-          }
-          if (p.write_map && by + n < p.BY) {
-            const long long obase = ((blk_index + n * (long long)p.BX) * p.WY + dy0) * p.WX + idx;
-            if (p.out_f32) {
-              float* o = static_cast<float*>(out) + obase;
+            for (int d = 0; d < D; ++d) bn = min(bn, (acc[n][d] << 16) + static_cast<uint32_t>(d * WX));
+            if (store) {
+              if (p.out_f32) {
+                float* o = static_cast<float*>(out) + obase;
 #pragma unroll
-              for (int d = 0; d < D; ++d, o += p.WX)
-                if (d < nd) __stcs(o, static_cast<float>(acc[n][d]));
-            } else {
-              int32_t* o = static_cast<int32_t*>(out) + obase;
+                for (int d = 0; d < D; ++d) __stcs(o + d * WX, static_cast<float>(acc[n][d]));
+              } else {
+                int32_t* o = static_cast<int32_t*>(out) + obase;
 #pragma unroll
-              for (int d = 0; d < D; ++d, o += p.WX)
-                if (d < nd) __stcs(o, static_cast<int32_t>(acc[n][d]));
+                for (int d = 0; d < D; ++d) __stcs(o + d * WX, static_cast<int32_t>(acc[n][d]));
+              }
+            }
+          } else {
+#pragma unroll
+            for (int d = 0; d < D; ++d)
+              if (d < nd) bn = min(bn, (acc[n][d] << 16) + static_cast<uint32_t>(d * WX));
+            if (store) {
+              if (p.out_f32) {
+                float* o = static_cast<float*>(out) + obase;
+#pragma unroll
+                for (int d = 0; d < D; ++d)
+                  if (d < nd) __stcs(o + d * WX, static_cast<float>(acc[n][d]));
+              } else {
+                int32_t* o = static_cast<int32_t*>(out) + obase;
+#pragma unroll
+                for (int d = 0; d < D; ++d)
+                  if (d < nd) __stcs(o + d * WX, static_cast<int32_t>(acc[n][d]));
+              }
             }
           }
+          best[n] = min(best[n], bn + key0);
         }
       }
       if (p.argmin) {
@@ -406,12 +453,12 @@ sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, voi
           const int slot = n * L.TBX + ib;
           atomicMin(&keys[slot], best[n]);
           __threadfence_block();
-          if (atomicAdd(&cnt[slot], 1u) == static_cast<uint32_t>(p.WX - 1)) {
+          if (atomicAdd(&cnt[slot], 1u) == static_cast<uint32_t>(WX - 1)) {
             __threadfence_block();
             const uint32_t key = atomicExch(&keys[slot], 0xffffffffu);
             cnt[slot] = 0u;
             const int k = static_cast<int>(key & 0xffffu);
-            const int dy = k / p.WX, dx = k - (k / p.WX) * p.WX;
+            const int dy = k / WX, dx = k - (k / WX) * WX;
             int32_t* a = aux + (blk_index + n * (long long)p.BX) * 3;
             a[0] = dy + p.oy - p.cy;
             a[1] = dx + p.ox - p.cx;
@@ -530,14 +577,33 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
   if (L.n_tiles == 0) return MERIT_OK;
   if (smem > (nt == 512 ? 220 : 110) * 1024)
     return fail(MERIT_E_UNSUPPORTED_VIEW, "SAD footprint exceeds shared memory");
-  auto kern = nt == 512 ? sad_kernel<BLK, D, 1, 512> : sad_kernel<BLK, D, 1, 256>;
+  auto kern = nt == 512 ? sad_kernel<BLK, D, 1, 512, 0> : sad_kernel<BLK, D, 1, 256, 0>;
   if constexpr (BLK == 8) {
-    if (L.nby == 2) kern = nt == 512 ? sad_kernel<BLK, D, 2, 512> : sad_kernel<BLK, D, 2, 256>;
+    if (L.nby == 2) kern = nt == 512 ? sad_kernel<BLK, D, 2, 512, 0> : sad_kernel<BLK, D, 2, 256, 0>;
+  }
+  // compile-time window widths for the +/-16 and +/-32 searches (C2, C5)
+  if constexpr (D == 33) {
+    if constexpr (BLK == 16) {
+      if (p.WX == 33) kern = nt == 512 ? sad_kernel<16, 33, 1, 512, 33> : sad_kernel<16, 33, 1, 256, 33>;
+      if (p.WX == 65) kern = nt == 512 ? sad_kernel<16, 33, 1, 512, 65> : sad_kernel<16, 33, 1, 256, 65>;
+    } else {
+      if (p.WX == 65 && L.nby == 2) kern = nt == 512 ? sad_kernel<8, 33, 2, 512, 65> : sad_kernel<8, 33, 2, 256, 65>;
+    }
+  }
+  if (const char* we = getenv("MERIT_SAD_WXC"); we && we[0] == '0') {  // A/B switch: runtime width
+    kern = nt == 512 ? sad_kernel<BLK, D, 1, 512, 0> : sad_kernel<BLK, D, 1, 256, 0>;
+    if constexpr (BLK == 8) {
+      if (L.nby == 2) kern = nt == 512 ? sad_kernel<BLK, D, 2, 512, 0> : sad_kernel<BLK, D, 2, 256, 0>;
+    }
   }
   cudaError_t e = set_smem_attr(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return cuda_check(e, "set_smem_attr(sad)");
   const int threads = (L.items + 31) / 32 * 32;
+  L.cp_sr = threads / L.Ww;
+  L.cp_sw = threads - L.cp_sr * L.Ww;
+  fast_div_init(static_cast<uint32_t>(L.n_tiles_x), L.ntx_m, L.ntx_s);
+  fast_div_init(static_cast<uint32_t>(L.BYT), L.byt_m, L.byt_s);
   long long grid = (nt == 512 ? 1LL : 2LL) * num_sms();
   if (grid > L.n_tiles) grid = L.n_tiles;
   e = launch_pdl(kern, dim3(static_cast<unsigned>(grid)), dim3(threads), smem, s, 1, cur, ref, out, aux, L, ref_map,
