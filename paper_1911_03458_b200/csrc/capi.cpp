@@ -61,10 +61,8 @@ cudaError_t set_smem_attr_impl(const void* fn, cudaFuncAttribute attr, int bytes
 
 using namespace merit_dev;
 
-namespace {
-
 // Device-side state a plan needs lazily (program image, error flag).
-merit_status ensure_device_state(const merit_plan& plan) {
+merit_status merit_dev::ensure_device_state(const merit_plan& plan) {
   std::lock_guard<std::mutex> lk(plan.mu);
   int dev = 0;
   merit_status st = cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
@@ -92,8 +90,6 @@ merit_status ensure_device_state(const merit_plan& plan) {
   }
   return MERIT_OK;
 }
-
-}  // namespace
 
 extern "C" {
 
@@ -148,6 +144,7 @@ merit_status merit_dev_plan_destroy(merit_plan* plan) {
     cudaSetDevice(plan->stage_dev);
     for (void* p : plan->stage)
       if (p) cudaFree(p);
+    release_host_pipeline(*plan);
     cudaSetDevice(cur);
   }
   delete plan;
@@ -251,6 +248,7 @@ merit_status merit_dev_run_host(const merit_plan* plan, const void* h_a, const v
         if (p) cudaFree(p);
         p = nullptr;
       }
+      release_host_pipeline(*plan);
       cudaSetDevice(dev);
     }
     for (size_t& b : plan->stage_bytes) b = 0;
@@ -276,6 +274,9 @@ merit_status merit_dev_run_host(const merit_plan* plan, const void* h_a, const v
     st = cuda_check((expr), what);                             \
     if (st != MERIT_OK) { cudaStreamSynchronize(s); return st; } \
   } while (0)
+  // Sliced plans overlap H2D, kernel and D2H slice by slice (host_pipeline.cpp)
+  st = run_host_pipelined(*plan, da, db, dout, daux, h_a, h_b, h_out, h_aux, need_b, stream);
+  if (st != MERIT_E_UNSUPPORTED_VIEW) return st;
   MERIT_TRY(cudaMemcpyAsync(da, h_a, info.src_a_bytes, cudaMemcpyHostToDevice, s), "H2D a");
   if (need_b) MERIT_TRY(cudaMemcpyAsync(db, h_b, info.src_b_bytes, cudaMemcpyHostToDevice, s), "H2D b");
   st = merit_dev_run(plan, da, db, dout, daux, stream);

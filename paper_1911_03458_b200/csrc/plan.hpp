@@ -90,6 +90,9 @@ struct SadParams {
   int32_t write_map = 1;
   int32_t argmin = 0;
   int32_t out_f32 = 0;      // SAD map as float (REAL32) instead of int32
+  // Block-row band of one launch (pipelined host-buffer runs): block rows
+  // [by_begin, by_begin + by_count) of every pair; by_count 0 = all BY rows.
+  int32_t by_begin = 0, by_count = 0;
 };
 
 // K3: implicit-GEMM convolution on tcgen05 (mac_program over conv views).
@@ -118,6 +121,23 @@ struct ConvParams {
 
 }  // namespace merit_dev
 
+struct merit_plan;
+
+namespace merit_dev {
+// One piece of a pipelined host-buffer run (merit_dev_run_host): a sub-plan
+// over a slice of the outermost independent axis (max-pool planes, conv
+// images, SAD frame pairs or block-row bands), the source prefixes it reads
+// and the output byte ranges it writes.
+struct HostSlice {
+  merit_plan* sub = nullptr;            // owned by the parent plan
+  int64_t a_off = 0, b_off = 0;         // launch pointer offsets (bytes)
+  int64_t out_off = 0, aux_off = 0;
+  int64_t a_need = 0, b_need = 0;       // source prefix (bytes) that must have landed
+  int64_t out_lo = 0, out_hi = 0;       // bytes written (D2H ranges)
+  int64_t aux_lo = 0, aux_hi = 0;
+};
+}  // namespace merit_dev
+
 struct merit_plan {
   int32_t kernel = MERIT_KERNEL_GENERIC;
   merit_workload_desc desc{};
@@ -141,6 +161,13 @@ struct merit_plan {
   mutable void* stage[4] = {nullptr, nullptr, nullptr, nullptr};
   mutable size_t stage_bytes[4] = {0, 0, 0, 0};
   mutable int stage_dev = -1;
+  // Pipelined host-buffer runs: slices (built on first use, host only) and
+  // the H2D / D2H copy streams + events (on stage_dev).
+  mutable bool slices_built = false;
+  mutable std::vector<merit_dev::HostSlice> slices;
+  mutable void* copy_stream[2] = {nullptr, nullptr};
+  mutable std::vector<void*> copy_events;
+  ~merit_plan();
 };
 
 namespace merit_dev {
@@ -149,6 +176,17 @@ namespace merit_dev {
 merit_status fail(merit_status st, const std::string& msg);
 
 merit_status lower(const merit_workload_desc& d, merit_plan& plan);
+
+// Pipelined host-buffer run (host_pipeline.cpp): H2D of slice k+1, the kernel
+// of slice k and the D2H of slice k-1 overlap on three streams.  Returns
+// MERIT_E_UNSUPPORTED_VIEW (and does nothing) when the plan does not slice.
+merit_status run_host_pipelined(const merit_plan& plan, void* da, void* db, void* dout, void* daux,
+                                const void* h_a, const void* h_b, void* h_out, void* h_aux, bool need_b,
+                                void* stream);
+// Lazily allocate a plan's device state on the current device (capi.cpp).
+merit_status ensure_device_state(const merit_plan& plan);
+// Release the pipeline's streams/events (plan destruction, device switch).
+void release_host_pipeline(const merit_plan& plan);
 
 // Kernel launchers (defined in the .cu files).  All asynchronous on `stream`.
 merit_status launch_generic(const merit_plan& plan, const void* a, const void* b, void* out,

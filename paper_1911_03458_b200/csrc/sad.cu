@@ -78,6 +78,7 @@ struct SadLaunch {
   uint32_t ntx_m, ntx_s;      // n / n_tiles_x as a multiply-high (fast_div)
   uint32_t byt_m, byt_s;      // n / BYT
   int cp_sr, cp_sw;           // copy builder: blockDim.x = cp_sr * Ww + cp_sw
+  int by0, by1;               // block-row band [by0, by1) of this launch
 };
 
 // n / d for n < 2^31 by multiply-high (Granlund-Montgomery): s = ceil(log2 d),
@@ -101,7 +102,7 @@ __device__ __forceinline__ void stage_tile(const SadLaunch& L, const uint8_t* __
   const int t2 = static_cast<int>(fast_div(tile, L.ntx_m, L.ntx_s));
   const int tx = tile - t2 * L.n_tiles_x;
   const long long pair = fast_div(t2, L.byt_m, L.byt_s);
-  const int by = t2 - static_cast<int>(pair) * L.BYT;  // nby == 1 on this path
+  const int by = L.by0 + t2 - static_cast<int>(pair) * L.BYT;  // nby == 1 on this path
   const int bx0 = tx * L.TBX;
   const int nb = min(L.TBX, p.BX - bx0);
   const uint8_t* refp = ref + pair * (long long)p.Hr * p.Wr;
@@ -212,7 +213,7 @@ __device__ __forceinline__ void issue_tile(const SadLaunch& L, const uint8_t* __
       const int t2 = static_cast<int>(fast_div(tile, L.ntx_m, L.ntx_s));
       const int tx = tile - t2 * L.n_tiles_x;
       const int pair = static_cast<int>(fast_div(t2, L.byt_m, L.byt_s));
-      const int by = (t2 - pair * L.BYT) * L.nby;
+      const int by = L.by0 + (t2 - pair * L.BYT) * L.nby;
       const int bx0 = tx * L.TBX;
       const uint32_t bytes = L.R_box * L.rw * 4 + L.nby * BLK * L.cur_pitch;
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
@@ -289,7 +290,7 @@ sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, voi
     const int t2 = static_cast<int>(fast_div(tile, L.ntx_m, L.ntx_s));
     const int tx = tile - t2 * L.n_tiles_x;
     const int pair_i = static_cast<int>(fast_div(t2, L.byt_m, L.byt_s));
-    const int by = (t2 - pair_i * L.BYT) * NBY;  // first block row of the tile
+    const int by = L.by0 + (t2 - pair_i * L.BYT) * NBY;  // first block row of the tile
     const long long pair = pair_i;
     const int bx0 = tx * L.TBX;
     const int nb = min(L.TBX, p.BX - bx0);
@@ -405,7 +406,7 @@ sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, voi
 #pragma unroll
         for (int n = 0; n < NBY; ++n) {
           uint32_t bn = 0xffffffffu;
-          const bool store = p.write_map && by + n < p.BY;
+          const bool store = p.write_map && by + n < L.by1;
           const long long obase = ((blk_index + n * (long long)p.BX) * p.WY + dy0) * WX + idx;
           if (nd == D) {  // full group: no per-displacement predicates
 #pragma unroll
@@ -449,7 +450,7 @@ sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, voi
         // the top of the loop).
 #pragma unroll
         for (int n = 0; n < NBY; ++n) {
-          if (by + n >= p.BY) break;
+          if (by + n >= L.by1) break;
           const int slot = n * L.TBX + ib;
           atomicMin(&keys[slot], best[n]);
           __threadfence_block();
@@ -530,9 +531,12 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
   L.vec_path = (L.word_path && (p.ox % 16) == 0 && (p.Wr % 16) == 0 && (BLK % 16) == 0 &&
                 (reinterpret_cast<uintptr_t>(ref) % 16) == 0) ? 1 : 0;
   // geometry for nby block rows per tile; TMA staging only where the boxes fit
+  L.by0 = p.by_begin;
+  L.by1 = p.by_count > 0 ? p.by_begin + p.by_count : p.BY;
+  if (L.by0 < 0 || L.by1 > p.BY || L.by0 >= L.by1) return fail(MERIT_E_INVALID_ARGUMENT, "bad SAD block-row band");
   auto geometry = [&](int nby, bool tma) {
     L.nby = nby;
-    L.BYT = (p.BY + nby - 1) / nby;
+    L.BYT = (L.by1 - L.by0 + nby - 1) / nby;
     L.R = L.G * D + nby * BLK - 1;
     L.rw = tma ? (L.Ww + 5 + 3) / 4 * 4 : (L.Ww + 1 + 3) / 4 * 4;  // raw words per row, 16-byte chunks
     L.CS = L.R * L.Ww;
