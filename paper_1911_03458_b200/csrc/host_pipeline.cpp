@@ -26,12 +26,14 @@ namespace merit_dev {
 
 namespace {
 
-// Slice count: ~4 MB of transfers per slice, at most 16, at most one slice
-// per unit.  MERIT_HOST_CHUNKS=n forces n (1 = the unpipelined path).
+// Slice count: one per ~6 MB of transfers, at most 16, at most one per unit
+// (measured: every slice costs ~8 us of copy-engine gaps, so a few large
+// slices beat many small ones).  MERIT_HOST_CHUNKS=n forces n (1 = the
+// unpipelined path).
 int64_t slice_count(const merit_plan& plan, int64_t units) {
   const merit_plan_info& in = plan.info;
   const int64_t total = in.src_a_bytes + in.src_b_bytes + in.out_bytes + in.aux_elems * 4;
-  int64_t k = std::max<int64_t>(1, std::min<int64_t>(16, total / (4 << 20)));
+  int64_t k = std::max<int64_t>(1, std::min<int64_t>(16, total / (6 << 20)));
   if (const char* e = getenv("MERIT_HOST_CHUNKS")) k = std::max(1, atoi(e));
   return std::min(k, units);
 }
@@ -47,10 +49,25 @@ merit_plan* clone_params(const merit_plan& p) {
   return s;
 }
 
-// Units [u0, u1) of slice i of k over n units (sizes differ by at most one).
+// Units [u0, u1) of slice i of k over n units, triangular weights
+// 1, 2, .., m, .., 2, 1: the first slice (whose H2D + kernel precede every
+// D2H) and the last one (whose kernel + D2H follow every H2D) are the
+// smallest, so the pipeline fills and drains in a fraction of a uniform
+// slice.  MERIT_HOST_RAMP=0 gives uniform slices.
+int64_t ramp_weight_sum(int64_t k, int64_t i) {  // sum of the first i weights
+  static const int ramp = [] {
+    const char* e = getenv("MERIT_HOST_RAMP");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  if (!ramp) return i;
+  int64_t s = 0;
+  for (int64_t j = 0; j < i; ++j) s += std::min(j + 1, k - j);
+  return s;
+}
 void split(int64_t n, int64_t k, int64_t i, int64_t& u0, int64_t& u1) {
-  u0 = n * i / k;
-  u1 = n * (i + 1) / k;
+  const int64_t tot = ramp_weight_sum(k, k);
+  u0 = n * ramp_weight_sum(k, i) / tot;
+  u1 = n * ramp_weight_sum(k, i + 1) / tot;
 }
 
 void build_slices(const merit_plan& plan) {
@@ -66,6 +83,7 @@ void build_slices(const merit_plan& plan) {
     for (int64_t i = 0; i < k; ++i) {
       int64_t u0, u1;
       split(n, k, i, u0, u1);
+      if (u1 == u0) continue;
       HostSlice s;
       s.sub = clone_params(plan);
       s.sub->mp.planes = u1 - u0;
@@ -90,6 +108,7 @@ void build_slices(const merit_plan& plan) {
     for (int64_t i = 0; i < k; ++i) {
       int64_t u0, u1;
       split(n, k, i, u0, u1);
+      if (u1 == u0) continue;
       HostSlice s;
       s.sub = clone_params(plan);
       s.sub->conv.N = static_cast<int32_t>(u1 - u0);
@@ -113,6 +132,7 @@ void build_slices(const merit_plan& plan) {
       for (int64_t i = 0; i < k; ++i) {
         int64_t u0, u1;
         split(n, k, i, u0, u1);
+        if (u1 == u0) continue;
         HostSlice s;
         s.sub = clone_params(plan);
         s.sub->sad.pairs = u1 - u0;
@@ -136,6 +156,7 @@ void build_slices(const merit_plan& plan) {
       for (int64_t i = 0; i < k; ++i) {
         int64_t u0, u1;
         split(n, k, i, u0, u1);
+        if (u1 == u0) continue;
         HostSlice s;
         s.sub = clone_params(plan);
         s.sub->sad.by_begin = static_cast<int32_t>(u0);
