@@ -339,8 +339,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tap3_kernel(Tap3Args A) {
     }
     __syncwarp();
   } else if (warp == kWarpMma) {
-    // ============ MMA issuer ===================================================
-    if (lane == 0) {
+    // ============ MMA issuer (whole warp, elected lane) ===================================================
+    {
       const uint32_t idesc = make_idesc(BN);
       const bool mprof = (A.debug & 64) != 0;
       unsigned long long m_a = 0, m_b = 0, m_t = 0;
@@ -367,31 +367,31 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tap3_kernel(Tap3Args A) {
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const uint32_t accum = (g > 0 || kx > 0 || k > 0) ? 1u : 0u;
-              tc_mma(d_tmem, sw128_desc(a_hi + 32 * k), sw128_desc(b_hi + 32 * k), idesc, accum);
+              tc_mma_w(d_tmem, (sw128_desc(a_hi) + 2 * k), (sw128_desc(b_hi) + 2 * k), idesc, accum);
               if (SPLIT3) {
-                tc_mma(d_tmem, sw128_desc(a_hi + 32 * k), sw128_desc(b_lo + 32 * k), idesc, 1u);
-                tc_mma(d_tmem, sw128_desc(a_lo + 32 * k), sw128_desc(b_hi + 32 * k), idesc, 1u);
+                tc_mma_w(d_tmem, (sw128_desc(a_hi) + 2 * k), (sw128_desc(b_lo) + 2 * k), idesc, 1u);
+                tc_mma_w(d_tmem, (sw128_desc(a_lo) + 2 * k), (sw128_desc(b_hi) + 2 * k), idesc, 1u);
               }
             }
-            tc_commit(b_empty(bs));
+            tc_commit_w(b_empty(bs));
             if (++bs == A.nb) {
               bs = 0;
               bph ^= 1;
             }
           }
-          tc_commit(a_empty(as));
+          tc_commit_w(a_empty(as));
           if (++as == A.na) {
             as = 0;
             aph ^= 1;
           }
         }
-        tc_commit(tfull_bar(acc));
+        tc_commit_w(tfull_bar(acc));
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
         }
       }
-      if (mprof) {
+      if (mprof && lane == 0) {
         unsigned long long* pr = A.prof + (blockIdx.x * 16 + warp) * 8;
         pr[0] = clock64() - m_start; pr[1] = m_a; pr[2] = m_b; pr[3] = m_t;
       }

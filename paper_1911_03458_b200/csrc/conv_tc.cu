@@ -479,8 +479,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(ConvArgs A) {
     }
     __syncwarp();
   } else if (warp == kWarpMma) {
-    // ================= MMA issuer (single thread) ===========================
-    if (lane == 0) {
+    // ================= MMA issuer (whole warp, elected lane) ===========================
+    {
       const bool mprof = (A.debug & 64) != 0;
       unsigned long long m_full = 0, m_tempty = 0;
       const unsigned long long m_start = clock64();
@@ -503,25 +503,25 @@ __global__ void __launch_bounds__(kThreads, 1) conv_tc_kernel(ConvArgs A) {
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             const uint32_t accum = (kb > 0 || k > 0) ? 1u : 0u;
-            tc_mma(d_tmem, sw128_desc(a_hi + 32 * k), sw128_desc(b_hi + 32 * k), idesc, accum);
+            tc_mma_w(d_tmem, (sw128_desc(a_hi) + 2 * k), (sw128_desc(b_hi) + 2 * k), idesc, accum);
             if (SPLIT3) {
-              tc_mma(d_tmem, sw128_desc(a_hi + 32 * k), sw128_desc(b_lo + 32 * k), idesc, 1u);
-              tc_mma(d_tmem, sw128_desc(a_lo + 32 * k), sw128_desc(b_hi + 32 * k), idesc, 1u);
+              tc_mma_w(d_tmem, (sw128_desc(a_hi) + 2 * k), (sw128_desc(b_lo) + 2 * k), idesc, 1u);
+              tc_mma_w(d_tmem, (sw128_desc(a_lo) + 2 * k), (sw128_desc(b_hi) + 2 * k), idesc, 1u);
             }
           }
-          tc_commit(empty_bar(stage));
+          tc_commit_w(empty_bar(stage));
           if (++stage == kStages) {
             stage = 0;
             phase ^= 1;
           }
         }
-        tc_commit(tfull_bar(acc));
+        tc_commit_w(tfull_bar(acc));
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
         }
       }
-      if (mprof) {
+      if (mprof && lane == 0) {
         unsigned long long* pr = A.prof + (blockIdx.x * 16 + warp) * 4;
         pr[0] = clock64() - m_start;
         pr[1] = m_full;

@@ -295,39 +295,41 @@ conv_tma_kernel(const __grid_constant__ CUtensorMap in_map, const __grid_constan
     }
     __syncwarp();
   } else if (warp == kWarpMma) {
-    // ============ MMA issuer ===================================================
-    if (lane == 0 && rank == 0) {
+    // ============ MMA issuer: the leader CTA's whole warp runs the loop
+    // (warp-uniform operands), one elected lane issues (tc_common.cuh) ======
+    if (rank == 0) {
+      const bool pon_w = (A.debug & 64) != 0;
       const uint32_t idesc = PAIR ? make_idesc_pair(BN) : make_idesc(BN);
       int as = 0, bs = 0, acc = 0;
       uint32_t aph = 0, bph = 0, acc_phase = 0;
       for (int tile = unit0; tile < A.n_units; tile += ustep) {
-        twait(tempty(acc), acc_phase ^ 1, w3, pon);
+        twait(tempty(acc), acc_phase ^ 1, w3, pon_w);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
         for (int g = 0; g < A.n_groups; ++g) {
-          twait(a_full(as), aph, w1, pon);
+          twait(a_full(as), aph, w1, pon_w);
           tc_fence_after();
           for (int kx = 0; kx < 3; ++kx) {
-            twait(b_full(bs), bph, w2, pon);
+            twait(b_full(bs), bph, w2, pon_w);
             tc_fence_after();
             // tap 0 = tap-2 plane one slot row earlier; tap 1; tap 2
             const uint32_t a0 = kx == 1 ? tap1_plane(as) : tap2_plane(as) - (kx == 0 ? 128u : 0u);
-            const uint32_t b0 = bring + bs * A.b_slot;
+            const uint64_t ad = sw128_desc(a0), bd = sw128_desc(bring + bs * A.b_slot);
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               const uint32_t accum = (g > 0 || kx > 0 || k > 0) ? 1u : 0u;
               if (PAIR)
-                tc_mma_pair(d_tmem, sw128_desc(a0 + 32 * k), sw128_desc(b0 + 32 * k), idesc, accum);
+                tc_mma_pair_w(d_tmem, ad + 2 * k, bd + 2 * k, idesc, accum);
               else
-                tc_mma(d_tmem, sw128_desc(a0 + 32 * k), sw128_desc(b0 + 32 * k), idesc, accum);
+                tc_mma_w(d_tmem, ad + 2 * k, bd + 2 * k, idesc, accum);
             }
-            if (PAIR) tc_commit_pair(b_empty(bs), 3); else tc_commit(b_empty(bs));
+            if (PAIR) tc_commit_pair_w(b_empty(bs), 3); else tc_commit_w(b_empty(bs));
             if (++bs == A.nb) { bs = 0; bph ^= 1; }
           }
-          if (PAIR) tc_commit_pair(a_empty(as), 3); else tc_commit(a_empty(as));
+          if (PAIR) tc_commit_pair_w(a_empty(as), 3); else tc_commit_w(a_empty(as));
           if (++as == A.na) { as = 0; aph ^= 1; }
         }
-        if (PAIR) tc_commit_pair(tfull(acc), 3); else tc_commit(tfull(acc));
+        if (PAIR) tc_commit_pair_w(tfull(acc), 3); else tc_commit_w(tfull(acc));
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }

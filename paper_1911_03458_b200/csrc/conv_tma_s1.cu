@@ -56,7 +56,7 @@ struct S1Args {
   int n_full;          // units below n_full are whole tiles; the last (n_tiles - n_full)
   int n_units;         // tiles run as two half-N units each (the final, partial wave)
   int n_groups;        // KH * CB
-  uint32_t raw_bytes;  // W * rows * 32 ch * 4 (half a 64-channel k-block)
+  uint32_t raw_bytes;  // 128 slots * 32 ch * 4 = 16 KB (half a 64-channel k-block)
   uint32_t a_slot;     // nsplit planes x 16 KB
   uint32_t b_plane;    // BN * 128: one tap, one split plane
   uint32_t b_slot;     // 3 taps x nsplit planes
@@ -84,9 +84,15 @@ __device__ __forceinline__ void twait_s1(uint32_t bar, uint32_t par, unsigned lo
   }
 }
 
-template <bool SPLIT3>
+// TMEMA: the A planes live in TMEM (columns 384..511: two slots of hi | lo,
+// 32 columns each) and the MMA reads A from there (tcgen05.mma [a_tmem]):
+// the repack writes them with tcgen05.st and the tensor core's shared-memory
+// traffic drops to B alone.  Needs 3 BN <= 192 (two 192-column accumulators).
+constexpr uint32_t kTmemA = 384;
+template <bool SPLIT3, bool TMEMA>
 __global__ void __maxnreg__(96)  // 19 warps: <= 5 per SM sub-partition x 96 regs
 conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
+  constexpr uint32_t acc_cols = TMEMA ? 192u : kAccCols;
   extern __shared__ uint8_t smem_raw[];
   const ConvParams& p = A.p;
   const int warp = threadIdx.x >> 5;
@@ -94,7 +100,7 @@ conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;
   const uint32_t aring = base;                          // na x a_slot
   const uint32_t bring = aring + A.na * A.a_slot;       // nb x b_slot
-  const uint32_t rring = bring + A.nb * A.b_slot;       // nr x raw_bytes
+  const uint32_t rring = bring + A.nb * A.b_slot + 128;  // nr x raw_bytes after a 128-B zero pad
   const uint32_t xring = rring + A.nr * A.raw_bytes;    // epilogue edge exchange
   const uint32_t bars = xring + 2 * 2 * 4 * 16 * 4;  // [set][parity][warp][8 P0 | 8 P2]
   auto r_full = [&](int s) { return bars + 8u * s; };
@@ -109,6 +115,10 @@ conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
   volatile uint32_t* tmem_slot_ptr =
       reinterpret_cast<volatile uint32_t*>(smem_raw + (tmem_slot - smem_u32(smem_raw)));
 
+  if (threadIdx.x < 32) {  // zero pad read as the x = -1 column of slot 0's first row
+    const uint32_t z = rring - 128 + 4u * threadIdx.x;
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(z), "r"(0u) : "memory");
+  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < A.nr; ++s) {
       mbar_init(r_full(s), 1);
@@ -184,6 +194,48 @@ conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
       }
     }
     __syncwarp();
+  } else if (TMEMA && warp < kRepackWarps) {
+    // ============ repack into TMEM: lane = A row (slot), 32 channels per warp
+    // warp w: TMEM lane quadrant w & 3 (the warp's own), channel half w >> 2
+    // (raw half slot); every lane loads its pixel's 32 channels (consecutive
+    // lanes = consecutive x: conflict-free), splits them and stores 16 hi +
+    // 16 lo columns.
+    const int w = warp;
+    const int q = w & 3, h = w >> 2;
+    const int m = 32 * q + lane;
+    // raw [c][128 slots]: A row m is slot m, i.e. raw word m - 1 (the
+    // zero-filled column x = slots - 1 of the previous row, or the pad, for
+    // x = -1); channel stride 512 B, an immediate
+    const uint32_t lane_off = static_cast<uint32_t>(m - 1) * 4u;
+    const uint32_t t_lane = tmem_base + (static_cast<uint32_t>(32 * q) << 16) + kTmemA + 16u * h;
+    int rs = h, as = 0;
+    uint32_t rph = 0, aph = 0;
+    for (int u = blockIdx.x; u < A.n_units; u += gridDim.x) {
+      for (int g = 0; g < A.n_groups; ++g) {
+        twait_s1(r_full(rs), rph, w1, pon);
+        float v[32];
+        const uint32_t src = rring + rs * A.raw_bytes + lane_off;
+        const float* sp = reinterpret_cast<const float*>(smem_raw + (src - smem_u32(smem_raw)));
+#pragma unroll
+        for (int c = 0; c < 32; ++c) v[c] = sp[c * 128];
+        mbar_arrive(r_empty(rs));
+        rs += 2;
+        while (rs >= A.nr) { rs -= A.nr; rph ^= 1; }
+        uint32_t hi[16], lo[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) split_bf16x2(v[2 * i], v[2 * i + 1], hi[i], lo[i]);
+        twait_s1(a_empty(as), aph ^ 1, w2, pon);
+        tc_fence_after();
+        const uint32_t ta = t_lane + static_cast<uint32_t>(as) * 64u;
+        TMEM_ST16(ta, hi);
+        if (SPLIT3) TMEM_ST16(ta + 32u, lo);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(a_full(as));
+        if (++as == A.na) { as = 0; aph ^= 1; }
+      }
+    }
   } else if (warp < kRepackWarps) {
     // ============ repack: raw fp32 [c][r][W] -> bf16 hi/lo K-major planes ===
     // warp w: channels 8w..8w+7 of the k-block (chunk column w of every A
@@ -191,8 +243,7 @@ conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
     // the odd ones); lane l: A rows 32j + l, j = 0..3, so an STS.128 phase
     // writes 8 consecutive rows and the 128-B swizzle spreads the banks.
     const int w = warp;
-    const uint32_t rowf = static_cast<uint32_t>(W);  // floats per raw row
-    const uint32_t cbase = static_cast<uint32_t>(8 * (w & 3)) * A.rows * rowf * 4u;
+    const uint32_t cbase = static_cast<uint32_t>(8 * (w & 3)) * 512u;  // raw [c][128 slots]
     int rs = w >> 2, as = 0;
     uint32_t rph = 0, aph = 0;
     for (int u = blockIdx.x; u < A.n_units; u += gridDim.x) {
@@ -204,17 +255,10 @@ conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
         const uint32_t src = rring + rs * A.raw_bytes + cbase;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const int arow = 32 * j + lane;
-          const int r = arow >> A.slots_log2;
-          const int x = (arow & slots_mask) - 1;
-          const bool ok = x >= 0 && x < W;
-          const uint32_t a0 = src + (static_cast<uint32_t>(r) * rowf + (ok ? x : 0)) * 4u;
+          const uint32_t a0 = src + static_cast<uint32_t>(32 * j + lane - 1) * 4u;
+          const float* sp = reinterpret_cast<const float*>(smem_raw + (a0 - smem_u32(smem_raw)));
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            float t = 0.f;
-            if (ok) asm volatile("ld.shared.f32 %0, [%1];" : "=f"(t) : "r"(a0 + c * A.rows * rowf * 4u));
-            v[j][c] = t;
-          }
+          for (int c = 0; c < 8; ++c) v[j][c] = sp[c * 128];
         }
         mbar_arrive(r_empty(rs));
         rs += 2;
@@ -265,42 +309,56 @@ conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
     }
     __syncwarp();
   } else if (warp == kWarpMma) {
-    // ============ MMA issuer ===================================================
-    if (lane == 0) {
-      const uint32_t idesc_full = make_idesc(3 * BN);
-      const uint32_t idesc_half = make_idesc(3 * (BN / 2));
-      int as = 0, bs = 0, acc = 0;
-      uint32_t aph = 0, bph = 0, acc_phase = 0;
-      for (int u = blockIdx.x; u < A.n_units; u += gridDim.x) {
-        int tile, half;
-        unit_of(u, tile, half);
-        const uint32_t idesc = half < 0 ? idesc_full : idesc_half;
-        const uint32_t b_lo = 3 * (half < 0 ? A.b_plane : A.b_plane / 2);
-        twait_s1(tempty(acc), acc_phase ^ 1, w3, pon);
+    // ============ MMA issuer: the whole warp runs the loop (warp-uniform
+    // operands in uniform registers), one elected lane issues each MMA ======
+    const bool pon_w = (A.debug & 64) != 0;
+    const uint32_t idesc_full = make_idesc(3 * BN);
+    const uint32_t idesc_half = make_idesc(3 * (BN / 2));
+    int as = 0, bs = 0, acc = 0;
+    uint32_t aph = 0, bph = 0, acc_phase = 0;
+    for (int u = blockIdx.x; u < A.n_units; u += gridDim.x) {
+      int tile, half;
+      unit_of(u, tile, half);
+      const uint32_t idesc = half < 0 ? idesc_full : idesc_half;
+      const uint32_t b_lo16 = (3 * (half < 0 ? A.b_plane : A.b_plane / 2)) >> 4;  // lo planes, descriptor units
+      twait_s1(tempty(acc), acc_phase ^ 1, w3, pon_w);
+      tc_fence_after();
+      const uint32_t d_tmem = tmem_base + acc * acc_cols;
+      for (int g = 0; g < A.n_groups; ++g) {
+        if (!(A.debug & 2048)) {  // 2048: timing experiment, MMAs without operand waits
+          twait_s1(a_full(as), aph, w1, pon_w);
+          twait_s1(b_full(bs), bph, w2, pon_w);
+        }
         tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * kAccCols;
-        for (int g = 0; g < A.n_groups; ++g) {
-          twait_s1(a_full(as), aph, w1, pon);
-          twait_s1(b_full(bs), bph, w2, pon);
-          tc_fence_after();
-          const uint32_t a0 = aring + as * A.a_slot;
-          const uint32_t b0 = bring + bs * A.b_slot;
+        const uint64_t bd = sw128_desc(bring + bs * A.b_slot);
+        if constexpr (TMEMA) {
+          const uint32_t ta = tmem_base + kTmemA + static_cast<uint32_t>(as) * 64u;
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            tc_mma(d_tmem, sw128_desc(a0 + 32 * k), sw128_desc(b0 + 32 * k), idesc, (g > 0 || k > 0) ? 1u : 0u);
+            tc_mma_ts_w(d_tmem, ta + 8 * k, bd + 2 * k, idesc, (g > 0 || k > 0) ? 1u : 0u);
             if (SPLIT3) {
-              tc_mma(d_tmem, sw128_desc(a0 + 32 * k), sw128_desc(b0 + b_lo + 32 * k), idesc, 1u);
-              tc_mma(d_tmem, sw128_desc(a0 + kAPlane + 32 * k), sw128_desc(b0 + 32 * k), idesc, 1u);
+              tc_mma_ts_w(d_tmem, ta + 8 * k, bd + b_lo16 + 2 * k, idesc, 1u);
+              tc_mma_ts_w(d_tmem, ta + 32 + 8 * k, bd + 2 * k, idesc, 1u);
             }
           }
-          tc_commit(b_empty(bs));
-          if (++bs == A.nb) { bs = 0; bph ^= 1; }
-          tc_commit(a_empty(as));
-          if (++as == A.na) { as = 0; aph ^= 1; }
+        } else {
+          const uint64_t ad = sw128_desc(aring + as * A.a_slot);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            tc_mma_w(d_tmem, ad + 2 * k, bd + 2 * k, idesc, (g > 0 || k > 0) ? 1u : 0u);
+            if (SPLIT3) {
+              tc_mma_w(d_tmem, ad + 2 * k, bd + b_lo16 + 2 * k, idesc, 1u);
+              tc_mma_w(d_tmem, ad + (kAPlane >> 4) + 2 * k, bd + 2 * k, idesc, 1u);
+            }
+          }
         }
-        tc_commit(tfull(acc));
-        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        tc_commit_w(b_empty(bs));
+        if (++bs == A.nb) { bs = 0; bph ^= 1; }
+        tc_commit_w(a_empty(as));
+        if (++as == A.na) { as = 0; aph ^= 1; }
       }
+      tc_commit_w(tfull(acc));
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
     __syncwarp();
   } else if ((warp >= kWarpEpi0 && warp < kWarpEpi0 + 4) || warp >= kWarpEpi1) {
@@ -343,7 +401,7 @@ conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         continue;
       }
-      const uint32_t t_row = tmem_base + acc * kAccCols + (static_cast<uint32_t>(q * 32) << 16);
+      const uint32_t t_row = tmem_base + acc * acc_cols + (static_cast<uint32_t>(q * 32) << 16);
       for (int ch = set; ch < n_chunks; ch += 2) {
         const int c0 = ch * kEC;
         uint32_t p0[kEC], p1[kEC], p2[kEC];
@@ -444,11 +502,13 @@ merit_status launch_conv_s1(const merit_plan& plan, const void* a, const void* p
   A.n_groups = p.KH * p.CB;
   const bool split3 = p.split == 3;
   const uint32_t nsp = split3 ? 2u : 1u;
-  A.raw_bytes = static_cast<uint32_t>(p.W) * A.rows * 32u * 4u;
-  A.a_slot = nsp * kAPlane;
+  const char* te = getenv("MERIT_S1_TMEMA");
+  const bool tmema = !(te && te[0] == '0') && 3 * p.BN <= 192;
+  A.raw_bytes = 128u * 32u * 4u;  // box {slots, rows, 32 ch}: slots * rows = 128
+  A.a_slot = tmema ? 0u : nsp * kAPlane;  // TMEM-resident A: no shared-memory ring
   A.b_plane = static_cast<uint32_t>(p.BN) * 128u;
   A.b_slot = 3u * nsp * A.b_plane;
-  const size_t fixed = 1024 + 2 * 2 * 4 * 16 * 4 + 8 * (6 * kMaxRing + 4) + 16;
+  const size_t fixed = 1024 + 128 + 2 * 2 * 4 * 16 * 4 + 8 * (6 * kMaxRing + 4) + 16;
   const size_t budget = 227 * 1024 - fixed;
   A.na = 2;
   A.nb = 2;
@@ -459,7 +519,7 @@ merit_status launch_conv_s1(const merit_plan& plan, const void* a, const void* p
   for (;;) {  // grow: raw (even), A, B
     const size_t used = used_bytes();
     if (A.nr < 4 && used + 2 * A.raw_bytes <= budget) { A.nr += 2; continue; }
-    if (A.na < 3 && used + A.a_slot <= budget) { ++A.na; continue; }
+    if (!tmema && A.na < 3 && used + A.a_slot <= budget) { ++A.na; continue; }
     if (A.nb < 3 && used + A.b_slot <= budget) { ++A.nb; continue; }
     break;
   }
@@ -467,7 +527,7 @@ merit_status launch_conv_s1(const merit_plan& plan, const void* a, const void* p
     int na, nb, nr;
     if (sscanf(re, "%d,%d,%d", &na, &nb, &nr) == 3 && na >= 1 && nb >= 1 && nr >= 2 && nr % 2 == 0 &&
         na <= kMaxRing && nb <= kMaxRing && nr <= kMaxRing) {
-      A.na = na; A.nb = nb; A.nr = nr;
+      A.na = tmema ? 2 : na; A.nb = nb; A.nr = nr;
     }
   }
   if (used_bytes() > budget) return fail(MERIT_E_UNSUPPORTED_VIEW, "stride-1 conv rings exceed shared memory");
@@ -476,7 +536,9 @@ merit_status launch_conv_s1(const merit_plan& plan, const void* a, const void* p
   const cuuint64_t dims[4] = {(cuuint64_t)p.W, (cuuint64_t)p.H, (cuuint64_t)p.Cin, (cuuint64_t)p.N};
   const cuuint64_t strides[3] = {(cuuint64_t)p.W * 4, (cuuint64_t)p.H * p.W * 4,
                                  (cuuint64_t)p.Cin * p.H * p.W * 4};
-  const cuuint32_t box[4] = {(cuuint32_t)p.W, (cuuint32_t)A.rows, 32, 1};
+  // box width = slots (> W): columns x >= W land as zeros, so the raw rows
+  // already have the A-row layout (x at slot x + 1, read at word m - 1)
+  const cuuint32_t box[4] = {(cuuint32_t)(1u << A.slots_log2), (cuuint32_t)A.rows, 32, 1};
   const cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult cr = tensor_map_encoder()(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(a), dims, strides,
                                      box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -484,7 +546,8 @@ merit_status launch_conv_s1(const merit_plan& plan, const void* a, const void* p
   if (cr != CUDA_SUCCESS) return fail(MERIT_E_CUDA, "cuTensorMapEncodeTiled failed for the conv input");
   if (A.n_tiles == 0) return MERIT_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  auto kfn = split3 ? conv_s1_kernel<true> : conv_s1_kernel<false>;
+  auto kfn = split3 ? (tmema ? conv_s1_kernel<true, true> : conv_s1_kernel<true, false>)
+                    : (tmema ? conv_s1_kernel<false, true> : conv_s1_kernel<false, false>);
   cudaError_t e = set_smem_attr(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return cuda_check(e, "set_smem_attr(conv_s1)");
   int grid = num_sms();
@@ -529,7 +592,10 @@ merit_status launch_conv_s1(const merit_plan& plan, const void* a, const void* p
             frac(kWarpEpi0, kWarpEpi0 + 4, 1));
     cudaFree(A.prof);
   }
-  return launch_status(split3 ? "conv_s1_kernel<split3, taps stacked on N>" : "conv_s1_kernel<bf16, taps stacked on N>");
+  return launch_status(split3 ? (tmema ? "conv_s1_kernel<split3, taps stacked on N, A in TMEM>"
+                                       : "conv_s1_kernel<split3, taps stacked on N>")
+                              : (tmema ? "conv_s1_kernel<bf16, taps stacked on N, A in TMEM>"
+                                       : "conv_s1_kernel<bf16, taps stacked on N>"));
 }
 
 }  // namespace merit_dev
