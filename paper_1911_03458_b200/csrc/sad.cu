@@ -75,7 +75,10 @@ struct SadLaunch {
   int BYT;        // tile rows = ceil(BY / nby)
   int cur_pitch;  // bytes per staged current-frame row: TBX*BW rounded up to 16
   uint32_t raw_buf, cur_buf;  // bytes per raw / current buffer (128-byte multiples)
-  uint32_t ntx_m, ntx_s;      // n / n_tiles_x as a multiply-high (fast_div)
+  uint32_t ntx_m, ntx_s;      // n / n_full_x as a multiply-high (fast_div)
+  int n_full_x;               // full (TBX-block) tiles per block row
+  int n_full_tiles;           // tiles [0, n_full_tiles) are full; the partial last
+                              // tiles of every row follow (cheap ones in the final wave)
   uint32_t byt_m, byt_s;      // n / BYT
   int cp_sr, cp_sw;           // copy builder: blockDim.x = cp_sr * Ww + cp_sw
   int by0, by1;               // block-row band [by0, by1) of this launch
@@ -93,14 +96,29 @@ __device__ __forceinline__ uint32_t fast_div(uint32_t n, uint32_t m, uint32_t s)
   return (__umulhi(n, m) + n) >> s;
 }
 
+// Tile order: every full tile first (row-major over (pair, block row), TBX
+// blocks each), then the partial last tile of every row.  The partial tiles
+// carry BX % TBX blocks (C2: 1 of 7), so the ragged final wave is made of
+// cheap tiles instead of full ones.  t2 = pair * BYT + tile row, tx = tile column.
+__device__ __forceinline__ void sad_tile_coords(int tile, int n_full_tiles, int n_full_x, uint32_t m, uint32_t s,
+                                                int& t2, int& tx) {
+  if (tile < n_full_tiles) {
+    t2 = static_cast<int>(fast_div(static_cast<uint32_t>(tile), m, s));
+    tx = tile - t2 * n_full_x;
+  } else {
+    t2 = tile - n_full_tiles;
+    tx = n_full_x;
+  }
+}
+
 template <int BLK>
 __device__ __forceinline__ void stage_tile(const SadLaunch& L, const uint8_t* __restrict__ cur,
                                            const uint8_t* __restrict__ ref, int tile,
                                            uint32_t raw_s, uint8_t* raw, uint32_t cur_s,
                                            uint8_t* curs) {
   const SadParams& p = L.p;
-  const int t2 = static_cast<int>(fast_div(tile, L.ntx_m, L.ntx_s));
-  const int tx = tile - t2 * L.n_tiles_x;
+  int t2, tx;
+  sad_tile_coords(tile, L.n_full_tiles, L.n_full_x, L.ntx_m, L.ntx_s, t2, tx);
   const long long pair = fast_div(t2, L.byt_m, L.byt_s);
   const int by = L.by0 + t2 - static_cast<int>(pair) * L.BYT;  // nby == 1 on this path
   const int bx0 = tx * L.TBX;
@@ -210,8 +228,8 @@ __device__ __forceinline__ void issue_tile(const SadLaunch& L, const uint8_t* __
   if (L.tma) {
     if (threadIdx.x == 0) {
       const SadParams& p = L.p;
-      const int t2 = static_cast<int>(fast_div(tile, L.ntx_m, L.ntx_s));
-      const int tx = tile - t2 * L.n_tiles_x;
+      int t2, tx;
+      sad_tile_coords(tile, L.n_full_tiles, L.n_full_x, L.ntx_m, L.ntx_s, t2, tx);
       const int pair = static_cast<int>(fast_div(t2, L.byt_m, L.byt_s));
       const int by = L.by0 + (t2 - pair * L.BYT) * L.nby;
       const int bx0 = tx * L.TBX;
@@ -287,8 +305,8 @@ sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, voi
     }
     __syncthreads();  // raw[buf] landed; previous tile's compute finished
     // tile coordinates
-    const int t2 = static_cast<int>(fast_div(tile, L.ntx_m, L.ntx_s));
-    const int tx = tile - t2 * L.n_tiles_x;
+    int t2, tx;
+    sad_tile_coords(tile, L.n_full_tiles, L.n_full_x, L.ntx_m, L.ntx_s, t2, tx);
     const int pair_i = static_cast<int>(fast_div(t2, L.byt_m, L.byt_s));
     const int by = L.by0 + (t2 - pair_i * L.BYT) * NBY;  // first block row of the tile
     const long long pair = pair_i;
@@ -606,7 +624,14 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
   const int threads = (L.items + 31) / 32 * 32;
   L.cp_sr = threads / L.Ww;
   L.cp_sw = threads - L.cp_sr * L.Ww;
-  fast_div_init(static_cast<uint32_t>(L.n_tiles_x), L.ntx_m, L.ntx_s);
+  L.n_full_x = p.BX / L.TBX;
+  L.n_full_tiles = static_cast<int>(p.pairs * (long long)L.BYT * L.n_full_x);
+  if (const char* oe = getenv("MERIT_SAD_ORDER"); oe && oe[0] == '0') {  // A/B: row-major order
+    L.n_full_x = L.n_tiles_x;
+    L.n_full_tiles = L.n_tiles;
+  }
+  L.ntx_m = L.ntx_s = 0;
+  if (L.n_full_x > 0) fast_div_init(static_cast<uint32_t>(L.n_full_x), L.ntx_m, L.ntx_s);
   fast_div_init(static_cast<uint32_t>(L.BYT), L.byt_m, L.byt_s);
   long long grid = (nt == 512 ? 1LL : 2LL) * num_sms();
   if (grid > L.n_tiles) grid = L.n_tiles;
