@@ -233,6 +233,21 @@ merit_status merit_dev_run(const merit_plan* plan, const void* d_src_a, const vo
 merit_status merit_dev_run_host(const merit_plan* plan, const void* h_src_a, const void* h_src_b,
                                 void* h_out, void* h_aux, void* cuda_stream);
 
+/* How merit_dev_run_host pipelines this plan (host-only, no device needed):
+ * the run is cut along the outermost independent axis (max-pool planes, conv
+ * images, SAD frame pairs or block-row bands) and slice k's H2D, kernel and
+ * D2H overlap slice k+1's.  Writes up to `cap` slices and sets *n_slices to
+ * the count (0: the plan runs unsliced).  a_need / b_need: source bytes that
+ * must have landed before the slice's kernel; out / aux: the byte ranges it
+ * writes.  MERIT_HOST_CHUNKS=n in the environment forces n slices. */
+typedef struct merit_host_slice {
+  int64_t a_need, b_need;
+  int64_t out_lo, out_hi;
+  int64_t aux_lo, aux_hi;
+} merit_host_slice;
+merit_status merit_dev_plan_slices(const merit_plan* plan, merit_host_slice* slices, int64_t cap,
+                                   int64_t* n_slices);
+
 /* merit::run_tiled's traffic report (engine.hpp:72-80, :189-278) for a
  * TilingPlan {t_p, t_a} over this plan's workload: the plan is validated like
  * TilingPlan::validate (engine.hpp:50-63; MERIT_E_BAD_PARAMS) and every pass

@@ -68,6 +68,11 @@ class TrafficReportC(C.Structure):  # merit_traffic_report (engine.hpp:72-80)
                 ("scratchpad_peak_words_b", C.c_uint64), ("passes", C.c_uint64), ("macs", C.c_uint64)]
 
 
+class HostSliceC(C.Structure):  # merit_host_slice (pipelined merit_dev_run_host)
+    _fields_ = [("a_need", C.c_int64), ("b_need", C.c_int64), ("out_lo", C.c_int64), ("out_hi", C.c_int64),
+                ("aux_lo", C.c_int64), ("aux_hi", C.c_int64)]
+
+
 # Exported symbols and their prototypes (kept in sync with include/merit_dev.h;
 # tests/test_capi_symbols.py checks every declared symbol is exported).
 PROTOTYPES = {
@@ -91,6 +96,7 @@ PROTOTYPES = {
     "merit_dev_launch_count": (C.c_int64, []),
     "merit_dev_last_kernel": (C.c_char_p, []),
     "merit_dev_tiled_traffic": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(TrafficReportC)]),
+    "merit_dev_plan_slices": (C.c_int, [C.c_void_p, C.POINTER(HostSliceC), C.c_int64, C.POINTER(C.c_int64)]),
 }
 
 _lib = None

@@ -66,9 +66,16 @@ int64_t ramp_weight_sum(int64_t k, int64_t i) {  // sum of the first i weights
 }
 void split(int64_t n, int64_t k, int64_t i, int64_t& u0, int64_t& u1) {
   const int64_t tot = ramp_weight_sum(k, k);
+  if (n < tot) {  // too few units for the ramp: uniform (no empty slices)
+    u0 = n * i / k;
+    u1 = n * (i + 1) / k;
+    return;
+  }
   u0 = n * ramp_weight_sum(k, i) / tot;
   u1 = n * ramp_weight_sum(k, i + 1) / tot;
 }
+
+}  // namespace
 
 void build_slices(const merit_plan& plan) {
   plan.slices_built = true;
@@ -185,6 +192,8 @@ void build_slices(const merit_plan& plan) {
   plan.slices = std::move(v);
 }
 
+namespace {
+
 merit_status launch_slice(const merit_plan& sub, const void* a, const void* b, void* out, void* aux,
                           void* stream) {
   switch (sub.kernel) {
@@ -297,6 +306,20 @@ merit_status run_host_pipelined(const merit_plan& plan, void* da, void* db, void
 }
 
 }  // namespace merit_dev
+
+extern "C" merit_status merit_dev_plan_slices(const merit_plan* plan, merit_host_slice* out, int64_t cap,
+                                              int64_t* n_slices) {
+  if (!plan || !n_slices || (cap > 0 && !out)) return merit_dev::fail(MERIT_E_INVALID_ARGUMENT, "null argument");
+  std::lock_guard<std::mutex> lock(plan->host_mu);
+  if (!plan->slices_built) merit_dev::build_slices(*plan);
+  *n_slices = static_cast<int64_t>(plan->slices.size());
+  for (int64_t i = 0; i < cap && i < *n_slices; ++i) {
+    const merit_dev::HostSlice& s = plan->slices[i];
+    out[i] = {std::min<int64_t>(s.a_need, plan->info.src_a_bytes), std::min<int64_t>(s.b_need, plan->info.src_b_bytes),
+              s.out_lo, s.out_hi, s.aux_lo, s.aux_hi};
+  }
+  return MERIT_OK;
+}
 
 merit_plan::~merit_plan() {
   for (merit_dev::HostSlice& s : slices) delete s.sub;

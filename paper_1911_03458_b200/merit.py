@@ -394,6 +394,15 @@ class Plan:
         _check(self.lib.merit_dev_run(self.handle, self._ptr(d_src_a), self._ptr(d_src_b),
                                       self._ptr(d_out), self._ptr(d_aux), C.c_void_p(stream or 0)))
 
+    def host_slices(self) -> list:
+        """How run_host pipelines this plan: [{a_need, b_need, out_lo, out_hi,
+        aux_lo, aux_hi}] per slice ([] = unsliced).  Host-only."""
+        n = C.c_int64(0)
+        _check(self.lib.merit_dev_plan_slices(self.handle, None, 0, C.byref(n)))
+        arr = (_capi.HostSliceC * max(1, n.value))()
+        _check(self.lib.merit_dev_plan_slices(self.handle, arr, n.value, C.byref(n)))
+        return [{k: int(getattr(arr[i], k)) for k, _ in _capi.HostSliceC._fields_} for i in range(n.value)]
+
     def tiled_traffic(self, t_p, t_a) -> dict:
         """merit::run_tiled's TrafficReport (engine.hpp:72-80) for the tiling plan
         {t_p, t_a}: validated like TilingPlan::validate, Eq. 6 words per pass."""
