@@ -22,6 +22,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "tc_common.cuh"
@@ -508,6 +509,22 @@ merit_status launch_conv_tma(const merit_plan& plan, const void* a, const void* 
   int grid;
   if (pair) {
     int pairs = num_sms() / 2;
+    // only as many pairs as can be co-resident (TPC / GPC placement): a
+    // surplus pair would run its units as a second wave after everyone else
+    static std::mutex mu;
+    static std::vector<std::pair<size_t, int>> cache;  // smem bytes -> clusters
+    int max_clusters = -1;
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      for (auto& c : cache)
+        if (c.first == smem) max_clusters = c.second;
+      if (max_clusters < 0) {
+        max_clusters = max_active_clusters(kfn, dim3(kThreads), smem, 2u);
+        cache.push_back({smem, max_clusters});
+      }
+    }
+    if (max_clusters > 0 && pairs > max_clusters) pairs = max_clusters;
+    if (A.debug & 4096) fprintf(stderr, "[conv_tma] max active 2-CTA clusters %d, pairs %d\n", max_clusters, pairs);
     if (pairs > A.n_units) pairs = A.n_units;
     grid = 2 * pairs;
   } else {
