@@ -82,6 +82,8 @@ struct SadLaunch {
   uint32_t byt_m, byt_s;      // n / BYT
   int cp_sr, cp_sw;           // copy builder: blockDim.x = cp_sr * Ww + cp_sw
   int by0, by1;               // block-row band [by0, by1) of this launch
+  uint32_t key_mul;           // 65536 as a launch parameter: argmin keys acc * key_mul + d * WX
+                              // stay IMADs (FMA pipe) instead of folding into ALU shift-adds
 };
 
 // n / d for n < 2^31 by multiply-high (Granlund-Montgomery): s = ceil(log2 d),
@@ -241,6 +243,24 @@ __device__ __forceinline__ void issue_tile(const SadLaunch& L, const uint8_t* __
   } else {
     stage_tile<BLK>(L, cur, ref, tile, raw_s, raw, cur_s, curs);
     cp_async_commit();
+  }
+}
+
+// SAD-map rows d < nd of one (block, dx) thread: out[obase + d * WX]
+// (int32, or float for a REAL32 map), streaming stores.
+template <int D>
+__device__ __forceinline__ void sad_store_map(void* out, int out_f32, long long obase, int WX, const uint32_t* acc,
+                                              int nd) {
+  if (out_f32) {
+    float* o = static_cast<float*>(out) + obase;
+#pragma unroll
+    for (int d = 0; d < D; ++d)
+      if (d < nd) __stcs(o + d * WX, static_cast<float>(acc[d]));
+  } else {
+    int32_t* o = static_cast<int32_t*>(out) + obase;
+#pragma unroll
+    for (int d = 0; d < D; ++d)
+      if (d < nd) __stcs(o + d * WX, static_cast<int32_t>(acc[d]));
   }
 }
 
@@ -426,37 +446,23 @@ sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, voi
           uint32_t bn = 0xffffffffu;
           const bool store = p.write_map && by + n < L.by1;
           const long long obase = ((blk_index + n * (long long)p.BX) * p.WY + dy0) * WX + idx;
-          if (nd == D) {  // full group: no per-displacement predicates
+          // keys on the FMA pipe (IMAD), mins on the ALU: the ALU is the
+          // VABSDIFF4 pipe.  Full groups and the one-short last group of an
+          // odd window (C5: 65 = 33 + 32) need no per-displacement predicates.
+          const uint32_t kmul = L.key_mul;
+          if (nd == D) {
 #pragma unroll
-            for (int d = 0; d < D; ++d) bn = min(bn, (acc[n][d] << 16) + static_cast<uint32_t>(d * WX));
-            if (store) {
-              if (p.out_f32) {
-                float* o = static_cast<float*>(out) + obase;
+            for (int d = 0; d < D; ++d) bn = min(bn, acc[n][d] * kmul + static_cast<uint32_t>(d * WX));
+            if (store) sad_store_map<D>(out, p.out_f32, obase, WX, acc[n], D);
+          } else if (WXC != 0 && nd == D - 1) {
 #pragma unroll
-                for (int d = 0; d < D; ++d) __stcs(o + d * WX, static_cast<float>(acc[n][d]));
-              } else {
-                int32_t* o = static_cast<int32_t*>(out) + obase;
-#pragma unroll
-                for (int d = 0; d < D; ++d) __stcs(o + d * WX, static_cast<int32_t>(acc[n][d]));
-              }
-            }
+            for (int d = 0; d < D - 1; ++d) bn = min(bn, acc[n][d] * kmul + static_cast<uint32_t>(d * WX));
+            if (store) sad_store_map<D>(out, p.out_f32, obase, WX, acc[n], D - 1);
           } else {
 #pragma unroll
             for (int d = 0; d < D; ++d)
-              if (d < nd) bn = min(bn, (acc[n][d] << 16) + static_cast<uint32_t>(d * WX));
-            if (store) {
-              if (p.out_f32) {
-                float* o = static_cast<float*>(out) + obase;
-#pragma unroll
-                for (int d = 0; d < D; ++d)
-                  if (d < nd) __stcs(o + d * WX, static_cast<float>(acc[n][d]));
-              } else {
-                int32_t* o = static_cast<int32_t*>(out) + obase;
-#pragma unroll
-                for (int d = 0; d < D; ++d)
-                  if (d < nd) __stcs(o + d * WX, static_cast<int32_t>(acc[n][d]));
-              }
-            }
+              if (d < nd) bn = min(bn, acc[n][d] * kmul + static_cast<uint32_t>(d * WX));
+            if (store) sad_store_map<D>(out, p.out_f32, obase, WX, acc[n], nd);
           }
           best[n] = min(best[n], bn + key0);
         }
@@ -622,6 +628,7 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
                                        static_cast<int>(smem));
   if (e != cudaSuccess) return cuda_check(e, "set_smem_attr(sad)");
   const int threads = (L.items + 31) / 32 * 32;
+  L.key_mul = 65536u;
   L.cp_sr = threads / L.Ww;
   L.cp_sw = threads - L.cp_sr * L.Ww;
   L.n_full_x = p.BX / L.TBX;
