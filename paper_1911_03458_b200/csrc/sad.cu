@@ -82,6 +82,7 @@ struct SadLaunch {
   uint32_t byt_m, byt_s;      // n / BYT
   int cp_sr, cp_sw;           // copy builder: blockDim.x = cp_sr * Ww + cp_sw
   int by0, by1;               // block-row band [by0, by1) of this launch
+  int dbl;                    // double-buffered shifted copies: one barrier per tile (TMA staging)
   uint32_t key_mul;           // 65536 as a launch parameter: argmin keys acc * key_mul + d * WX
                               // stay IMADs (FMA pipe) instead of folding into ALU shift-adds
 };
@@ -278,11 +279,11 @@ sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, voi
   constexpr int BWW = BLK / 4;  // words per block row
   const int raw_words = static_cast<int>(L.raw_buf / 4);
   const int cur_words = static_cast<int>(L.cur_buf / 4);
-  // --- shared memory carve-up: raw[2] | cur[2] | copies[4] | keys | counters | mbarriers
+  // --- shared memory carve-up: raw[2] | cur[2] | copies[4 or 2 x 4] | keys | counters | mbarriers
   uint32_t* raw0 = reinterpret_cast<uint32_t*>(smem_b + ((128u - (smem_u32(smem_b) & 127u)) & 127u));
   uint32_t* cur0 = raw0 + 2 * raw_words;
-  uint32_t* copies = cur0 + 2 * cur_words;
-  uint32_t* keys = copies + 4 * L.CS;       // per block: running argmin key
+  uint32_t* copies0 = cur0 + 2 * cur_words;
+  uint32_t* keys = copies0 + (L.dbl ? 8 : 4) * L.CS;  // per block: running argmin key
   uint32_t* cnt = keys + NBY * L.TBX;       // per block: contributions so far
   const uint32_t bar0 = (smem_u32(cnt + NBY * L.TBX) + 7u) & ~7u;
   const int cpw = L.cur_pitch / 4;  // words per staged current row
@@ -317,13 +318,18 @@ sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, voi
   for (; tile < L.n_tiles; tile += gridDim.x, buf ^= 1) {
     uint32_t* raw = raw0 + buf * raw_words;
     uint32_t* curw = cur0 + buf * cur_words;
+    uint32_t* copies = copies0 + (L.dbl ? buf * 4 * L.CS : 0);
     if (L.tma) {
       sad_mbar_wait(bar0 + 8u * buf, (phase_bits >> buf) & 1u);
       phase_bits ^= 1u << buf;
     } else {
       cp_async_wait_all();
     }
-    __syncthreads();  // raw[buf] landed; previous tile's compute finished
+    // Single copy buffer: the previous tile's compute must finish before it is
+    // rebuilt (and cp.async / byte staging must become visible).  Double
+    // buffer (TMA staging only): copies[buf] was last read by tile - 2, which
+    // every thread finished before the previous iteration's barrier.
+    if (!L.dbl) __syncthreads();
     // tile coordinates
     int t2, tx;
     sad_tile_coords(tile, L.n_full_tiles, L.n_full_x, L.ntx_m, L.ntx_s, t2, tx);
@@ -600,11 +606,15 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
                                  CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
     if (!L.tma) return fail(MERIT_E_CUDA, "cuTensorMapEncodeTiled failed for the SAD frames");
   }
-  const size_t smem =
-      128 + 2ull * L.raw_buf + 2ull * L.cur_buf + 4ull * (4ull * L.CS + 2ull * L.nby * L.TBX) + 8 + 16;
+  const size_t smem_cap = (nt == 512 ? 220 : 110) * 1024;
+  auto smem_for = [&](int ncopy) {
+    return 128 + 2ull * L.raw_buf + 2ull * L.cur_buf + 4ull * (4ull * ncopy * L.CS + 2ull * L.nby * L.TBX) + 8 + 16;
+  };
+  const char* de = getenv("MERIT_SAD_DBL");
+  L.dbl = (L.tma && !(de && de[0] == '0') && smem_for(2) <= smem_cap) ? 1 : 0;
+  const size_t smem = smem_for(L.dbl ? 2 : 1);
   if (L.n_tiles == 0) return MERIT_OK;
-  if (smem > (nt == 512 ? 220 : 110) * 1024)
-    return fail(MERIT_E_UNSUPPORTED_VIEW, "SAD footprint exceeds shared memory");
+  if (smem > smem_cap) return fail(MERIT_E_UNSUPPORTED_VIEW, "SAD footprint exceeds shared memory");
   auto kern = nt == 512 ? sad_kernel<BLK, D, 1, 512, 0> : sad_kernel<BLK, D, 1, 256, 0>;
   if constexpr (BLK == 8) {
     if (L.nby == 2) kern = nt == 512 ? sad_kernel<BLK, D, 2, 512, 0> : sad_kernel<BLK, D, 2, 256, 0>;
