@@ -16,6 +16,7 @@
  *   MERIT_KERNEL_MAXPOOL  window max on CUDA cores (K1)
  *   MERIT_KERNEL_SAD      byte-SIMD block matching + fused argmin (K2)
  *   MERIT_KERNEL_CONV_TC  implicit-GEMM convolution on tcgen05/TMEM (K3)
+ *   MERIT_KERNEL_CORR     displacement correlation on CUDA cores (K4), bit-exact
  *   MERIT_KERNEL_GENERIC  exact device interpreter of any REAL32/FIX16 program
  * There is no CPU execution path: a plan that cannot run on the device fails
  * with a status code (mirroring merit::ErrorCode, tensor.hpp:15-29).
@@ -180,7 +181,8 @@ typedef enum merit_kernel_kind {
   MERIT_KERNEL_GENERIC = 0,
   MERIT_KERNEL_MAXPOOL = 1,
   MERIT_KERNEL_SAD = 2,
-  MERIT_KERNEL_CONV_TC = 3
+  MERIT_KERNEL_CONV_TC = 3,
+  MERIT_KERNEL_CORR = 4
 } merit_kernel_kind;
 
 /* What a plan needs and produces. */

@@ -221,6 +221,10 @@ merit_status merit_dev_run(const merit_plan* plan, const void* d_a, const void* 
       }
       return launch_conv(*plan, in, plan->d_packed_b, d_out, stream);
     }
+    case MERIT_KERNEL_CORR:
+      if (!d_a || !d_b) return fail(MERIT_E_INVALID_ARGUMENT, "null source");
+      return plan->corr_swapped ? launch_corr(*plan, d_b, d_a, d_out, stream)
+                                : launch_corr(*plan, d_a, d_b, d_out, stream);
     default:
       return fail(MERIT_E_INVALID_ARGUMENT, "corrupt plan");
   }

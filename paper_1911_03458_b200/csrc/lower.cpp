@@ -445,6 +445,49 @@ bool lower_gemm(const merit_workload_desc& d, const ViewAffine& fa, const ViewAf
   return finish_conv(d, post, cp);
 }
 
+// Correlation views (workloads.hpp:230-251): A = (a0, p0 + ay, p1 + ax),
+// B = (a0, p0 + p2 + by, p1 + p3 + bx), p = (y, x, dy, dx), a = (c), both
+// REAL32 [C][H][W]; either port may carry the displaced view.  ZERO_PAD (or a
+// view provably inside its source) so the kernel's zero fill is the view's.
+bool lower_corr(const merit_workload_desc& d, const ViewAffine& fa, const ViewAffine& fb, int32_t post,
+                CorrParams& cr, bool& swapped) {
+  if (d.dtype_a != MERIT_F32 || d.dtype_b != MERIT_F32 || d.dtype_out != MERIT_F32) return false;
+  auto try_one = [&](const merit_view_spec& v1, const ViewAffine& f1, const merit_view_spec& v2,
+                     const ViewAffine& f2) -> bool {
+    if (v1.src_rank != 3 || v2.src_rank != 3 || v1.p_rank != 4 || v1.a_rank != 1) return false;
+    const int cy = 0, cx = 1, cdy = 2, cdx = 3, cc = 4;
+    if (!axis_single(f1, 0, cc, 1) || f1.off[0] != 0 || !axis_single(f2, 0, cc, 1) || f2.off[0] != 0)
+      return false;
+    if (!axis_single(f1, 1, cy, 1) || !axis_single(f1, 2, cx, 1)) return false;
+    for (int i = 0; i < 3; ++i)
+      if (f2.coef[i][cy] != (i == 1) || f2.coef[i][cdy] != (i == 1) || f2.coef[i][cx] != (i == 2) ||
+          f2.coef[i][cdx] != (i == 2))
+        return false;
+    if (v1.src_shape[0] != v1.a_shape[0] || v2.src_shape[0] != v1.a_shape[0]) return false;
+    int64_t kshape[kMaxK];
+    for (int j = 0; j < 4; ++j) kshape[j] = v1.p_shape[j];
+    kshape[4] = v1.a_shape[0];
+    if (v1.boundary != MERIT_ZERO_PAD && !view_in_range(f1, kshape)) return false;
+    if (v2.boundary != MERIT_ZERO_PAD && !view_in_range(f2, kshape)) return false;
+    for (int j = 0; j < 4; ++j)
+      if (v1.p_shape[j] > (1 << 20)) return false;
+    if (corr_threads_per_column_quad((int)v1.p_shape[cdy], (int)v1.p_shape[cdx]) == 0) return false;
+    cr.C = (int32_t)v1.a_shape[0];
+    cr.Ha = (int32_t)v1.src_shape[1]; cr.Wa = (int32_t)v1.src_shape[2];
+    cr.Hb = (int32_t)v2.src_shape[1]; cr.Wb = (int32_t)v2.src_shape[2];
+    cr.Ho = (int32_t)v1.p_shape[cy]; cr.Wo = (int32_t)v1.p_shape[cx];
+    cr.DY = (int32_t)v1.p_shape[cdy]; cr.DX = (int32_t)v1.p_shape[cdx];
+    cr.ay = (int32_t)f1.off[1]; cr.ax = (int32_t)f1.off[2];
+    cr.by = (int32_t)f2.off[1]; cr.bx = (int32_t)f2.off[2];
+    cr.post = post;
+    return true;
+  };
+  swapped = false;
+  if (try_one(d.view_a, fa, d.view_b, fb)) return true;
+  swapped = true;
+  return try_one(d.view_b, fb, d.view_a, fa);
+}
+
 bool finish_conv(const merit_workload_desc& d, int32_t post, ConvParams& cp) {
   const bool both_bf16 = cp.in_bf16 && cp.w_bf16;
   cp.split = (both_bf16 || (d.flags & MERIT_FLAG_FAST_BF16)) ? 1 : 3;
@@ -628,6 +671,15 @@ merit_status lower(const merit_workload_desc& d, merit_plan& plan) {
                       cp.dy, cp.dx, cp.oy, cp.ox, cp.in_bf16 ? "bf16" : "f32", cp.split, cp.BN,
                       cp.n_kb, cp.post == POST_RELU ? " relu" : "");
       plan.conv_swapped = swapped;
+    } else if (lower_corr(d, fa, fb, post, plan.corr, swapped)) {
+      plan.kernel = MERIT_KERNEL_CORR;
+      plan.corr_swapped = swapped;
+      const auto& cr = plan.corr;
+      info.algorithmic_ops = (double)info.n_outputs * avol;  // MACs
+      info.algorithmic_bytes = (double)info.src_a_bytes + (double)info.src_b_bytes + (double)info.out_elems * 4;
+      std::snprintf(info.description, sizeof(info.description),
+                    "corr C=%d %dx%d displacements %dx%d off a=%d,%d b=%d,%d exact%s", cr.C, cr.Ho, cr.Wo, cr.DY,
+                    cr.DX, cr.ay, cr.ax, cr.by, cr.bx, cr.post == POST_RELU ? " relu" : "");
     }
   }
   if (plan.kernel != MERIT_KERNEL_SAD && (d.flags & (MERIT_FLAG_ARGMIN | MERIT_FLAG_NO_MAP)))

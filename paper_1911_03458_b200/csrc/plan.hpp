@@ -119,6 +119,18 @@ struct ConvParams {
   int32_t gemm = 0;                                // not NCHW: general kernel only
 };
 
+// K4: displacement correlation (correlation template, workloads.hpp:230-251):
+// out[y][x][dy][dx] = post(sum_c A[c][y + ay][x + ax] * B[c][y + dy + by][x + dx + bx])
+// with the engine's REAL32 MAC (fl(fl(a * b) + r), channel order), ZERO_PAD
+// reads outside either source.  A is the undisplaced view.
+struct CorrParams {
+  int32_t C = 0;
+  int32_t Ha = 0, Wa = 0, Hb = 0, Wb = 0;  // source extents
+  int32_t Ho = 0, Wo = 0, DY = 0, DX = 0;  // p extents
+  int32_t ay = 0, ax = 0, by = 0, bx = 0;  // view offsets
+  int32_t post = POST_ADD_ZERO;
+};
+
 }  // namespace merit_dev
 
 struct merit_plan;
@@ -147,7 +159,9 @@ struct merit_plan {
   merit_dev::MaxpoolParams mp{};
   merit_dev::SadParams sad{};
   merit_dev::ConvParams conv{};
+  merit_dev::CorrParams corr{};
   bool conv_swapped = false;  // input tensor is src_b, weights are src_a
+  bool corr_swapped = false;  // the displaced view is src_a
   // Lazily created device state (plan creation itself needs no GPU).
   mutable std::mutex mu;
   mutable void* d_prog = nullptr;      // ProgramImage copy for K0
@@ -199,6 +213,9 @@ merit_status launch_sad(const merit_plan& plan, const void* a, const void* b, vo
 merit_status launch_conv_pack(const merit_plan& plan, const void* b, void* packed, void* stream);
 merit_status launch_conv(const merit_plan& plan, const void* a, const void* packed_b, void* out,
                          void* stream);
+merit_status launch_corr(const merit_plan& plan, const void* a, const void* b, void* out, void* stream);
+// K4 threads per 4 output columns for a DY x DX window (0: does not fit a CTA).
+int corr_threads_per_column_quad(int DY, int DX);
 
 // Check a CUDA status from C++ host code; returns MERIT_E_CUDA with context.
 merit_status cuda_check(int err, const char* what);

@@ -94,6 +94,7 @@ class Kernel(enum.IntEnum):  # merit_kernel_kind
     MAXPOOL = 1
     SAD = 2
     CONV_TC = 3
+    CORR = 4
 
 
 FLAG_EXACT = 1

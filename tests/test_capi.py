@@ -88,8 +88,14 @@ def test_templates_lower():
     assert kinds["maxpool"] == Kernel.MAXPOOL
     assert kinds["alexnet_conv1"] == Kernel.CONV_TC
     assert kinds["gemm"] == Kernel.CONV_TC  # through operand strides on the general kernel
-    for t in ("correlation", "bilateral", "motion_estimation", "conv2d", "dilated"):
+    assert kinds["correlation"] == Kernel.CORR  # displacement correlation kernel (K4)
+    for t in ("bilateral", "motion_estimation", "conv2d", "dilated"):
         assert kinds[t] == Kernel.GENERIC
+    corr = {"c": 16, "h": 12, "w": 10, "d": 5}
+    assert Plan(W.build_template("correlation", corr)).description.startswith("corr C=16 12x10 displacements 5x5")
+    assert Plan(W.build_template("correlation", corr), FLAG_EXACT).kernel == Kernel.GENERIC
+    # a window wider than one CTA's threads stays on the interpreter
+    assert Plan(W.build_template("correlation", dict(corr, d=200))).kernel == Kernel.GENERIC
     assert Plan(W.build_template("conv2d", {"cin": 4, "cout": 8})).kernel == Kernel.CONV_TC
     assert Plan(W.build_template("relu_fused_conv", {"cin": 4, "cout": 8})).description.endswith("relu")
     # FIX16 always runs the exact interpreter
