@@ -358,6 +358,11 @@ def run_ours(args):
             for i in range(args.steps):
                 case.step(i, sp)
         torch.cuda.synchronize()
+        # one untimed replay: the first launch of an instantiated graph also
+        # uploads it (~1 us per captured node), which is not a step's cost
+        with torch.cuda.stream(stream):
+            graph.replay()
+        torch.cuda.synchronize()
     launches = lib.merit_dev_launch_count() - l0
     kern_name = (lib.merit_dev_last_kernel() or b"").decode()
     e0 = torch.cuda.Event(enable_timing=True)

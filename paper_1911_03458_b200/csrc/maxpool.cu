@@ -216,14 +216,17 @@ __global__ void __launch_bounds__(NT) maxpool3s2_bulk_kernel(const float* __rest
   if (threadIdx.x == 0) {
     for (int i = 0; i < ns; ++i) mp_mbar_init(bar0 + 8u * i, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    // warm L2 with this CTA's first bands while the previous launch drains
-    for (int i = 0; i < ns; ++i) {
+  }
+  // warm L2 with this CTA's first p.pf bands while the previous launch drains
+  // (when the CTAs of consecutive launches fit on an SM together, the whole
+  // input of launch i+1 streams into L2 under launch i's tail)
+  if (threadIdx.x < 32 && !(p.dbg & 4)) {
+    for (int i = threadIdx.x; i < p.pf; i += 32) {
       const int item = first + i * step;
       if (item >= n_items) break;
       int plane, r0, nr;
       rows_of(item, plane, r0, nr);
-      if (!(p.dbg & 4))
-        prefetch_l2(in + ((long long)plane * H + r0) * W, static_cast<uint32_t>(nr) * W * 4u);
+      prefetch_l2(in + ((long long)plane * H + r0) * W, static_cast<uint32_t>(nr) * W * 4u);
     }
   }
   __syncthreads();
@@ -366,6 +369,8 @@ merit_status launch_maxpool(const merit_plan& plan, const void* a, void* out, vo
       MaxpoolParams pp = p;
       if (const char* de = getenv("MERIT_MP_DEBUG")) pp.dbg = atoi(de);
       pp.vec_out = (p.Wo % 4 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+      pp.pf = ns;
+      if (const char* pe = getenv("MERIT_MP_PF")) pp.pf = atoi(pe) < 0 ? (1 << 30) : atoi(pe);
       e = launch_pdl(k, dim3(static_cast<unsigned>(grid)), dim3(128), smem, s, 1, in, o, pp, nband,
                      static_cast<int>(items), ns,
                      rmap);

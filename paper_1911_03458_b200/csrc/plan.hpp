@@ -73,6 +73,7 @@ struct MaxpoolParams {
   int32_t fast = 0;                // 3x3 / stride 2 / offset -1 warp-row path
   int32_t vec_out = 0;             // launch-time: Wo % 4 == 0 and 16-byte aligned output
   int32_t dbg = 0;                 // launch-time timing experiments (MERIT_MP_DEBUG)
+  int32_t pf = 0;                  // launch-time: bands per CTA prefetched into L2 before the PDL wait
 };
 
 // K2: L1 block matching (motion estimation, workloads.hpp:255-279).
