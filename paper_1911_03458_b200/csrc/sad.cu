@@ -389,6 +389,9 @@ sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, voi
                       reinterpret_cast<uint8_t*>(raw0 + (buf ^ 1) * raw_words),
                       smem_u32(cur0 + (buf ^ 1) * cur_words),
                       reinterpret_cast<uint8_t*>(cur0 + (buf ^ 1) * cur_words), bar0 + 8u * (buf ^ 1));
+    // lanes with an item in this tile (warp-converged here; the argmin
+    // folds each block's lanes with a warp reduction before the shared atomics)
+    const unsigned act = __ballot_sync(0xffffffffu, has_item && ib < nb);
     if (has_item && ib < nb) {
       // current blocks (NBY block rows) in registers: rows of cur_pitch bytes,
       // block ib at byte dcur + ib*BLK (dcur % 4 == 0), block row n at row n*BLK
@@ -482,9 +485,16 @@ sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, voi
         for (int n = 0; n < NBY; ++n) {
           if (by + n >= L.by1) break;
           const int slot = n * L.TBX + ib;
-          atomicMin(&keys[slot], best[n]);
+          // the lanes of this warp on the same block fold their keys first
+          // (REDUX): one shared atomic per (warp, block) instead of one per lane
+          const unsigned grp = __match_any_sync(act, slot);
+          const uint32_t wmin = __reduce_min_sync(grp, best[n]);
+          const int lane = threadIdx.x & 31;
+          if (lane != __ffs(grp) - 1) continue;
+          atomicMin(&keys[slot], wmin);
           __threadfence_block();
-          if (atomicAdd(&cnt[slot], 1u) == static_cast<uint32_t>(WX - 1)) {
+          const uint32_t np = static_cast<uint32_t>(__popc(grp));
+          if (atomicAdd(&cnt[slot], np) == static_cast<uint32_t>(WX) - np) {
             __threadfence_block();
             const uint32_t key = atomicExch(&keys[slot], 0xffffffffu);
             cnt[slot] = 0u;
