@@ -83,6 +83,7 @@ struct SadLaunch {
   int cp_sr, cp_sw;           // copy builder: blockDim.x = cp_sr * Ww + cp_sw
   int by0, by1;               // block-row band [by0, by1) of this launch
   int dbl;                    // double-buffered shifted copies: one barrier per tile (TMA staging)
+  int dbg;                    // timing experiments (MERIT_SAD_DBG): 1 skip the copy builder, 2 skip the epilogue
   uint32_t key_mul;           // 65536 as a launch parameter: argmin keys acc * key_mul + d * WX
                               // stay IMADs (FMA pipe) instead of folding into ALU shift-adds
 };
@@ -220,6 +221,23 @@ __device__ __forceinline__ void sad_mbar_wait(uint32_t bar, uint32_t parity) {
       : "memory");
 }
 
+// The TMA part of a tile's staging, issued by the calling thread.
+template <int BLK>
+__device__ __forceinline__ void issue_tile_tma(const SadLaunch& L, const CUtensorMap* ref_map,
+                                               const CUtensorMap* cur_map, int tile, uint32_t raw_s,
+                                               uint32_t cur_s, uint32_t bar) {
+  const SadParams& p = L.p;
+  int t2, tx;
+  sad_tile_coords(tile, L.n_full_tiles, L.n_full_x, L.ntx_m, L.ntx_s, t2, tx);
+  const int pair = static_cast<int>(fast_div(t2, L.byt_m, L.byt_s));
+  const int by = L.by0 + (t2 - pair * L.BYT) * L.nby;
+  const int bx0 = tx * L.TBX;
+  const uint32_t bytes = L.R_box * L.rw * 4 + L.nby * BLK * L.cur_pitch;
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+  sad_tma_3d(raw_s, ref_map, floor16(bx0 * BLK + p.ox), by * BLK + p.oy, pair, bar);
+  sad_tma_3d(cur_s, cur_map, floor16(bx0 * BLK + p.cx), by * BLK + p.cy, pair, bar);
+}
+
 // One tile's staging: TMA (one 3-D box for the reference window, one for the
 // current blocks, completion on the buffer's mbarrier; zero fill outside the
 // frame = ZERO_PAD) or the cp.async / byte paths.
@@ -229,18 +247,7 @@ __device__ __forceinline__ void issue_tile(const SadLaunch& L, const uint8_t* __
                                            const CUtensorMap* cur_map, int tile, uint32_t raw_s, uint8_t* raw,
                                            uint32_t cur_s, uint8_t* curs, uint32_t bar) {
   if (L.tma) {
-    if (threadIdx.x == 0) {
-      const SadParams& p = L.p;
-      int t2, tx;
-      sad_tile_coords(tile, L.n_full_tiles, L.n_full_x, L.ntx_m, L.ntx_s, t2, tx);
-      const int pair = static_cast<int>(fast_div(t2, L.byt_m, L.byt_s));
-      const int by = L.by0 + (t2 - pair * L.BYT) * L.nby;
-      const int bx0 = tx * L.TBX;
-      const uint32_t bytes = L.R_box * L.rw * 4 + L.nby * BLK * L.cur_pitch;
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-      sad_tma_3d(raw_s, ref_map, floor16(bx0 * BLK + p.ox), by * BLK + p.oy, pair, bar);
-      sad_tma_3d(cur_s, cur_map, floor16(bx0 * BLK + p.cx), by * BLK + p.cy, pair, bar);
-    }
+    if (threadIdx.x == 0) issue_tile_tma<BLK>(L, ref_map, cur_map, tile, raw_s, cur_s, bar);
   } else {
     stage_tile<BLK>(L, cur, ref, tile, raw_s, raw, cur_s, curs);
     cp_async_commit();
@@ -268,15 +275,219 @@ __device__ __forceinline__ void sad_store_map(void* out, int out_f32, long long 
 // WXC: the displacement-window width as a compile-time constant (0 = runtime
 // p.WX).  A constant width turns the per-displacement key and SAD-map store
 // offsets into immediates (the epilogue was ~8% of the issued instructions).
+// The four byte-shifted word copies of a tile's staged reference window:
+// copy_s[r][w] = window bytes (4w+s .. 4w+s+3), one (row, word) per thread per
+// step over the flattened R x Ww range, starting at (cp_r0, cp_w0).
+template <int BLK>
+__device__ __forceinline__ void sad_build_copies(const SadLaunch& L, int tile, const uint32_t* raw,
+                                                 uint32_t* copies, int cp_r0, int cp_w0) {
+  const SadParams& p = L.p;
+  int t2, tx;
+  sad_tile_coords(tile, L.n_full_tiles, L.n_full_x, L.ntx_m, L.ntx_s, t2, tx);
+  const int bx0 = tx * L.TBX;
+  // leading bytes of the staged rows before the window (TMA boxes start at
+  // a 16-byte multiple)
+  const int dref = L.tma ? (bx0 * BLK + p.ox) - floor16(bx0 * BLK + p.ox) : 0;
+  const uint32_t cs4 = static_cast<uint32_t>(L.CS) * 4u;
+  const uint32_t raw_s = smem_u32(raw) + static_cast<uint32_t>(dref >> 2) * 4u;
+  const uint32_t cop_s = smem_u32(copies);
+  const int dr = dref & 3;
+  int r = (L.dbg & 1) ? L.R : cp_r0, w = cp_w0;
+  while (r < L.R) {
+    const uint32_t ra = raw_s + static_cast<uint32_t>(r * L.rw + w) * 4u;
+    const uint32_t ca = cop_s + static_cast<uint32_t>(r * L.Ww + w) * 4u;
+    uint32_t a0, a1, a2;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(a0) : "r"(ra));
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(a1) : "r"(ra + 4));
+    uint32_t c0, c1, c2, c3;
+    if (dr == 0) {
+      c0 = a0;
+      c1 = __byte_perm(a0, a1, 0x4321);
+      c2 = __byte_perm(a0, a1, 0x5432);
+      c3 = __byte_perm(a0, a1, 0x6543);
+    } else {
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(a2) : "r"(ra + 8));
+      c0 = __funnelshift_r(a0, a1, 8 * dr);
+      c1 = dr + 1 < 4 ? __funnelshift_r(a0, a1, 8 * (dr + 1)) : a1;
+      c2 = dr + 2 < 4 ? __funnelshift_r(a0, a1, 8 * (dr + 2)) : __funnelshift_r(a1, a2, 8 * (dr - 2));
+      c3 = __funnelshift_r(a1, a2, 8 * (dr - 1));
+    }
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(ca), "r"(c0) : "memory");
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(ca + cs4), "r"(c1) : "memory");
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(ca + 2 * cs4), "r"(c2) : "memory");
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(ca + 3 * cs4), "r"(c3) : "memory");
+    w += L.cp_sw;
+    r += L.cp_sr;
+    if (w >= L.Ww) {
+      w -= L.Ww;
+      ++r;
+    }
+  }
+}
+
+// One tile's matching for this thread's (block, dx) item: the current
+// block(s) into registers from the staged rows, `after_cw()` (called by every
+// thread of the CTA once the staged current rows are no longer needed), the
+// SAD accumulation over the shifted copies, then the SAD-map stores and the
+// argmin fold into keys / cnt.
+template <int BLK, int D, int NBY, int WXC, typename AfterCw>
+__device__ __forceinline__ void sad_tile_work(const SadLaunch& L, void* __restrict__ out, int32_t* __restrict__ aux,
+                                              int tile, const uint32_t* curw, const uint32_t* copies,
+                                              uint32_t* keys, uint32_t* cnt, AfterCw after_cw) {
+  const SadParams& p = L.p;
+  const int WX = WXC ? WXC : p.WX;
+  constexpr int BWW = BLK / 4;  // words per block row
+  const int cpw = L.cur_pitch / 4;  // words per staged current row
+  const int item = threadIdx.x;
+  const int ib = item / WX;
+  const int idx = item - ib * WX;
+  const bool has_item = item < L.items;
+  int t2, tx;
+  sad_tile_coords(tile, L.n_full_tiles, L.n_full_x, L.ntx_m, L.ntx_s, t2, tx);
+  const int pair_i = static_cast<int>(fast_div(t2, L.byt_m, L.byt_s));
+  const int by = L.by0 + (t2 - pair_i * L.BYT) * NBY;  // first block row of the tile
+  const long long pair = pair_i;
+  const int bx0 = tx * L.TBX;
+  const int nb = min(L.TBX, p.BX - bx0);
+  const int dcur = L.tma ? (bx0 * BLK + p.cx) - floor16(bx0 * BLK + p.cx) : 0;
+  // lanes with an item in this tile (warp-converged here; the argmin
+  // folds each block's lanes with a warp reduction before the shared atomics)
+  const unsigned act = __ballot_sync(0xffffffffu, has_item && ib < nb);
+  // current blocks (NBY block rows) in registers: rows of cur_pitch bytes,
+  // block ib at byte dcur + ib*BLK (dcur % 4 == 0), block row n at row n*BLK
+  uint32_t cw[NBY][BLK][BWW];
+  if (has_item && ib < nb) {
+    const uint32_t* cb = curw + (dcur >> 2) + ib * BWW;
+    if (BWW == 4 && ((dcur & 15) == 0)) {
+#pragma unroll
+      for (int n = 0; n < NBY; ++n)
+#pragma unroll
+        for (int i = 0; i < BLK; ++i) {
+          const uint4 q4 = *reinterpret_cast<const uint4*>(cb + (n * BLK + i) * cpw);
+          cw[n][i][0] = q4.x; cw[n][i][1 % BWW] = q4.y; cw[n][i][2 % BWW] = q4.z; cw[n][i][3 % BWW] = q4.w;
+        }
+    } else {
+#pragma unroll
+      for (int n = 0; n < NBY; ++n)
+#pragma unroll
+        for (int i = 0; i < BLK; ++i)
+#pragma unroll
+          for (int j = 0; j < BWW; ++j) cw[n][i][j] = cb[(n * BLK + i) * cpw + j];
+    }
+  }
+  after_cw();
+  if (!(has_item && ib < nb)) return;
+  const int col = ib * BLK + idx;  // byte column in the staged window
+  const uint32_t* cp0 = copies + (col & 3) * L.CS + (col >> 2);
+  const long long blk_index = (pair * p.BY + by) * (long long)p.BX + bx0 + ib;
+  uint32_t best[NBY];
+#pragma unroll
+  for (int n = 0; n < NBY; ++n) best[n] = 0xffffffffu;
+  for (int ig = 0; ig < L.G; ++ig) {
+    const uint32_t* cp = cp0 + ig * D * L.Ww;
+    uint32_t acc[NBY][D];
+#pragma unroll
+    for (int n = 0; n < NBY; ++n)
+#pragma unroll
+      for (int d = 0; d < D; ++d) acc[n][d] = 0;
+    // block row n at displacement d reads staged row r = n*BLK + d + i:
+    // every loaded reference word feeds all NBY block rows
+#pragma unroll
+    for (int r = 0; r < D + NBY * BLK - 1; ++r) {
+      uint32_t rwv[BWW];
+#pragma unroll
+      for (int j = 0; j < BWW; ++j) rwv[j] = cp[j];
+      cp += L.Ww;
+#pragma unroll
+      for (int n = 0; n < NBY; ++n)
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          const int i = r - d - n * BLK;
+          if (i >= 0 && i < BLK) {
+#pragma unroll
+            for (int j = 0; j < BWW; ++j) acc[n][d] = vabsdiff4_acc(cw[n][i][j], rwv[j], acc[n][d]);
+          }
+        }
+    }
+    if (L.dbg & 2) {
+      uint32_t x = 0;
+#pragma unroll
+      for (int n = 0; n < NBY; ++n)
+#pragma unroll
+        for (int d = 0; d < D; ++d) x ^= acc[n][d];
+      best[0] ^= x;
+      continue;
+    }
+    const int dy0 = ig * D;
+    const int nd = min(D, p.WY - dy0);
+    // argmin key = sad << 16 | (dy * WX + dx): the per-thread part
+    // dy0 * WX + idx is added after the min (it does not change the order)
+    const uint32_t key0 = static_cast<uint32_t>(dy0 * WX + idx);
+#pragma unroll
+    for (int n = 0; n < NBY; ++n) {
+      uint32_t bn = 0xffffffffu;
+      const bool store = p.write_map && by + n < L.by1;
+      const long long obase = ((blk_index + n * (long long)p.BX) * p.WY + dy0) * WX + idx;
+      // keys on the FMA pipe (IMAD), mins on the ALU: the ALU is the
+      // VABSDIFF4 pipe.  Full groups and the one-short last group of an
+      // odd window (C5: 65 = 33 + 32) need no per-displacement predicates.
+      const uint32_t kmul = L.key_mul;
+      if (nd == D) {
+#pragma unroll
+        for (int d = 0; d < D; ++d) bn = min(bn, acc[n][d] * kmul + static_cast<uint32_t>(d * WX));
+        if (store) sad_store_map<D>(out, p.out_f32, obase, WX, acc[n], D);
+      } else if (WXC != 0 && nd == D - 1) {
+#pragma unroll
+        for (int d = 0; d < D - 1; ++d) bn = min(bn, acc[n][d] * kmul + static_cast<uint32_t>(d * WX));
+        if (store) sad_store_map<D>(out, p.out_f32, obase, WX, acc[n], D - 1);
+      } else {
+#pragma unroll
+        for (int d = 0; d < D; ++d)
+          if (d < nd) bn = min(bn, acc[n][d] * kmul + static_cast<uint32_t>(d * WX));
+        if (store) sad_store_map<D>(out, p.out_f32, obase, WX, acc[n], nd);
+      }
+      best[n] = min(best[n], bn + key0);
+    }
+  }
+  if ((L.dbg & 2) && best[0] == 0x12345u) aux[0] = 1;  // keep the work live
+  if (p.argmin && !(L.dbg & 2)) {
+    // Barrier-free per-block argmin: every (block, dx) thread folds its key
+    // in; the thread that arrives last writes the record and re-arms the
+    // slot for a later tile.
+#pragma unroll
+    for (int n = 0; n < NBY; ++n) {
+      if (by + n >= L.by1) break;
+      const int slot = n * L.TBX + ib;
+      // the lanes of this warp on the same block fold their keys first
+      // (REDUX): one shared atomic per (warp, block) instead of one per lane
+      const unsigned grp = __match_any_sync(act, slot);
+      const uint32_t wmin = __reduce_min_sync(grp, best[n]);
+      const int lane = threadIdx.x & 31;
+      if (lane != __ffs(grp) - 1) continue;
+      atomicMin(&keys[slot], wmin);
+      __threadfence_block();
+      const uint32_t np = static_cast<uint32_t>(__popc(grp));
+      if (atomicAdd(&cnt[slot], np) == static_cast<uint32_t>(WX) - np) {
+        __threadfence_block();
+        const uint32_t key = atomicExch(&keys[slot], 0xffffffffu);
+        cnt[slot] = 0u;
+        const int k = static_cast<int>(key & 0xffffu);
+        const int dy = k / WX, dx = k - (k / WX) * WX;
+        int32_t* a = aux + (blk_index + n * (long long)p.BX) * 3;
+        a[0] = dy + p.oy - p.cy;
+        a[1] = dx + p.ox - p.cx;
+        a[2] = static_cast<int32_t>(key >> 16);
+      }
+    }
+  }
+}
+
 template <int BLK, int D, int NBY, int NT, int WXC>
 __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1)
 sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, void* __restrict__ out,
            int32_t* __restrict__ aux, SadLaunch L, const __grid_constant__ CUtensorMap ref_map,
            const __grid_constant__ CUtensorMap cur_map) {
   extern __shared__ __align__(128) uint8_t smem_b[];
-  const SadParams& p = L.p;
-  const int WX = WXC ? WXC : p.WX;
-  constexpr int BWW = BLK / 4;  // words per block row
   const int raw_words = static_cast<int>(L.raw_buf / 4);
   const int cur_words = static_cast<int>(L.cur_buf / 4);
   // --- shared memory carve-up: raw[2] | cur[2] | copies[4 or 2 x 4] | keys | counters | mbarriers
@@ -286,13 +497,6 @@ sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, voi
   uint32_t* keys = copies0 + (L.dbl ? 8 : 4) * L.CS;  // per block: running argmin key
   uint32_t* cnt = keys + NBY * L.TBX;       // per block: contributions so far
   const uint32_t bar0 = (smem_u32(cnt + NBY * L.TBX) + 7u) & ~7u;
-  const int cpw = L.cur_pitch / 4;  // words per staged current row
-
-  // per-thread item: (block, dx); the thread walks all dy groups
-  const int item = threadIdx.x;
-  const int ib = item / WX;
-  const int idx = item - ib * WX;
-  const bool has_item = item < L.items;
   // copy-builder start (row, word) of this thread in the flattened R x Ww walk
   const int cp_r0 = static_cast<int>(threadIdx.x) / L.Ww;
   const int cp_w0 = static_cast<int>(threadIdx.x) - cp_r0 * L.Ww;
@@ -330,57 +534,7 @@ sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, voi
     // buffer (TMA staging only): copies[buf] was last read by tile - 2, which
     // every thread finished before the previous iteration's barrier.
     if (!L.dbl) __syncthreads();
-    // tile coordinates
-    int t2, tx;
-    sad_tile_coords(tile, L.n_full_tiles, L.n_full_x, L.ntx_m, L.ntx_s, t2, tx);
-    const int pair_i = static_cast<int>(fast_div(t2, L.byt_m, L.byt_s));
-    const int by = L.by0 + (t2 - pair_i * L.BYT) * NBY;  // first block row of the tile
-    const long long pair = pair_i;
-    const int bx0 = tx * L.TBX;
-    const int nb = min(L.TBX, p.BX - bx0);
-    // leading bytes of the staged rows before the window (TMA boxes start at
-    // a 16-byte multiple)
-    const int dref = L.tma ? (bx0 * BLK + p.ox) - floor16(bx0 * BLK + p.ox) : 0;
-    const int dcur = L.tma ? (bx0 * BLK + p.cx) - floor16(bx0 * BLK + p.cx) : 0;
-    // four byte-shifted word copies: copy_s[r][w] = window bytes (4w+s .. 4w+s+3),
-    // one (row, word) per thread per step over the flattened R x Ww range
-    {
-      const uint32_t cs4 = static_cast<uint32_t>(L.CS) * 4u;
-      const uint32_t raw_s = smem_u32(raw) + static_cast<uint32_t>(dref >> 2) * 4u;
-      const uint32_t cop_s = smem_u32(copies);
-      const int dr = dref & 3;
-      int r = cp_r0, w = cp_w0;
-      while (r < L.R) {
-        const uint32_t ra = raw_s + static_cast<uint32_t>(r * L.rw + w) * 4u;
-        const uint32_t ca = cop_s + static_cast<uint32_t>(r * L.Ww + w) * 4u;
-        uint32_t a0, a1, a2;
-        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(a0) : "r"(ra));
-        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(a1) : "r"(ra + 4));
-        uint32_t c0, c1, c2, c3;
-        if (dr == 0) {
-          c0 = a0;
-          c1 = __byte_perm(a0, a1, 0x4321);
-          c2 = __byte_perm(a0, a1, 0x5432);
-          c3 = __byte_perm(a0, a1, 0x6543);
-        } else {
-          asm volatile("ld.shared.u32 %0, [%1];" : "=r"(a2) : "r"(ra + 8));
-          c0 = __funnelshift_r(a0, a1, 8 * dr);
-          c1 = dr + 1 < 4 ? __funnelshift_r(a0, a1, 8 * (dr + 1)) : a1;
-          c2 = dr + 2 < 4 ? __funnelshift_r(a0, a1, 8 * (dr + 2)) : __funnelshift_r(a1, a2, 8 * (dr - 2));
-          c3 = __funnelshift_r(a1, a2, 8 * (dr - 1));
-        }
-        asm volatile("st.shared.u32 [%0], %1;" ::"r"(ca), "r"(c0) : "memory");
-        asm volatile("st.shared.u32 [%0], %1;" ::"r"(ca + cs4), "r"(c1) : "memory");
-        asm volatile("st.shared.u32 [%0], %1;" ::"r"(ca + 2 * cs4), "r"(c2) : "memory");
-        asm volatile("st.shared.u32 [%0], %1;" ::"r"(ca + 3 * cs4), "r"(c3) : "memory");
-        w += L.cp_sw;
-        r += L.cp_sr;
-        if (w >= L.Ww) {
-          w -= L.Ww;
-          ++r;
-        }
-      }
-    }
+    sad_build_copies<BLK>(L, tile, raw, copies, cp_r0, cp_w0);
     __syncthreads();
     // prefetch the next tile into the other buffer while this one computes
     const int next = tile + gridDim.x;
@@ -389,128 +543,107 @@ sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, voi
                       reinterpret_cast<uint8_t*>(raw0 + (buf ^ 1) * raw_words),
                       smem_u32(cur0 + (buf ^ 1) * cur_words),
                       reinterpret_cast<uint8_t*>(cur0 + (buf ^ 1) * cur_words), bar0 + 8u * (buf ^ 1));
-    // lanes with an item in this tile (warp-converged here; the argmin
-    // folds each block's lanes with a warp reduction before the shared atomics)
-    const unsigned act = __ballot_sync(0xffffffffu, has_item && ib < nb);
-    if (has_item && ib < nb) {
-      // current blocks (NBY block rows) in registers: rows of cur_pitch bytes,
-      // block ib at byte dcur + ib*BLK (dcur % 4 == 0), block row n at row n*BLK
-      uint32_t cw[NBY][BLK][BWW];
-      const uint32_t* cb = curw + (dcur >> 2) + ib * BWW;
-      if (BWW == 4 && ((dcur & 15) == 0)) {
-#pragma unroll
-        for (int n = 0; n < NBY; ++n)
-#pragma unroll
-          for (int i = 0; i < BLK; ++i) {
-            const uint4 q4 = *reinterpret_cast<const uint4*>(cb + (n * BLK + i) * cpw);
-            cw[n][i][0] = q4.x; cw[n][i][1 % BWW] = q4.y; cw[n][i][2 % BWW] = q4.z; cw[n][i][3 % BWW] = q4.w;
-          }
-      } else {
-#pragma unroll
-        for (int n = 0; n < NBY; ++n)
-#pragma unroll
-          for (int i = 0; i < BLK; ++i)
-#pragma unroll
-            for (int j = 0; j < BWW; ++j) cw[n][i][j] = cb[(n * BLK + i) * cpw + j];
-      }
-      const int col = ib * BLK + idx;  // byte column in the staged window
-      const uint32_t* cp0 = copies + (col & 3) * L.CS + (col >> 2);
-      const long long blk_index = (pair * p.BY + by) * (long long)p.BX + bx0 + ib;
-      uint32_t best[NBY];
-#pragma unroll
-      for (int n = 0; n < NBY; ++n) best[n] = 0xffffffffu;
-      for (int ig = 0; ig < L.G; ++ig) {
-        const uint32_t* cp = cp0 + ig * D * L.Ww;
-        uint32_t acc[NBY][D];
-#pragma unroll
-        for (int n = 0; n < NBY; ++n)
-#pragma unroll
-          for (int d = 0; d < D; ++d) acc[n][d] = 0;
-        // block row n at displacement d reads staged row r = n*BLK + d + i:
-        // every loaded reference word feeds all NBY block rows
-#pragma unroll
-        for (int r = 0; r < D + NBY * BLK - 1; ++r) {
-          uint32_t rwv[BWW];
-#pragma unroll
-          for (int j = 0; j < BWW; ++j) rwv[j] = cp[j];
-          cp += L.Ww;
-#pragma unroll
-          for (int n = 0; n < NBY; ++n)
-#pragma unroll
-            for (int d = 0; d < D; ++d) {
-              const int i = r - d - n * BLK;
-              if (i >= 0 && i < BLK) {
-#pragma unroll
-                for (int j = 0; j < BWW; ++j) acc[n][d] = vabsdiff4_acc(cw[n][i][j], rwv[j], acc[n][d]);
-              }
-            }
-        }
-        const int dy0 = ig * D;
-        const int nd = min(D, p.WY - dy0);
-        // argmin key = sad << 16 | (dy * WX + dx): the per-thread part
-        // dy0 * WX + idx is added after the min (it does not change the order)
-        const uint32_t key0 = static_cast<uint32_t>(dy0 * WX + idx);
-#pragma unroll
-        for (int n = 0; n < NBY; ++n) {
-          uint32_t bn = 0xffffffffu;
-          const bool store = p.write_map && by + n < L.by1;
-          const long long obase = ((blk_index + n * (long long)p.BX) * p.WY + dy0) * WX + idx;
-          // keys on the FMA pipe (IMAD), mins on the ALU: the ALU is the
-          // VABSDIFF4 pipe.  Full groups and the one-short last group of an
-          // odd window (C5: 65 = 33 + 32) need no per-displacement predicates.
-          const uint32_t kmul = L.key_mul;
-          if (nd == D) {
-#pragma unroll
-            for (int d = 0; d < D; ++d) bn = min(bn, acc[n][d] * kmul + static_cast<uint32_t>(d * WX));
-            if (store) sad_store_map<D>(out, p.out_f32, obase, WX, acc[n], D);
-          } else if (WXC != 0 && nd == D - 1) {
-#pragma unroll
-            for (int d = 0; d < D - 1; ++d) bn = min(bn, acc[n][d] * kmul + static_cast<uint32_t>(d * WX));
-            if (store) sad_store_map<D>(out, p.out_f32, obase, WX, acc[n], D - 1);
-          } else {
-#pragma unroll
-            for (int d = 0; d < D; ++d)
-              if (d < nd) bn = min(bn, acc[n][d] * kmul + static_cast<uint32_t>(d * WX));
-            if (store) sad_store_map<D>(out, p.out_f32, obase, WX, acc[n], nd);
-          }
-          best[n] = min(best[n], bn + key0);
-        }
-      }
-      if (p.argmin) {
-        // Barrier-free per-block argmin: every (block, dx) thread folds its key
-        // in; the thread that arrives last writes the record and re-arms the
-        // slot for the next tile (the next tile's atomics follow the barrier at
-        // the top of the loop).
-#pragma unroll
-        for (int n = 0; n < NBY; ++n) {
-          if (by + n >= L.by1) break;
-          const int slot = n * L.TBX + ib;
-          // the lanes of this warp on the same block fold their keys first
-          // (REDUX): one shared atomic per (warp, block) instead of one per lane
-          const unsigned grp = __match_any_sync(act, slot);
-          const uint32_t wmin = __reduce_min_sync(grp, best[n]);
-          const int lane = threadIdx.x & 31;
-          if (lane != __ffs(grp) - 1) continue;
-          atomicMin(&keys[slot], wmin);
-          __threadfence_block();
-          const uint32_t np = static_cast<uint32_t>(__popc(grp));
-          if (atomicAdd(&cnt[slot], np) == static_cast<uint32_t>(WX) - np) {
-            __threadfence_block();
-            const uint32_t key = atomicExch(&keys[slot], 0xffffffffu);
-            cnt[slot] = 0u;
-            const int k = static_cast<int>(key & 0xffffu);
-            const int dy = k / WX, dx = k - (k / WX) * WX;
-            int32_t* a = aux + (blk_index + n * (long long)p.BX) * 3;
-            a[0] = dy + p.oy - p.cy;
-            a[1] = dx + p.ox - p.cx;
-            a[2] = static_cast<int32_t>(key >> 16);
-          }
-        }
-      }
-    }
+    sad_tile_work<BLK, D, NBY, WXC>(L, out, aux, tile, curw, copies, keys, cnt, [] {});
   }
   cp_async_wait_all();
 }
+
+// Barrier-free variant for TMA staging: the warps of a CTA run their tiles
+// without ever meeting at a CTA barrier in steady state.  Staging buffers
+// (raw window + current rows) are double-buffered and the shifted copies
+// triple-buffered; after finishing tile k a warp builds its share of tile
+// k + 2's copies, then starts tile k + 1, whose copies every warp finished
+// one tile earlier.  So the copy building, the epilogue and the staging
+// waits of one warp overlap the VABSDIFF4 streams of the others instead of
+// being aligned across the SM by tile barriers.
+//   tma[b]  (b = k % 2): TMA of tile k landed in raw[b] / cur[b]
+//   full[c] (c = k % 3): all threads built their share of copies[c] for tile k
+//   done[c]:             all threads finished tile k's matching (copies[c] free)
+// The last warp to load its current blocks of tile k issues tile k + 2's TMA
+// into raw / cur[b] (every build from raw[b] for tile k came before full[c]).
+template <int BLK, int D, int NBY, int NT, int WXC>
+__global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1)
+sad_async_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, void* __restrict__ out,
+                 int32_t* __restrict__ aux, SadLaunch L, const __grid_constant__ CUtensorMap ref_map,
+                 const __grid_constant__ CUtensorMap cur_map) {
+  extern __shared__ __align__(128) uint8_t smem_b[];
+  const int raw_words = static_cast<int>(L.raw_buf / 4);
+  const int cur_words = static_cast<int>(L.cur_buf / 4);
+  // --- carve-up: raw[2] | cur[2] | copies[3 x 4] | keys[2] | cnt[2] | ctr[2] | mbarriers tma[2] full[3] done[3]
+  uint32_t* raw0 = reinterpret_cast<uint32_t*>(smem_b + ((128u - (smem_u32(smem_b) & 127u)) & 127u));
+  uint32_t* cur0 = raw0 + 2 * raw_words;
+  uint32_t* copies0 = cur0 + 2 * cur_words;
+  const int nslot = NBY * L.TBX;
+  uint32_t* keys0 = copies0 + 12 * L.CS;
+  uint32_t* cnt0 = keys0 + 2 * nslot;
+  uint32_t* ctr = cnt0 + 2 * nslot;
+  const uint32_t bar_tma = (smem_u32(ctr + 2) + 7u) & ~7u;
+  const uint32_t bar_full = bar_tma + 16u;
+  const uint32_t bar_done = bar_full + 24u;
+  const int cp_r0 = static_cast<int>(threadIdx.x) / L.Ww;
+  const int cp_w0 = static_cast<int>(threadIdx.x) - cp_r0 * L.Ww;
+  const int nwarps = static_cast<int>(blockDim.x) >> 5;
+
+  if (threadIdx.x < 2 * nslot) {
+    keys0[threadIdx.x] = 0xffffffffu;
+    cnt0[threadIdx.x] = 0u;
+  }
+  if (threadIdx.x < 2) ctr[threadIdx.x] = 0u;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_tma + 8u * i) : "memory");
+    for (int i = 0; i < 3; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar_full + 8u * i), "r"(blockDim.x) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar_done + 8u * i), "r"(blockDim.x) : "memory");
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  pdl_launch_dependents();
+  pdl_wait();  // first global access follows
+  const int first = blockIdx.x, step = gridDim.x;
+  const int nk = first < L.n_tiles ? (L.n_tiles - 1 - first) / step + 1 : 0;  // tiles of this CTA
+  auto tile_of = [&](int k) { return first + k * step; };
+  auto issue = [&](int k) {  // one thread: TMA of tile k into buffer k % 2
+    const int b = k & 1;
+    issue_tile_tma<BLK>(L, &ref_map, &cur_map, tile_of(k), smem_u32(raw0 + b * raw_words),
+                        smem_u32(cur0 + b * cur_words), bar_tma + 8u * b);
+  };
+  auto arrive = [](uint32_t bar) { asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory"); };
+  auto build = [&](int k) {  // this thread's share of tile k's copies
+    const int b = k & 1, c = k % 3;
+    if (k >= 3) sad_mbar_wait(bar_done + 8u * c, static_cast<uint32_t>((k - 3) / 3) & 1u);  // copies[c] free
+    sad_mbar_wait(bar_tma + 8u * b, static_cast<uint32_t>(k >> 1) & 1u);
+    sad_build_copies<BLK>(L, tile_of(k), raw0 + b * raw_words, copies0 + c * 4 * L.CS, cp_r0, cp_w0);
+    arrive(bar_full + 8u * c);
+  };
+  if (threadIdx.x == 0) {
+    if (nk > 0) issue(0);
+    if (nk > 1) issue(1);
+  }
+  if (nk > 0) build(0);
+  if (nk > 1) build(1);
+  for (int k = 0; k < nk; ++k) {
+    const int b = k & 1, c = k % 3;
+    sad_mbar_wait(bar_full + 8u * c, static_cast<uint32_t>(k / 3) & 1u);
+    sad_tile_work<BLK, D, NBY, WXC>(
+        L, out, aux, tile_of(k), cur0 + b * cur_words, copies0 + c * 4 * L.CS, keys0 + b * nslot,
+        cnt0 + b * nslot, [&] {
+          // the last warp done with cur[b] for tile k refills buffer b with tile k + 2
+          __syncwarp();
+          if ((threadIdx.x & 31) == 0) {
+            __threadfence_block();
+            if (atomicAdd(&ctr[b], 1u) == static_cast<uint32_t>(nwarps - 1)) {
+              ctr[b] = 0u;
+              __threadfence_block();
+              if (k + 2 < nk) issue(k + 2);
+            }
+          }
+        });
+    arrive(bar_done + 8u * c);
+    if (k + 2 < nk) build(k + 2);
+  }
+}
+
 
 template <int BLK, int D>
 merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t* ref, void* out,
@@ -620,11 +753,18 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
   auto smem_for = [&](int ncopy) {
     return 128 + 2ull * L.raw_buf + 2ull * L.cur_buf + 4ull * (4ull * ncopy * L.CS + 2ull * L.nby * L.TBX) + 8 + 16;
   };
+  L.dbg = 0;
+  if (const char* ge = getenv("MERIT_SAD_DBG")) L.dbg = atoi(ge);
   const char* de = getenv("MERIT_SAD_DBL");
   L.dbl = (L.tma && !(de && de[0] == '0') && smem_for(2) <= smem_cap) ? 1 : 0;
   const size_t smem = smem_for(L.dbl ? 2 : 1);
   if (L.n_tiles == 0) return MERIT_OK;
   if (smem > smem_cap) return fail(MERIT_E_UNSUPPORTED_VIEW, "SAD footprint exceeds shared memory");
+  // barrier-free variant (TMA staging): two staging buffers, three copy buffers
+  const size_t smem_async = 128 + 2ull * L.raw_buf + 2ull * L.cur_buf +
+                            4ull * (12ull * L.CS + 4ull * L.nby * L.TBX + 2) + 8 + 64;
+  const char* ae = getenv("MERIT_SAD_ASYNC");
+  const bool use_async = L.tma && !(ae && ae[0] == '0') && smem_async <= smem_cap;
   auto kern = nt == 512 ? sad_kernel<BLK, D, 1, 512, 0> : sad_kernel<BLK, D, 1, 256, 0>;
   if constexpr (BLK == 8) {
     if (L.nby == 2) kern = nt == 512 ? sad_kernel<BLK, D, 2, 512, 0> : sad_kernel<BLK, D, 2, 256, 0>;
@@ -644,8 +784,32 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
       if (L.nby == 2) kern = nt == 512 ? sad_kernel<BLK, D, 2, 512, 0> : sad_kernel<BLK, D, 2, 256, 0>;
     }
   }
+  if (use_async) {
+    // same template arguments, barrier-free kernel
+#define MERIT_SAD_ASYNC_OF(B, DD, NB, T, W) \
+  if (kern == sad_kernel<B, DD, NB, T, W>) kern = sad_async_kernel<B, DD, NB, T, W>;
+    MERIT_SAD_ASYNC_OF(BLK, D, 1, 512, 0)
+    MERIT_SAD_ASYNC_OF(BLK, D, 1, 256, 0)
+    if constexpr (BLK == 8) {
+      MERIT_SAD_ASYNC_OF(BLK, D, 2, 512, 0)
+      MERIT_SAD_ASYNC_OF(BLK, D, 2, 256, 0)
+    }
+    if constexpr (D == 33) {
+      if constexpr (BLK == 16) {
+        MERIT_SAD_ASYNC_OF(16, 33, 1, 512, 33)
+        MERIT_SAD_ASYNC_OF(16, 33, 1, 256, 33)
+        MERIT_SAD_ASYNC_OF(16, 33, 1, 512, 65)
+        MERIT_SAD_ASYNC_OF(16, 33, 1, 256, 65)
+      } else {
+        MERIT_SAD_ASYNC_OF(8, 33, 2, 512, 65)
+        MERIT_SAD_ASYNC_OF(8, 33, 2, 256, 65)
+      }
+    }
+#undef MERIT_SAD_ASYNC_OF
+  }
+  const size_t smem_launch = use_async ? smem_async : smem;
   cudaError_t e = set_smem_attr(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem));
+                                       static_cast<int>(smem_launch));
   if (e != cudaSuccess) return cuda_check(e, "set_smem_attr(sad)");
   const int threads = (L.items + 31) / 32 * 32;
   L.key_mul = 65536u;
@@ -662,10 +826,10 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
   fast_div_init(static_cast<uint32_t>(L.BYT), L.byt_m, L.byt_s);
   long long grid = (nt == 512 ? 1LL : 2LL) * num_sms();
   if (grid > L.n_tiles) grid = L.n_tiles;
-  e = launch_pdl(kern, dim3(static_cast<unsigned>(grid)), dim3(threads), smem, s, 1, cur, ref, out, aux, L, ref_map,
-                 cur_map);
+  e = launch_pdl(kern, dim3(static_cast<unsigned>(grid)), dim3(threads), smem_launch, s, 1, cur, ref, out, aux, L,
+                 ref_map, cur_map);
   if (e != cudaSuccess) return cuda_check(e, "launch(sad)");
-  return launch_status("sad_kernel");
+  return launch_status(use_async ? "sad_async_kernel" : "sad_kernel");
 }
 
 }  // namespace
