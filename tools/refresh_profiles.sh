@@ -9,7 +9,7 @@ set -u
 TAG=$1; shift
 CONFIGS=${*:-C1 C2 C3 C4 C5}
 mkdir -p gpurun_out
-declare -A KERN=([C1]=maxpool [C2]=sad_kernel [C3]=conv_s1 [C4]=conv_tma [C5]=sad_kernel)
+declare -A KERN=([C1]=maxpool [C2]=sad_ [C3]=conv_s1 [C4]=conv_tma [C5]=sad_)
 for C in $CONFIGS; do
   c=$(echo "$C" | tr 'C' 'c')
   timeout 900 python bench.py --config "$C" > "gpurun_out/bench_${TAG}_${C}.json" 2> "gpurun_out/bench_${TAG}_${C}.err" || { echo "$C bench failed"; continue; }
