@@ -88,6 +88,17 @@ __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(leader_bar)
       : "memory");
 }
+// The same, multicast to the CTAs of `mask` (same shared offset in each); each
+// destination's bytes complete on its own pair leader's barrier at the same
+// offset (CUTLASS's 2-SM multicast load)
+__device__ __forceinline__ void tma_load_2d_pair_mc(uint32_t dst, const CUtensorMap* map, int x, int y,
+                                                    uint32_t leader_bar, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
+      "[%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(leader_bar), "h"(mask)
+      : "memory");
+}
 
 __device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, uint32_t src, int x, int y, int c, int n) {
   asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
@@ -102,7 +113,12 @@ __device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, uint32_t sr
 // fetched from L2 feeds 256 output slots.  The leader (rank 0) issues the
 // MMAs; operand-ready signals of the peer arrive on the leader's barriers,
 // and the MMA commits multicast back to both CTAs.
-template <bool PAIR>
+//
+// QUAD (needs PAIR): clusters of two such pairs that share every weight tile:
+// the CTAs holding the same half of it (ranks 0 / 2 and 1 / 3) each load a
+// quarter and multicast it to both, so a weight byte read from L2 feeds 512
+// output slots.  A weight slot is refilled once both pairs' MMAs released it.
+template <bool PAIR, bool QUAD = false>
 __global__ void __maxnreg__(128)  // 15 warps: <= 4 per SM sub-partition x 128 regs
 conv_tma_kernel(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap out_map,
                 const __grid_constant__ CUtensorMap b_map, TmaArgs A) {
@@ -134,10 +150,13 @@ conv_tma_kernel(const __grid_constant__ CUtensorMap in_map, const __grid_constan
   auto tap1_plane = [&](int s) { return aring + s * kASlot + kPlane; };
 
   constexpr uint32_t kSplit = PAIR ? 2u : 1u;  // CTAs feeding one MMA
-  const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+  const uint32_t crank = PAIR ? cluster_ctarank() : 0u;  // rank in the cluster
+  const uint32_t rank = crank & 1u;                          // rank in the pair
+  const uint32_t lead = crank & ~1u;                         // the pair's leader
+  const uint16_t pair_mask = static_cast<uint16_t>(3u << lead);
   // operand-ready / accumulator-free signals go to the MMA-issuing CTA
   auto to_leader = [&](uint32_t bar) {
-    if (PAIR) mbar_arrive_cluster(mapa_shared(bar, 0)); else mbar_arrive(bar);
+    if (PAIR) mbar_arrive_cluster(mapa_shared(bar, lead)); else mbar_arrive(bar);
   };
   if (threadIdx.x == 0) {
     for (int s = 0; s < A.nr; ++s) {
@@ -150,7 +169,7 @@ conv_tma_kernel(const __grid_constant__ CUtensorMap in_map, const __grid_constan
     }
     for (int s = 0; s < A.nb; ++s) {
       mbar_init(b_full(s), 1);
-      mbar_init(b_empty(s), 1);
+      mbar_init(b_empty(s), QUAD ? 2 : 1);  // quad: both pairs' MMAs release it
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(tfull(a), 1);
@@ -185,9 +204,10 @@ conv_tma_kernel(const __grid_constant__ CUtensorMap in_map, const __grid_constan
   // scheduling unit -> (M tile, N tile); in pair mode the two CTAs of a
   // cluster take adjacent M tiles (an odd last one reads / writes out of
   // bounds image N, which TMA zero-fills / clips)
-  const int unit0 = PAIR ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
-  const int ustep = PAIR ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
-  auto m_tile = [&](int u) { return PAIR ? 2 * (u / p.n_tiles_n) + static_cast<int>(rank) : u / p.n_tiles_n; };
+  constexpr int kCl = QUAD ? 4 : (PAIR ? 2 : 1);  // CTAs per cluster = M tiles per unit
+  const int unit0 = static_cast<int>(blockIdx.x) / kCl;
+  const int ustep = static_cast<int>(gridDim.x) / kCl;
+  auto m_tile = [&](int u) { return kCl * (u / p.n_tiles_n) + static_cast<int>(crank); };
 
   if (warp == kWarpTma) {
     // ============ raw-row loader: the MERIT gather on the TMA engine ======
@@ -278,13 +298,23 @@ conv_tma_kernel(const __grid_constant__ CUtensorMap in_map, const __grid_constan
         const int nt = tile % p.n_tiles_n;
         for (int kb = 0; kb < p.n_kb; ++kb) {
           twait(b_empty(st), ph ^ 1, w1, pon);
-          if (PAIR) {
+          if (QUAD) {
+            // this CTA's quarter: sub-half (crank >> 1) of weight half `rank`,
+            // multicast to the two CTAs holding that half; every pair leader
+            // still receives its whole tile
+            if (rank == 0) mbar_expect_tx(b_full(st), A.b_bytes);
+            const uint32_t q = A.b_slot / 2;
+            const uint32_t sub = crank >> 1;
+            const long long off = ((long long)nt * p.n_kb + kb) * A.b_bytes + rank * A.b_slot + sub * q;
+            tma_load_2d_pair_mc(bring + st * A.b_slot + sub * q, &b_map, 0, static_cast<int>(off >> 8),
+                                mapa_shared(b_full(st), lead), static_cast<uint16_t>(rank ? 0xAu : 0x5u));
+          } else if (PAIR) {
             // both halves complete on the leader's barrier, which expects the
             // whole tile
             if (rank == 0) mbar_expect_tx(b_full(st), A.b_bytes);
             const long long off = ((long long)nt * p.n_kb + kb) * A.b_bytes + rank * A.b_slot;
             tma_load_2d_pair(bring + st * A.b_slot, &b_map, 0, static_cast<int>(off >> 8),
-                             mapa_shared(b_full(st), 0));
+                             mapa_shared(b_full(st), lead));
           } else {
             mbar_expect_tx(b_full(st), A.b_bytes);
             bulk_g2s(bring + st * A.b_bytes, A.wpk + ((long long)nt * p.n_kb + kb) * A.b_bytes, A.b_bytes,
@@ -324,13 +354,13 @@ conv_tma_kernel(const __grid_constant__ CUtensorMap in_map, const __grid_constan
               else
                 tc_mma_w(d_tmem, ad + 2 * k, bd + 2 * k, idesc, accum);
             }
-            if (PAIR) tc_commit_pair_w(b_empty(bs), 3); else tc_commit_w(b_empty(bs));
+            if (PAIR) tc_commit_pair_w(b_empty(bs), QUAD ? 0xF : pair_mask); else tc_commit_w(b_empty(bs));
             if (++bs == A.nb) { bs = 0; bph ^= 1; }
           }
-          if (PAIR) tc_commit_pair_w(a_empty(as), 3); else tc_commit_w(a_empty(as));
+          if (PAIR) tc_commit_pair_w(a_empty(as), pair_mask); else tc_commit_w(a_empty(as));
           if (++as == A.na) { as = 0; aph ^= 1; }
         }
-        if (PAIR) tc_commit_pair_w(tfull(acc), 3); else tc_commit_w(tfull(acc));
+        if (PAIR) tc_commit_pair_w(tfull(acc), pair_mask); else tc_commit_w(tfull(acc));
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
@@ -438,7 +468,12 @@ merit_status launch_conv_tma(const merit_plan& plan, const void* a, const void* 
   // a weight tile a whole number of 8-row swizzle atoms
   const char* pe = getenv("MERIT_CONV_PAIR");
   const bool pair = !(pe && pe[0] == '0') && p.BN % 16 == 0 && num_sms() >= 2;
-  A.n_units = pair ? ((m_tiles + 1) / 2) * p.n_tiles_n : A.n_tiles;
+  // two pairs per cluster sharing weight tiles by multicast: each quarter of
+  // a tile must be whole 1 KB swizzle atoms (BN % 32 == 0)
+  const char* qe = getenv("MERIT_CONV_QUAD");
+  const bool quad = pair && (qe && qe[0] == '1') && p.BN % 32 == 0 && num_sms() >= 4;
+  const int mpu = quad ? 4 : (pair ? 2 : 1);  // M tiles per scheduling unit
+  A.n_units = ((m_tiles + mpu - 1) / mpu) * p.n_tiles_n;
   A.n_groups = p.KH * p.CB;
   A.raw_bytes = static_cast<uint32_t>(p.W) * 4u * 32u * 2u;
   A.b_bytes = static_cast<uint32_t>(p.BN) * 128u;
@@ -494,7 +529,7 @@ merit_status launch_conv_tma(const merit_plan& plan, const void* a, const void* 
   if (pair) {
     const cuuint64_t bdims[2] = {256, (cuuint64_t)(p.packed_b_bytes / 256)};
     const cuuint64_t bstr[1] = {256};
-    const cuuint32_t bbox[2] = {256, A.b_slot / 256};
+    const cuuint32_t bbox[2] = {256, (quad ? A.b_slot / 2 : A.b_slot) / 256};
     const cuuint32_t bestr[2] = {1, 1};
     cr = get_encode()(&bmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(packed_b), bdims, bstr, bbox,
                       bestr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -503,11 +538,29 @@ merit_status launch_conv_tma(const merit_plan& plan, const void* a, const void* 
   }
   if (A.n_tiles == 0) return MERIT_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  auto kfn = pair ? conv_tma_kernel<true> : conv_tma_kernel<false>;
+  auto kfn = quad ? conv_tma_kernel<true, true> : (pair ? conv_tma_kernel<true> : conv_tma_kernel<false>);
   cudaError_t e = set_smem_attr(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return cuda_check(e, "set_smem_attr(conv_tma)");
   int grid;
-  if (pair) {
+  if (quad) {
+    int quads = num_sms() / 4;
+    static std::mutex qmu;
+    static std::vector<std::pair<size_t, int>> qcache;  // smem bytes -> 4-CTA clusters
+    int mc = -1;
+    {
+      std::lock_guard<std::mutex> lk(qmu);
+      for (auto& c : qcache)
+        if (c.first == smem) mc = c.second;
+      if (mc < 0) {
+        mc = max_active_clusters(kfn, dim3(kThreads), smem, 4u);
+        qcache.push_back({smem, mc});
+      }
+    }
+    if (mc > 0 && quads > mc) quads = mc;
+    if (A.debug & 4096) fprintf(stderr, "[conv_tma] max active 4-CTA clusters %d, quads %d\n", mc, quads);
+    if (quads > A.n_units) quads = A.n_units;
+    grid = 4 * quads;
+  } else if (pair) {
     int pairs = num_sms() / 2;
     // only as many pairs as can be co-resident (TPC / GPC placement): a
     // surplus pair would run its units as a second wave after everyone else
@@ -540,7 +593,7 @@ merit_status launch_conv_tma(const merit_plan& plan, const void* a, const void* 
     cudaMalloc(&A.prof, 8ull * 4 * 16 * grid);
     cudaMemset(A.prof, 0, 8ull * 4 * 16 * grid);
   }
-  e = launch_pdl(kfn, dim3(grid), dim3(kThreads), smem, s, pair ? 2u : 1u, map, omap, bmap, A);
+  e = launch_pdl(kfn, dim3(grid), dim3(kThreads), smem, s, static_cast<unsigned>(mpu), map, omap, bmap, A);
   if (e != cudaSuccess) return cuda_check(e, "launch(conv_tma)");
   if (A.debug & 64) {
     cudaStreamSynchronize(s);
@@ -559,7 +612,8 @@ merit_status launch_conv_tma(const merit_plan& plan, const void* a, const void* 
             frac(kWarpMma, kWarpMma + 1, 2, ms), frac(kWarpMma, kWarpMma + 1, 3, ms), frac(kWarpEpi0, kWarpEpi0 + 4, 1, 1));
     cudaFree(A.prof);
   }
-  return launch_status(pair ? "conv_tma_kernel<pair, cta_group::2>" : "conv_tma_kernel<single>");
+  return launch_status(quad ? "conv_tma_kernel<quad, cta_group::2, weight multicast>"
+                              : (pair ? "conv_tma_kernel<pair, cta_group::2>" : "conv_tma_kernel<single>"));
 }
 
 }  // namespace merit_dev

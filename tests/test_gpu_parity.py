@@ -116,12 +116,15 @@ def test_sad_small_bit_exact(cuda, h, wd, blk, r, boundary):
     assert np.array_equal(mv, O.me_argmin(want, r))
 
 
-@pytest.mark.parametrize("mode", ["1", "0"])  # staging: TMA boxes / cp.async
+# staging: TMA boxes with the barrier-free kernel / TMA boxes with one tile
+# barrier per tile / cp.async
+@pytest.mark.parametrize("mode", ["1", "1-sync", "0"])
 @pytest.mark.parametrize("blk", [8, 16])
 def test_sad_staging_modes_unaligned_windows(cuda, monkeypatch, mode, blk):
     # windows that start at every byte offset mod 16 (radius r: x0 = bx*blk - r),
     # the case TMA boxes cannot start at (tools/microbench/tma_u8.cu)
-    monkeypatch.setenv("MERIT_SAD_TMA", mode)
+    monkeypatch.setenv("MERIT_SAD_TMA", mode[0])
+    monkeypatch.setenv("MERIT_SAD_ASYNC", "0" if mode == "1-sync" else "1")
     for (h, wd, r) in [(64, 96, 2), (48, 128, 5), (80, 160, 7), (72, 112, 12), (88, 80, 23)]:  # BY odd for 8x8 in the last two
         cur, ref = W.gen_me_pair(h, wd, 17, blk, min(r, 16), 4)
         w = W.me_view(h, wd, blk, r)
@@ -253,6 +256,7 @@ def test_conv_fp32_stride1_tap_stacked(cuda, monkeypatch, variant, n, cin, h, wd
 CONV_VARIANTS = {
     "default": {},                                  # TMA gather, CTA pairs where eligible
     "single": {"MERIT_CONV_PAIR": "0"},             # TMA gather, one CTA per tile
+    "quad": {"MERIT_CONV_QUAD": "1"},               # two CTA pairs per cluster, weight multicast
     "tap3": {"MERIT_CONV_TMA": "0"},                # register gather, tap-shared planes
     "general": {"MERIT_CONV_KERNEL": "general"},    # per-tap gather
 }
@@ -263,6 +267,7 @@ CONV_VARIANTS = {
     (2, 128, 16, 256),    # small image: tap3 path, two channel blocks
     (2, 128, 32, 256),
     (3, 128, 56, 256),    # C4 geometry, 21 M tiles: odd -> ghost tile in pair mode
+    (5, 128, 56, 256),    # 35 M tiles: three ghost tiles in quad mode
     (1, 192, 56, 96),     # three channel blocks, BN = 96
     (2, 64, 56, 320),     # two N tiles (BN = 160)
 ])
