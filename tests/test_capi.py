@@ -147,6 +147,19 @@ def test_validate_errors_mirror_reference():
     assert e.value.code == ErrorCode.UnsupportedProgram   # argmin needs the SAD kernel
 
 
+@pytest.mark.parametrize("make", [
+    lambda: W.conv_nchw_view(0, 64, 14, 14, 64, 3, 1, 1),     # empty batch
+    lambda: W.maxpool_nchw_view(0, 8, 16, 16),
+    lambda: W.me_view(64, 128, 16, 16, pairs=0),               # no frame pairs
+])
+def test_empty_outputs_rejected_like_reference_tensor(make):
+    # the reference builds the output Tensor from p_shape, and Tensor rejects
+    # zero extents with BadParams (tensor.hpp:167-169): no empty run exists
+    with pytest.raises(Error) as e:
+        Plan(make())
+    assert e.value.code == ErrorCode.BadParams
+
+
 def test_reject_out_of_range_views_go_to_checking_interpreter():
     w = W.build_template("maxpool", {"h": 4, "w": 4, "k": 2})
     w.view_a.terms[1].offset = -1
