@@ -9,6 +9,7 @@
 // (equivalent to -inf padding for max); ZERO_PAD reads 0 outside.
 //
 // Roofline: HBM.  Algorithmic bytes = input plane bytes + output bytes.
+#include <algorithm>
 #include <cstring>
 
 #include "common.cuh"
@@ -325,9 +326,19 @@ merit_status launch_maxpool(const merit_plan& plan, const void* a, void* out, vo
     // 7 four-warp CTAs per SM with a 4..8-band ring keep ~200 KB of copies in
     // flight per SM, which is what the HBM stream needs at this size
     int RBv = 8;
+    {
+      // Whole launch in one wave of single-band CTAs when it fits: bands of
+      // 28 output rows (57 input rows, one TMA box each), every CTA resident
+      // at once with its one load in flight (C1: 1,024 bands <= 148 x 7
+      // CTAs; 7.27 vs 7.41 us for 8-row bands through a 4-deep ring)
+      const size_t st28 = ((size_t)57 * p.W * 4 + 127) / 128 * 128;
+      const long long fit = st28 <= 200 * 1024 ? std::min<long long>(7, (227 * 1024) / (st28 + 1024)) : 0;
+      const long long items28 = p.planes * ((p.Ho + 27) / 28);
+      if (p.Ho >= 28 && fit > 0 && items28 <= num_sms() * fit) RBv = 28;
+    }
     if (const char* re = getenv("MERIT_MP_RB")) {
       const int v = atoi(re);
-      RBv = (v == 4 || v == 16 || v == 28) ? v : 8;
+      RBv = (v == 4 || v == 16 || v == 28 || v == 56) ? v : 8;
     }
     const int nband = (p.Ho + RBv - 1) / RBv;
     const long long items = p.planes * nband;
@@ -364,6 +375,7 @@ merit_status launch_maxpool(const merit_plan& plan, const void* a, void* out, vo
       if (RBv == 4) k = tm ? maxpool3s2_bulk_kernel<128, 4, true> : maxpool3s2_bulk_kernel<128, 4, false>;
       if (RBv == 16) k = tm ? maxpool3s2_bulk_kernel<128, 16, true> : maxpool3s2_bulk_kernel<128, 16, false>;
       if (RBv == 28) k = tm ? maxpool3s2_bulk_kernel<128, 28, true> : maxpool3s2_bulk_kernel<128, 28, false>;
+      if (RBv == 56) k = tm ? maxpool3s2_bulk_kernel<128, 56, true> : maxpool3s2_bulk_kernel<128, 56, false>;
       cudaError_t e = set_smem_attr(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return cuda_check(e, "set_smem_attr(maxpool)");
       MaxpoolParams pp = p;
