@@ -327,10 +327,11 @@ merit_status launch_maxpool(const merit_plan& plan, const void* a, void* out, vo
     // flight per SM, which is what the HBM stream needs at this size
     int RBv = 8;
     {
-      // Whole launch in one wave of single-band CTAs when it fits: bands of
-      // 28 output rows (57 input rows, one TMA box each), every CTA resident
-      // at once with its one load in flight (C1: 1,024 bands <= 148 x 7
-      // CTAs; 7.27 vs 7.41 us for 8-row bands through a 4-deep ring)
+      // Single-band CTAs when the launch is small: bands of 28 output rows
+      // (57 input rows, one TMA box each), one load in flight per CTA, used
+      // when the bands would fit 7 resident CTAs per SM (C1: 1,024 bands;
+      // measured 6.67 us with the 8-warp, 6-per-SM launch below vs 7.41 us
+      // for 8-row bands through a 4-deep ring)
       const size_t st28 = ((size_t)57 * p.W * 4 + 127) / 128 * 128;
       const long long fit = st28 <= 200 * 1024 ? std::min<long long>(7, (227 * 1024) / (st28 + 1024)) : 0;
       const long long items28 = p.planes * ((p.Ho + 27) / 28);
@@ -350,7 +351,8 @@ merit_status launch_maxpool(const merit_plan& plan, const void* a, void* out, vo
     if (const char* se = getenv("MERIT_MP_STAGES")) ns = atoi(se);
     if (ns > kMpMaxStages) ns = kMpMaxStages;
     while (ns > 1 && ns * stage > 100 * 1024) --ns;
-    const size_t smem = ns * stage;
+    size_t smem = ns * stage;
+    if (const char* pe = getenv("MERIT_MP_SMEM_PAD")) smem += static_cast<size_t>(atoi(pe));  // residency experiments
     if (smem <= 200 * 1024) {
       long long grid = (long long)num_sms() * ctas;
       if (grid > items) grid = items;
@@ -376,6 +378,20 @@ merit_status launch_maxpool(const merit_plan& plan, const void* a, void* out, vo
       if (RBv == 16) k = tm ? maxpool3s2_bulk_kernel<128, 16, true> : maxpool3s2_bulk_kernel<128, 16, false>;
       if (RBv == 28) k = tm ? maxpool3s2_bulk_kernel<128, 28, true> : maxpool3s2_bulk_kernel<128, 28, false>;
       if (RBv == 56) k = tm ? maxpool3s2_bulk_kernel<128, 56, true> : maxpool3s2_bulk_kernel<128, 56, false>;
+      // 28-row bands: 8 warps per CTA (a band's 392 16-byte output groups in
+      // two passes instead of four shortens every CTA's compute-and-store
+      // tail) and exactly 6 CTAs per SM (dynamic shared memory padded to 32
+      // KB): C1 runs 888 bands as the first wave and 136 as a second one,
+      // 6.67 us vs 7.33 us with all 1,024 resident at once (7 per SM)
+      int nt = 128;
+      if (RBv == 28) {
+        const char* ne = getenv("MERIT_MP_NT");
+        if (!(ne && atoi(ne) == 128)) {
+          nt = 256;
+          k = tm ? maxpool3s2_bulk_kernel<256, 28, true> : maxpool3s2_bulk_kernel<256, 28, false>;
+          if (!getenv("MERIT_MP_SMEM_PAD") && smem < 32768) smem = 32768;
+        }
+      }
       cudaError_t e = set_smem_attr(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return cuda_check(e, "set_smem_attr(maxpool)");
       MaxpoolParams pp = p;
@@ -383,7 +399,7 @@ merit_status launch_maxpool(const merit_plan& plan, const void* a, void* out, vo
       pp.vec_out = (p.Wo % 4 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
       pp.pf = ns;
       if (const char* pe = getenv("MERIT_MP_PF")) pp.pf = atoi(pe) < 0 ? (1 << 30) : atoi(pe);
-      e = launch_pdl(k, dim3(static_cast<unsigned>(grid)), dim3(128), smem, s, 1, in, o, pp, nband,
+      e = launch_pdl(k, dim3(static_cast<unsigned>(grid)), dim3(nt), smem, s, 1, in, o, pp, nband,
                      static_cast<int>(items), ns,
                      rmap);
       if (e != cudaSuccess) return cuda_check(e, "launch(maxpool3s2_bulk_kernel)");
