@@ -11,7 +11,7 @@ import oracle.binding as O
 
 n_cases = int(sys.argv[1]) if len(sys.argv) > 1 else 40
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 1)
-variants = [{}, {"MERIT_CONV_PAIR": "0"}, {"MERIT_CONV_TMA": "0"}, {"MERIT_CONV_S1": "0"},
+variants = [{}, {"MERIT_CONV_PAIR": "0"}, {"MERIT_CONV_QUAD": "1"}, {"MERIT_CONV_TMA": "0"}, {"MERIT_CONV_S1": "0"},
             {"MERIT_CONV_KERNEL": "general"}]
 bad = 0
 for t in range(n_cases):
