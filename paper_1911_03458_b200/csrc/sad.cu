@@ -482,7 +482,124 @@ __device__ __forceinline__ void sad_tile_work(const SadLaunch& L, void* __restri
   }
 }
 
-template <int BLK, int D, int NBY, int NT, int WXC>
+// Warp-per-block matching for 16x16 blocks and a 33 x 33 window (the +/-16
+// search of C2): warp w owns block w of the tile and lane l the column
+// dx = l for all 33 dy (33 accumulators, the loop of sad_tile_work), plus
+// the 33rd column split over the lanes: lane l also matches (dy = l,
+// dx = 32) in a 16-row side loop, and (dy = 32, dx = 32) is shared by the
+// warp (two products per lane, REDUX sum).  Every lane does useful work
+// (231 of 256 lanes in the (block, dx) mapping), tiles are 8 blocks wide
+// (C2: 120 = 15 x 8, no partial tiles) and the argmin is one warp REDUX per
+// block, with no shared-memory atomics.
+__device__ __forceinline__ void sad_tile_work_warp(const SadLaunch& L, void* __restrict__ out,
+                                                   int32_t* __restrict__ aux, int tile, const uint32_t* curw,
+                                                   const uint32_t* copies) {
+  constexpr int BLK = 16, D = 33, WX = 33, BWW = 4;
+  const SadParams& p = L.p;
+  const int cpw = L.cur_pitch / 4;
+  const int ib = static_cast<int>(threadIdx.x) >> 5;
+  const int lane = static_cast<int>(threadIdx.x) & 31;
+  int t2, tx;
+  sad_tile_coords(tile, L.n_full_tiles, L.n_full_x, L.ntx_m, L.ntx_s, t2, tx);
+  const int pair_i = static_cast<int>(fast_div(t2, L.byt_m, L.byt_s));
+  const int by = L.by0 + (t2 - pair_i * L.BYT);
+  const long long pair = pair_i;
+  const int bx0 = tx * L.TBX;
+  const int nb = min(L.TBX, p.BX - bx0);
+  if (ib >= nb) return;  // warp-uniform
+  const int dcur = L.tma ? (bx0 * BLK + p.cx) - floor16(bx0 * BLK + p.cx) : 0;
+  const uint32_t* cb = curw + (dcur >> 2) + ib * BWW;
+  uint32_t cw[BLK][BWW];
+  if ((dcur & 15) == 0) {
+#pragma unroll
+    for (int i = 0; i < BLK; ++i) {
+      const uint4 q4 = *reinterpret_cast<const uint4*>(cb + i * cpw);
+      cw[i][0] = q4.x; cw[i][1] = q4.y; cw[i][2] = q4.z; cw[i][3] = q4.w;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < BLK; ++i)
+#pragma unroll
+      for (int j = 0; j < BWW; ++j) cw[i][j] = cb[i * cpw + j];
+  }
+  const int col = ib * BLK + lane;  // byte column of this lane's dx in the staged window
+  const uint32_t* cp = copies + (col & 3) * L.CS + (col >> 2);
+  uint32_t acc[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) acc[d] = 0;
+#pragma unroll
+  for (int r = 0; r < D + BLK - 1; ++r) {
+    uint32_t rwv[BWW];
+#pragma unroll
+    for (int j = 0; j < BWW; ++j) rwv[j] = cp[j];
+    cp += L.Ww;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const int i = r - d;
+      if (i >= 0 && i < BLK) {
+#pragma unroll
+        for (int j = 0; j < BWW; ++j) acc[d] = vabsdiff4_acc(cw[i][j], rwv[j], acc[d]);
+      }
+    }
+  }
+  // column dx = 32 (byte column ib*16 + 32: a multiple of 4, shifted copy 0):
+  // lane l takes dy = l, reading staged rows l .. l + 15
+  const int col32 = ib * BLK + 32;
+  uint32_t ax = 0;
+  {
+    const uint32_t* cx = copies + (col32 & 3) * L.CS + (col32 >> 2) + lane * L.Ww;
+#pragma unroll
+    for (int i = 0; i < BLK; ++i) {
+#pragma unroll
+      for (int j = 0; j < BWW; ++j) ax = vabsdiff4_acc(cw[i][j], cx[j], ax);
+      cx += L.Ww;
+    }
+  }
+  // (dy = 32, dx = 32): lane l takes block row l >> 1, words 2 (l & 1) .. + 1
+  uint32_t axx;
+  {
+    const int i = lane >> 1, j0 = 2 * (lane & 1);
+    const uint32_t* cr = copies + (col32 & 3) * L.CS + (col32 >> 2) + (32 + i) * L.Ww + j0;
+    uint32_t v = vabsdiff4_acc(cb[i * cpw + j0], cr[0], 0u);
+    v = vabsdiff4_acc(cb[i * cpw + j0 + 1], cr[1], v);
+    axx = __reduce_add_sync(0xffffffffu, v);
+  }
+  const long long blk_index = (pair * p.BY + by) * (long long)p.BX + bx0 + ib;
+  if (p.write_map && by < L.by1) {
+    const long long obase = blk_index * (long long)(D * WX);
+    sad_store_map<D>(out, p.out_f32, obase + lane, WX, acc, D);  // (dy = d, dx = lane)
+    if (p.out_f32) {
+      float* o = static_cast<float*>(out) + obase;
+      __stcs(o + lane * WX + 32, static_cast<float>(ax));
+      if (lane == 0) __stcs(o + 32 * WX + 32, static_cast<float>(axx));
+    } else {
+      int32_t* o = static_cast<int32_t*>(out) + obase;
+      __stcs(o + lane * WX + 32, static_cast<int32_t>(ax));
+      if (lane == 0) __stcs(o + 32 * WX + 32, static_cast<int32_t>(axx));
+    }
+  }
+  if (p.argmin && by < L.by1) {
+    // key = sad << 16 | (dy * 33 + dx): lowest SAD, then lowest raster index
+    const uint32_t kmul = L.key_mul;
+    uint32_t best = 0xffffffffu;
+#pragma unroll
+    for (int d = 0; d < D; ++d) best = min(best, acc[d] * kmul + static_cast<uint32_t>(d * WX));
+    best += static_cast<uint32_t>(lane);
+    best = min(best, ax * kmul + static_cast<uint32_t>(lane * WX + 32));
+    if (lane == 0) best = min(best, axx * kmul + static_cast<uint32_t>(32 * WX + 32));
+    const uint32_t key = __reduce_min_sync(0xffffffffu, best);
+    if (lane == 0) {
+      const int k = static_cast<int>(key & 0xffffu);
+      const int dy = k / WX, dx = k - (k / WX) * WX;
+      int32_t* a = aux + blk_index * 3;
+      a[0] = dy + p.oy - p.cy;
+      a[1] = dx + p.ox - p.cx;
+      a[2] = static_cast<int32_t>(key >> 16);
+    }
+  }
+}
+
+template <int BLK, int D, int NBY, int NT, int WXC, bool WARP = false>
 __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1)
 sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, void* __restrict__ out,
            int32_t* __restrict__ aux, SadLaunch L, const __grid_constant__ CUtensorMap ref_map,
@@ -543,7 +660,10 @@ sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, voi
                       reinterpret_cast<uint8_t*>(raw0 + (buf ^ 1) * raw_words),
                       smem_u32(cur0 + (buf ^ 1) * cur_words),
                       reinterpret_cast<uint8_t*>(cur0 + (buf ^ 1) * cur_words), bar0 + 8u * (buf ^ 1));
-    sad_tile_work<BLK, D, NBY, WXC>(L, out, aux, tile, curw, copies, keys, cnt, [] {});
+    if constexpr (WARP)
+      sad_tile_work_warp(L, out, aux, tile, curw, copies);
+    else
+      sad_tile_work<BLK, D, NBY, WXC>(L, out, aux, tile, curw, copies, keys, cnt, [] {});
   }
   cp_async_wait_all();
 }
@@ -688,6 +808,15 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
   if (const char* te = getenv("MERIT_SAD_THREADS")) nt = atoi(te) == 512 ? 512 : 256;
   L.TBX = nt == 512 ? tbx512 : tbx256;
   L.items = L.TBX * per_block;
+  // warp-per-block mapping for the +/-16 search of 16x16 blocks (C2): 8-block
+  // tiles, every lane busy (sad_tile_work_warp)
+  const char* wme = getenv("MERIT_SAD_WARP");
+  const bool warp_mode = BLK == 16 && D == 33 && p.WX == 33 && p.WY == 33 && p.BX >= 8 && !(wme && wme[0] == '0');
+  if (warp_mode) {
+    nt = 256;
+    L.TBX = 8;
+    L.items = 256;
+  }
   L.n_tiles_x = (p.BX + L.TBX - 1) / L.TBX;
   L.span = L.TBX * BLK + p.WX - 1;
   L.Ww = (L.span + 3) / 4;
@@ -764,7 +893,7 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
   const size_t smem_async = 128 + 2ull * L.raw_buf + 2ull * L.cur_buf +
                             4ull * (12ull * L.CS + 4ull * L.nby * L.TBX + 2) + 8 + 64;
   const char* ae = getenv("MERIT_SAD_ASYNC");
-  const bool use_async = L.tma && !(ae && ae[0] == '0') && smem_async <= smem_cap;
+  const bool use_async = !warp_mode && L.tma && !(ae && ae[0] == '0') && smem_async <= smem_cap;
   auto kern = nt == 512 ? sad_kernel<BLK, D, 1, 512, 0> : sad_kernel<BLK, D, 1, 256, 0>;
   if constexpr (BLK == 8) {
     if (L.nby == 2) kern = nt == 512 ? sad_kernel<BLK, D, 2, 512, 0> : sad_kernel<BLK, D, 2, 256, 0>;
@@ -773,12 +902,13 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
   if constexpr (D == 33) {
     if constexpr (BLK == 16) {
       if (p.WX == 33) kern = nt == 512 ? sad_kernel<16, 33, 1, 512, 33> : sad_kernel<16, 33, 1, 256, 33>;
+      if (warp_mode) kern = sad_kernel<16, 33, 1, 256, 33, true>;
       if (p.WX == 65) kern = nt == 512 ? sad_kernel<16, 33, 1, 512, 65> : sad_kernel<16, 33, 1, 256, 65>;
     } else {
       if (p.WX == 65 && L.nby == 2) kern = nt == 512 ? sad_kernel<8, 33, 2, 512, 65> : sad_kernel<8, 33, 2, 256, 65>;
     }
   }
-  if (const char* we = getenv("MERIT_SAD_WXC"); we && we[0] == '0') {  // A/B switch: runtime width
+  if (const char* we = getenv("MERIT_SAD_WXC"); we && we[0] == '0' && !warp_mode) {  // A/B: runtime width
     kern = nt == 512 ? sad_kernel<BLK, D, 1, 512, 0> : sad_kernel<BLK, D, 1, 256, 0>;
     if constexpr (BLK == 8) {
       if (L.nby == 2) kern = nt == 512 ? sad_kernel<BLK, D, 2, 512, 0> : sad_kernel<BLK, D, 2, 256, 0>;
@@ -829,7 +959,7 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
   e = launch_pdl(kern, dim3(static_cast<unsigned>(grid)), dim3(threads), smem_launch, s, 1, cur, ref, out, aux, L,
                  ref_map, cur_map);
   if (e != cudaSuccess) return cuda_check(e, "launch(sad)");
-  return launch_status(use_async ? "sad_async_kernel" : "sad_kernel");
+  return launch_status(warp_mode ? "sad_kernel<warp per block>" : (use_async ? "sad_async_kernel" : "sad_kernel"));
 }
 
 }  // namespace
