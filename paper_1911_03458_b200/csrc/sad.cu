@@ -820,6 +820,9 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
   L.n_tiles_x = (p.BX + L.TBX - 1) / L.TBX;
   L.span = L.TBX * BLK + p.WX - 1;
   L.Ww = (L.span + 3) / 4;
+  // warp mode: the 33rd column's side loop has lane l read staged row l + i,
+  // so an odd row pitch keeps the 32 lanes on 32 banks (40 words: 8-way conflicts)
+  if (warp_mode && (L.Ww & 1) == 0) L.Ww += 1;
   // TMA staging lands rows from floor16(x): up to 15 leading bytes, and the
   // copy builder reads 2 words past the window
   const char* te = getenv("MERIT_SAD_TMA");
