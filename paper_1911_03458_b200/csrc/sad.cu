@@ -482,23 +482,30 @@ __device__ __forceinline__ void sad_tile_work(const SadLaunch& L, void* __restri
   }
 }
 
-// Warp-per-block matching for 16x16 blocks and a 33 x 33 window (the +/-16
-// search of C2): warp w owns block w of the tile and lane l the column
-// dx = l for all 33 dy (33 accumulators, the loop of sad_tile_work), plus
-// the 33rd column split over the lanes: lane l also matches (dy = l,
-// dx = 32) in a 16-row side loop, and (dy = 32, dx = 32) is shared by the
-// warp (two products per lane, REDUX sum).  Every lane does useful work
-// (231 of 256 lanes in the (block, dx) mapping), tiles are 8 blocks wide
-// (C2: 120 = 15 x 8, no partial tiles) and the argmin is one warp REDUX per
-// block, with no shared-memory atomics.
+// Warp-per-block matching for 16x16 blocks and a square window of 32k + 1
+// displacements per axis (WXC = 33: the +/-16 search of C2; 65: +/-32, C5):
+// the k warps of block b own its columns dx = 32 w + lane for every dy (dy
+// groups of D = 33 accumulators, the loop of sad_tile_work), and the last
+// column dx = 32k is split over the block's lanes: lane l of warp w also
+// matches (dy = 32 w + l, dx = 32k) in a 16-row side loop, and the corner
+// (dy = 32k, dx = 32k) is shared by the last warp (two products per lane,
+// REDUX sum).  Every lane does useful work (C2: 231 of 256 lanes in the
+// (block, dx) mapping), tiles are 8 blocks wide (C2: 120 = 15 x 8, no
+// partial tiles) and the argmin is a warp REDUX per block (plus one shared
+// atomic per warp when k = 2).
+template <int WXC>
 __device__ __forceinline__ void sad_tile_work_warp(const SadLaunch& L, void* __restrict__ out,
                                                    int32_t* __restrict__ aux, int tile, const uint32_t* curw,
-                                                   const uint32_t* copies) {
-  constexpr int BLK = 16, D = 33, WX = 33, BWW = 4;
+                                                   const uint32_t* copies, uint32_t* keys, uint32_t* cnt) {
+  constexpr int BLK = 16, D = 33, WX = WXC, WY = WXC, BWW = 4;
+  constexpr int WPB = (WX - 1) / 32;  // warps per block
+  constexpr int G = (WY + D - 1) / D;
   const SadParams& p = L.p;
   const int cpw = L.cur_pitch / 4;
-  const int ib = static_cast<int>(threadIdx.x) >> 5;
+  const int warp = static_cast<int>(threadIdx.x) >> 5;
+  const int ib = warp / WPB, wsub = warp - (warp / WPB) * WPB;
   const int lane = static_cast<int>(threadIdx.x) & 31;
+  const int dxl = 32 * wsub + lane;  // this lane's column
   int t2, tx;
   sad_tile_coords(tile, L.n_full_tiles, L.n_full_x, L.ntx_m, L.ntx_s, t2, tx);
   const int pair_i = static_cast<int>(fast_div(t2, L.byt_m, L.byt_s));
@@ -522,32 +529,53 @@ __device__ __forceinline__ void sad_tile_work_warp(const SadLaunch& L, void* __r
 #pragma unroll
       for (int j = 0; j < BWW; ++j) cw[i][j] = cb[i * cpw + j];
   }
-  const int col = ib * BLK + lane;  // byte column of this lane's dx in the staged window
-  const uint32_t* cp = copies + (col & 3) * L.CS + (col >> 2);
-  uint32_t acc[D];
+  const long long blk_index = (pair * p.BY + by) * (long long)p.BX + bx0 + ib;
+  const long long blk_base = blk_index * (long long)(WY * WX);
+  const bool store = p.write_map && by < L.by1;
+  const uint32_t kmul = L.key_mul;
+  uint32_t best = 0xffffffffu;
+  const int col = ib * BLK + dxl;  // byte column of this lane's dx in the staged window
+#pragma unroll 1
+  for (int ig = 0; ig < G; ++ig) {
+    const uint32_t* cp = copies + (col & 3) * L.CS + (col >> 2) + ig * D * L.Ww;
+    uint32_t acc[D];
 #pragma unroll
-  for (int d = 0; d < D; ++d) acc[d] = 0;
+    for (int d = 0; d < D; ++d) acc[d] = 0;
 #pragma unroll
-  for (int r = 0; r < D + BLK - 1; ++r) {
-    uint32_t rwv[BWW];
+    for (int r = 0; r < D + BLK - 1; ++r) {
+      uint32_t rwv[BWW];
 #pragma unroll
-    for (int j = 0; j < BWW; ++j) rwv[j] = cp[j];
-    cp += L.Ww;
+      for (int j = 0; j < BWW; ++j) rwv[j] = cp[j];
+      cp += L.Ww;
 #pragma unroll
-    for (int d = 0; d < D; ++d) {
-      const int i = r - d;
-      if (i >= 0 && i < BLK) {
+      for (int d = 0; d < D; ++d) {
+        const int i = r - d;
+        if (i >= 0 && i < BLK) {
 #pragma unroll
-        for (int j = 0; j < BWW; ++j) acc[d] = vabsdiff4_acc(cw[i][j], rwv[j], acc[d]);
+          for (int j = 0; j < BWW; ++j) acc[d] = vabsdiff4_acc(cw[i][j], rwv[j], acc[d]);
+        }
       }
     }
+    // the last group of a 65-row window has 32 rows (65 = 33 + 32)
+    const int nd = (ig + 1) * D <= WY ? D : WY - ig * D;
+    uint32_t bn = 0xffffffffu;
+    if (nd == D) {
+#pragma unroll
+      for (int d = 0; d < D; ++d) bn = min(bn, acc[d] * kmul + static_cast<uint32_t>(d * WX));
+      if (store) sad_store_map<D>(out, p.out_f32, blk_base + ig * D * WX + dxl, WX, acc, D);
+    } else {
+#pragma unroll
+      for (int d = 0; d < D - 1; ++d) bn = min(bn, acc[d] * kmul + static_cast<uint32_t>(d * WX));
+      if (store) sad_store_map<D>(out, p.out_f32, blk_base + ig * D * WX + dxl, WX, acc, D - 1);
+    }
+    best = min(best, bn + static_cast<uint32_t>(ig * D * WX + dxl));
   }
-  // column dx = 32 (byte column ib*16 + 32: a multiple of 4, shifted copy 0):
-  // lane l takes dy = l, reading staged rows l .. l + 15
-  const int col32 = ib * BLK + 32;
+  // the last column dx = 32k (byte column ib*16 + 32k: a multiple of 4,
+  // shifted copy 0): this lane takes dy = dxl, reading staged rows dxl .. dxl + 15
+  const int colx = ib * BLK + (WX - 1);
   uint32_t ax = 0;
   {
-    const uint32_t* cx = copies + (col32 & 3) * L.CS + (col32 >> 2) + lane * L.Ww;
+    const uint32_t* cx = copies + (colx & 3) * L.CS + (colx >> 2) + dxl * L.Ww;
 #pragma unroll
     for (int i = 0; i < BLK; ++i) {
 #pragma unroll
@@ -555,46 +583,48 @@ __device__ __forceinline__ void sad_tile_work_warp(const SadLaunch& L, void* __r
       cx += L.Ww;
     }
   }
-  // (dy = 32, dx = 32): lane l takes block row l >> 1, words 2 (l & 1) .. + 1
-  uint32_t axx;
-  {
+  best = min(best, ax * kmul + static_cast<uint32_t>(dxl * WX + (WX - 1)));
+  if (wsub == WPB - 1) {
+    // corner (dy = 32k, dx = 32k): lane l takes block row l >> 1, words 2 (l & 1) .. + 1
     const int i = lane >> 1, j0 = 2 * (lane & 1);
-    const uint32_t* cr = copies + (col32 & 3) * L.CS + (col32 >> 2) + (32 + i) * L.Ww + j0;
+    const uint32_t* cr = copies + (colx & 3) * L.CS + (colx >> 2) + (WY - 1 + i) * L.Ww + j0;
     uint32_t v = vabsdiff4_acc(cb[i * cpw + j0], cr[0], 0u);
     v = vabsdiff4_acc(cb[i * cpw + j0 + 1], cr[1], v);
-    axx = __reduce_add_sync(0xffffffffu, v);
-  }
-  const long long blk_index = (pair * p.BY + by) * (long long)p.BX + bx0 + ib;
-  if (p.write_map && by < L.by1) {
-    const long long obase = blk_index * (long long)(D * WX);
-    sad_store_map<D>(out, p.out_f32, obase + lane, WX, acc, D);  // (dy = d, dx = lane)
-    if (p.out_f32) {
-      float* o = static_cast<float*>(out) + obase;
-      __stcs(o + lane * WX + 32, static_cast<float>(ax));
-      if (lane == 0) __stcs(o + 32 * WX + 32, static_cast<float>(axx));
-    } else {
-      int32_t* o = static_cast<int32_t*>(out) + obase;
-      __stcs(o + lane * WX + 32, static_cast<int32_t>(ax));
-      if (lane == 0) __stcs(o + 32 * WX + 32, static_cast<int32_t>(axx));
+    const uint32_t axx = __reduce_add_sync(0xffffffffu, v);
+    if (lane == 0) best = min(best, axx * kmul + static_cast<uint32_t>((WY - 1) * WX + (WX - 1)));
+    if (store && lane == 0) {
+      if (p.out_f32) __stcs(static_cast<float*>(out) + blk_base + (WY - 1) * WX + (WX - 1), static_cast<float>(axx));
+      else __stcs(static_cast<int32_t*>(out) + blk_base + (WY - 1) * WX + (WX - 1), static_cast<int32_t>(axx));
     }
   }
+  if (store) {
+    if (p.out_f32) __stcs(static_cast<float*>(out) + blk_base + dxl * WX + (WX - 1), static_cast<float>(ax));
+    else __stcs(static_cast<int32_t*>(out) + blk_base + dxl * WX + (WX - 1), static_cast<int32_t>(ax));
+  }
   if (p.argmin && by < L.by1) {
-    // key = sad << 16 | (dy * 33 + dx): lowest SAD, then lowest raster index
-    const uint32_t kmul = L.key_mul;
-    uint32_t best = 0xffffffffu;
-#pragma unroll
-    for (int d = 0; d < D; ++d) best = min(best, acc[d] * kmul + static_cast<uint32_t>(d * WX));
-    best += static_cast<uint32_t>(lane);
-    best = min(best, ax * kmul + static_cast<uint32_t>(lane * WX + 32));
-    if (lane == 0) best = min(best, axx * kmul + static_cast<uint32_t>(32 * WX + 32));
+    // key = sad << 16 | (dy * WX + dx): lowest SAD, then lowest raster index
     const uint32_t key = __reduce_min_sync(0xffffffffu, best);
     if (lane == 0) {
-      const int k = static_cast<int>(key & 0xffffu);
-      const int dy = k / WX, dx = k - (k / WX) * WX;
-      int32_t* a = aux + blk_index * 3;
-      a[0] = dy + p.oy - p.cy;
-      a[1] = dx + p.ox - p.cx;
-      a[2] = static_cast<int32_t>(key >> 16);
+      uint32_t fin = key;
+      bool last = true;
+      if (WPB > 1) {  // the block's warps meet in a shared slot; the last one writes
+        atomicMin(&keys[ib], key);
+        __threadfence_block();
+        last = atomicAdd(&cnt[ib], 1u) == static_cast<uint32_t>(WPB - 1);
+        if (last) {
+          __threadfence_block();
+          fin = atomicExch(&keys[ib], 0xffffffffu);
+          cnt[ib] = 0u;
+        }
+      }
+      if (last) {
+        const int k = static_cast<int>(fin & 0xffffu);
+        const int dy = k / WX, dx = k - (k / WX) * WX;
+        int32_t* a = aux + blk_index * 3;
+        a[0] = dy + p.oy - p.cy;
+        a[1] = dx + p.ox - p.cx;
+        a[2] = static_cast<int32_t>(fin >> 16);
+      }
     }
   }
 }
@@ -661,7 +691,7 @@ sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, voi
                       smem_u32(cur0 + (buf ^ 1) * cur_words),
                       reinterpret_cast<uint8_t*>(cur0 + (buf ^ 1) * cur_words), bar0 + 8u * (buf ^ 1));
     if constexpr (WARP)
-      sad_tile_work_warp(L, out, aux, tile, curw, copies);
+      sad_tile_work_warp<WXC>(L, out, aux, tile, curw, copies, keys, cnt);
     else
       sad_tile_work<BLK, D, NBY, WXC>(L, out, aux, tile, curw, copies, keys, cnt, [] {});
   }
@@ -811,11 +841,12 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
   // warp-per-block mapping for the +/-16 search of 16x16 blocks (C2): 8-block
   // tiles, every lane busy (sad_tile_work_warp)
   const char* wme = getenv("MERIT_SAD_WARP");
-  const bool warp_mode = BLK == 16 && D == 33 && p.WX == 33 && p.WY == 33 && p.BX >= 8 && !(wme && wme[0] == '0');
+  const bool warp_mode = BLK == 16 && D == 33 && (p.WX == 33 || p.WX == 65) && p.WY == p.WX && p.BX >= 8 &&
+                         !(wme && wme[0] == '0');
   if (warp_mode) {
-    nt = 256;
+    nt = 8 * (p.WX - 1);  // 8 blocks x (WX - 1) / 32 warps
     L.TBX = 8;
-    L.items = 256;
+    L.items = nt;
   }
   L.n_tiles_x = (p.BX + L.TBX - 1) / L.TBX;
   L.span = L.TBX * BLK + p.WX - 1;
@@ -905,8 +936,8 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
   if constexpr (D == 33) {
     if constexpr (BLK == 16) {
       if (p.WX == 33) kern = nt == 512 ? sad_kernel<16, 33, 1, 512, 33> : sad_kernel<16, 33, 1, 256, 33>;
-      if (warp_mode) kern = sad_kernel<16, 33, 1, 256, 33, true>;
       if (p.WX == 65) kern = nt == 512 ? sad_kernel<16, 33, 1, 512, 65> : sad_kernel<16, 33, 1, 256, 65>;
+      if (warp_mode) kern = p.WX == 33 ? sad_kernel<16, 33, 1, 256, 33, true> : sad_kernel<16, 33, 1, 512, 65, true>;
     } else {
       if (p.WX == 65 && L.nby == 2) kern = nt == 512 ? sad_kernel<8, 33, 2, 512, 65> : sad_kernel<8, 33, 2, 256, 65>;
     }
