@@ -482,23 +482,24 @@ __device__ __forceinline__ void sad_tile_work(const SadLaunch& L, void* __restri
   }
 }
 
-// Warp-per-block matching for 16x16 blocks and a square window of 32k + 1
-// displacements per axis (WXC = 33: the +/-16 search of C2; 65: +/-32, C5):
-// the k warps of block b own its columns dx = 32 w + lane for every dy (dy
-// groups of D = 33 accumulators, the loop of sad_tile_work), and the last
-// column dx = 32k is split over the block's lanes: lane l of warp w also
-// matches (dy = 32 w + l, dx = 32k) in a 16-row side loop, and the corner
+// Warp-per-block matching for a square window of 32k + 1 displacements per
+// axis (WXC = 33: the +/-16 search of C2; 65: +/-32, C5): the k warps of a
+// block column own its columns dx = 32 w + lane for every dy (dy groups of
+// D = 33 accumulators per block row, the loop of sad_tile_work; NBY = 2
+// vertically adjacent 8x8 blocks share every loaded reference word), and the
+// last column dx = 32k is split over the lanes: lane l of warp w also
+// matches (dy = 32 w + l, dx = 32k) in a side loop, and the corner
 // (dy = 32k, dx = 32k) is shared by the last warp (two products per lane,
 // REDUX sum).  Every lane does useful work (C2: 231 of 256 lanes in the
-// (block, dx) mapping), tiles are 8 blocks wide (C2: 120 = 15 x 8, no
+// (block, dx) mapping), tiles are 8 block columns wide (C2: 120 = 15 x 8, no
 // partial tiles) and the argmin is a warp REDUX per block (plus one shared
 // atomic per warp when k = 2).
-template <int WXC>
+template <int BLK, int NBY, int WXC>
 __device__ __forceinline__ void sad_tile_work_warp(const SadLaunch& L, void* __restrict__ out,
                                                    int32_t* __restrict__ aux, int tile, const uint32_t* curw,
                                                    const uint32_t* copies, uint32_t* keys, uint32_t* cnt) {
-  constexpr int BLK = 16, D = 33, WX = WXC, WY = WXC, BWW = 4;
-  constexpr int WPB = (WX - 1) / 32;  // warps per block
+  constexpr int D = 33, WX = WXC, WY = WXC, BWW = BLK / 4;
+  constexpr int WPB = (WX - 1) / 32;  // warps per block column
   constexpr int G = (WY + D - 1) / D;
   const SadParams& p = L.p;
   const int cpw = L.cur_pitch / 4;
@@ -509,118 +510,147 @@ __device__ __forceinline__ void sad_tile_work_warp(const SadLaunch& L, void* __r
   int t2, tx;
   sad_tile_coords(tile, L.n_full_tiles, L.n_full_x, L.ntx_m, L.ntx_s, t2, tx);
   const int pair_i = static_cast<int>(fast_div(t2, L.byt_m, L.byt_s));
-  const int by = L.by0 + (t2 - pair_i * L.BYT);
+  const int by = L.by0 + (t2 - pair_i * L.BYT) * NBY;  // first block row of the tile
   const long long pair = pair_i;
   const int bx0 = tx * L.TBX;
   const int nb = min(L.TBX, p.BX - bx0);
   if (ib >= nb) return;  // warp-uniform
   const int dcur = L.tma ? (bx0 * BLK + p.cx) - floor16(bx0 * BLK + p.cx) : 0;
+  // current blocks in registers: block row n at staged rows n*BLK .., bytes dcur + ib*BLK
   const uint32_t* cb = curw + (dcur >> 2) + ib * BWW;
-  uint32_t cw[BLK][BWW];
-  if ((dcur & 15) == 0) {
+  uint32_t cw[NBY][BLK][BWW];
+  if (BWW == 4 && (dcur & 15) == 0) {
 #pragma unroll
-    for (int i = 0; i < BLK; ++i) {
-      const uint4 q4 = *reinterpret_cast<const uint4*>(cb + i * cpw);
-      cw[i][0] = q4.x; cw[i][1] = q4.y; cw[i][2] = q4.z; cw[i][3] = q4.w;
-    }
+    for (int n = 0; n < NBY; ++n)
+#pragma unroll
+      for (int i = 0; i < BLK; ++i) {
+        const uint4 q4 = *reinterpret_cast<const uint4*>(cb + (n * BLK + i) * cpw);
+        cw[n][i][0] = q4.x; cw[n][i][1 % BWW] = q4.y; cw[n][i][2 % BWW] = q4.z; cw[n][i][3 % BWW] = q4.w;
+      }
   } else {
 #pragma unroll
-    for (int i = 0; i < BLK; ++i)
+    for (int n = 0; n < NBY; ++n)
 #pragma unroll
-      for (int j = 0; j < BWW; ++j) cw[i][j] = cb[i * cpw + j];
+      for (int i = 0; i < BLK; ++i)
+#pragma unroll
+        for (int j = 0; j < BWW; ++j) cw[n][i][j] = cb[(n * BLK + i) * cpw + j];
   }
   const long long blk_index = (pair * p.BY + by) * (long long)p.BX + bx0 + ib;
-  const long long blk_base = blk_index * (long long)(WY * WX);
-  const bool store = p.write_map && by < L.by1;
   const uint32_t kmul = L.key_mul;
-  uint32_t best = 0xffffffffu;
+  uint32_t best[NBY];
+#pragma unroll
+  for (int n = 0; n < NBY; ++n) best[n] = 0xffffffffu;
   const int col = ib * BLK + dxl;  // byte column of this lane's dx in the staged window
 #pragma unroll 1
   for (int ig = 0; ig < G; ++ig) {
     const uint32_t* cp = copies + (col & 3) * L.CS + (col >> 2) + ig * D * L.Ww;
-    uint32_t acc[D];
+    uint32_t acc[NBY][D];
 #pragma unroll
-    for (int d = 0; d < D; ++d) acc[d] = 0;
+    for (int n = 0; n < NBY; ++n)
 #pragma unroll
-    for (int r = 0; r < D + BLK - 1; ++r) {
+      for (int d = 0; d < D; ++d) acc[n][d] = 0;
+#pragma unroll
+    for (int r = 0; r < D + NBY * BLK - 1; ++r) {
       uint32_t rwv[BWW];
 #pragma unroll
       for (int j = 0; j < BWW; ++j) rwv[j] = cp[j];
       cp += L.Ww;
 #pragma unroll
-      for (int d = 0; d < D; ++d) {
-        const int i = r - d;
-        if (i >= 0 && i < BLK) {
+      for (int n = 0; n < NBY; ++n)
 #pragma unroll
-          for (int j = 0; j < BWW; ++j) acc[d] = vabsdiff4_acc(cw[i][j], rwv[j], acc[d]);
+        for (int d = 0; d < D; ++d) {
+          const int i = r - d - n * BLK;
+          if (i >= 0 && i < BLK) {
+#pragma unroll
+            for (int j = 0; j < BWW; ++j) acc[n][d] = vabsdiff4_acc(cw[n][i][j], rwv[j], acc[n][d]);
+          }
         }
-      }
     }
     // the last group of a 65-row window has 32 rows (65 = 33 + 32)
     const int nd = (ig + 1) * D <= WY ? D : WY - ig * D;
-    uint32_t bn = 0xffffffffu;
-    if (nd == D) {
 #pragma unroll
-      for (int d = 0; d < D; ++d) bn = min(bn, acc[d] * kmul + static_cast<uint32_t>(d * WX));
-      if (store) sad_store_map<D>(out, p.out_f32, blk_base + ig * D * WX + dxl, WX, acc, D);
-    } else {
+    for (int n = 0; n < NBY; ++n) {
+      const bool store = p.write_map && by + n < L.by1;
+      const long long obase = ((blk_index + n * (long long)p.BX) * WY + ig * D) * WX + dxl;
+      uint32_t bn = 0xffffffffu;
+      if (nd == D) {
 #pragma unroll
-      for (int d = 0; d < D - 1; ++d) bn = min(bn, acc[d] * kmul + static_cast<uint32_t>(d * WX));
-      if (store) sad_store_map<D>(out, p.out_f32, blk_base + ig * D * WX + dxl, WX, acc, D - 1);
+        for (int d = 0; d < D; ++d) bn = min(bn, acc[n][d] * kmul + static_cast<uint32_t>(d * WX));
+        if (store) sad_store_map<D>(out, p.out_f32, obase, WX, acc[n], D);
+      } else {
+#pragma unroll
+        for (int d = 0; d < D - 1; ++d) bn = min(bn, acc[n][d] * kmul + static_cast<uint32_t>(d * WX));
+        if (store) sad_store_map<D>(out, p.out_f32, obase, WX, acc[n], D - 1);
+      }
+      best[n] = min(best[n], bn + static_cast<uint32_t>(ig * D * WX + dxl));
     }
-    best = min(best, bn + static_cast<uint32_t>(ig * D * WX + dxl));
   }
-  // the last column dx = 32k (byte column ib*16 + 32k: a multiple of 4,
-  // shifted copy 0): this lane takes dy = dxl, reading staged rows dxl .. dxl + 15
+  // the last column dx = 32k (byte column ib*BLK + 32k: a multiple of 4,
+  // shifted copy 0): this lane takes dy = dxl; block row n reads staged rows
+  // dxl + n*BLK ..
   const int colx = ib * BLK + (WX - 1);
-  uint32_t ax = 0;
-  {
-    const uint32_t* cx = copies + (colx & 3) * L.CS + (colx >> 2) + dxl * L.Ww;
+  const uint32_t* cx0 = copies + (colx & 3) * L.CS + (colx >> 2);
+#pragma unroll
+  for (int n = 0; n < NBY; ++n) {
+    uint32_t ax = 0;
+    const uint32_t* cx = cx0 + (dxl + n * BLK) * L.Ww;
 #pragma unroll
     for (int i = 0; i < BLK; ++i) {
 #pragma unroll
-      for (int j = 0; j < BWW; ++j) ax = vabsdiff4_acc(cw[i][j], cx[j], ax);
+      for (int j = 0; j < BWW; ++j) ax = vabsdiff4_acc(cw[n][i][j], cx[j], ax);
       cx += L.Ww;
     }
-  }
-  best = min(best, ax * kmul + static_cast<uint32_t>(dxl * WX + (WX - 1)));
-  if (wsub == WPB - 1) {
-    // corner (dy = 32k, dx = 32k): lane l takes block row l >> 1, words 2 (l & 1) .. + 1
-    const int i = lane >> 1, j0 = 2 * (lane & 1);
-    const uint32_t* cr = copies + (colx & 3) * L.CS + (colx >> 2) + (WY - 1 + i) * L.Ww + j0;
-    uint32_t v = vabsdiff4_acc(cb[i * cpw + j0], cr[0], 0u);
-    v = vabsdiff4_acc(cb[i * cpw + j0 + 1], cr[1], v);
-    const uint32_t axx = __reduce_add_sync(0xffffffffu, v);
-    if (lane == 0) best = min(best, axx * kmul + static_cast<uint32_t>((WY - 1) * WX + (WX - 1)));
-    if (store && lane == 0) {
-      if (p.out_f32) __stcs(static_cast<float*>(out) + blk_base + (WY - 1) * WX + (WX - 1), static_cast<float>(axx));
-      else __stcs(static_cast<int32_t*>(out) + blk_base + (WY - 1) * WX + (WX - 1), static_cast<int32_t>(axx));
+    best[n] = min(best[n], ax * kmul + static_cast<uint32_t>(dxl * WX + (WX - 1)));
+    const long long bb = (blk_index + n * (long long)p.BX) * (long long)(WY * WX);
+    if (p.write_map && by + n < L.by1) {
+      if (p.out_f32) __stcs(static_cast<float*>(out) + bb + dxl * WX + (WX - 1), static_cast<float>(ax));
+      else __stcs(static_cast<int32_t*>(out) + bb + dxl * WX + (WX - 1), static_cast<int32_t>(ax));
+    }
+    if (wsub == WPB - 1) {
+      // corner (dy = 32k, dx = 32k): BLK x BWW words over the 32 lanes
+      constexpr int PER = BLK * BWW / 32;  // words per lane: 2 (16x16) or 0 (8x8: 16 lanes, one word)
+      uint32_t v = 0;
+      if constexpr (PER >= 1) {
+        const int i = lane / (BWW / PER), j0 = PER * (lane % (BWW / PER));
+#pragma unroll
+        for (int q = 0; q < PER; ++q)
+          v = vabsdiff4_acc(cb[(n * BLK + i) * cpw + j0 + q], cx0[(WY - 1 + n * BLK + i) * L.Ww + j0 + q], v);
+      } else if (lane < BLK * BWW) {
+        const int i = lane / BWW, j = lane % BWW;
+        v = vabsdiff4_acc(cb[(n * BLK + i) * cpw + j], cx0[(WY - 1 + n * BLK + i) * L.Ww + j], 0u);
+      }
+      const uint32_t axx = __reduce_add_sync(0xffffffffu, v);
+      if (lane == 0) best[n] = min(best[n], axx * kmul + static_cast<uint32_t>((WY - 1) * WX + (WX - 1)));
+      if (p.write_map && by + n < L.by1 && lane == 0) {
+        if (p.out_f32) __stcs(static_cast<float*>(out) + bb + (WY - 1) * WX + (WX - 1), static_cast<float>(axx));
+        else __stcs(static_cast<int32_t*>(out) + bb + (WY - 1) * WX + (WX - 1), static_cast<int32_t>(axx));
+      }
     }
   }
-  if (store) {
-    if (p.out_f32) __stcs(static_cast<float*>(out) + blk_base + dxl * WX + (WX - 1), static_cast<float>(ax));
-    else __stcs(static_cast<int32_t*>(out) + blk_base + dxl * WX + (WX - 1), static_cast<int32_t>(ax));
-  }
-  if (p.argmin && by < L.by1) {
+  if (p.argmin) {
     // key = sad << 16 | (dy * WX + dx): lowest SAD, then lowest raster index
-    const uint32_t key = __reduce_min_sync(0xffffffffu, best);
-    if (lane == 0) {
+#pragma unroll
+    for (int n = 0; n < NBY; ++n) {
+      if (by + n >= L.by1) break;
+      const uint32_t key = __reduce_min_sync(0xffffffffu, best[n]);
+      if (lane != 0) continue;
       uint32_t fin = key;
       bool last = true;
       if (WPB > 1) {  // the block's warps meet in a shared slot; the last one writes
-        atomicMin(&keys[ib], key);
+        const int slot = n * L.TBX + ib;
+        atomicMin(&keys[slot], key);
         __threadfence_block();
-        last = atomicAdd(&cnt[ib], 1u) == static_cast<uint32_t>(WPB - 1);
+        last = atomicAdd(&cnt[slot], 1u) == static_cast<uint32_t>(WPB - 1);
         if (last) {
           __threadfence_block();
-          fin = atomicExch(&keys[ib], 0xffffffffu);
-          cnt[ib] = 0u;
+          fin = atomicExch(&keys[slot], 0xffffffffu);
+          cnt[slot] = 0u;
         }
       }
       if (last) {
         const int k = static_cast<int>(fin & 0xffffu);
         const int dy = k / WX, dx = k - (k / WX) * WX;
-        int32_t* a = aux + blk_index * 3;
+        int32_t* a = aux + (blk_index + n * (long long)p.BX) * 3;
         a[0] = dy + p.oy - p.cy;
         a[1] = dx + p.ox - p.cx;
         a[2] = static_cast<int32_t>(fin >> 16);
@@ -691,7 +721,7 @@ sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, voi
                       smem_u32(cur0 + (buf ^ 1) * cur_words),
                       reinterpret_cast<uint8_t*>(cur0 + (buf ^ 1) * cur_words), bar0 + 8u * (buf ^ 1));
     if constexpr (WARP)
-      sad_tile_work_warp<WXC>(L, out, aux, tile, curw, copies, keys, cnt);
+      sad_tile_work_warp<BLK, NBY, WXC>(L, out, aux, tile, curw, copies, keys, cnt);
     else
       sad_tile_work<BLK, D, NBY, WXC>(L, out, aux, tile, curw, copies, keys, cnt, [] {});
   }
@@ -841,8 +871,8 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
   // warp-per-block mapping for the +/-16 search of 16x16 blocks (C2): 8-block
   // tiles, every lane busy (sad_tile_work_warp)
   const char* wme = getenv("MERIT_SAD_WARP");
-  const bool warp_mode = BLK == 16 && D == 33 && (p.WX == 33 || p.WX == 65) && p.WY == p.WX && p.BX >= 8 &&
-                         !(wme && wme[0] == '0');
+  const bool warp_mode = D == 33 && (BLK == 16 ? (p.WX == 33 || p.WX == 65) : p.WX == 65) && p.WY == p.WX &&
+                         p.BX >= 8 && !(wme && wme[0] == '0');
   if (warp_mode) {
     nt = 8 * (p.WX - 1);  // 8 blocks x (WX - 1) / 32 warps
     L.TBX = 8;
@@ -940,6 +970,7 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
       if (warp_mode) kern = p.WX == 33 ? sad_kernel<16, 33, 1, 256, 33, true> : sad_kernel<16, 33, 1, 512, 65, true>;
     } else {
       if (p.WX == 65 && L.nby == 2) kern = nt == 512 ? sad_kernel<8, 33, 2, 512, 65> : sad_kernel<8, 33, 2, 256, 65>;
+      if (warp_mode) kern = L.nby == 2 ? sad_kernel<8, 33, 2, 512, 65, true> : sad_kernel<8, 33, 1, 512, 65, true>;
     }
   }
   if (const char* we = getenv("MERIT_SAD_WXC"); we && we[0] == '0' && !warp_mode) {  // A/B: runtime width
