@@ -494,10 +494,11 @@ __device__ __forceinline__ void sad_tile_work(const SadLaunch& L, void* __restri
 // (block, dx) mapping), tiles are 8 block columns wide (C2: 120 = 15 x 8, no
 // partial tiles) and the argmin is a warp REDUX per block (plus one shared
 // atomic per warp when k = 2).
-template <int BLK, int NBY, int WXC>
+template <int BLK, int NBY, int WXC, typename AfterCw>
 __device__ __forceinline__ void sad_tile_work_warp(const SadLaunch& L, void* __restrict__ out,
                                                    int32_t* __restrict__ aux, int tile, const uint32_t* curw,
-                                                   const uint32_t* copies, uint32_t* keys, uint32_t* cnt) {
+                                                   const uint32_t* copies, uint32_t* keys, uint32_t* cnt,
+                                                   AfterCw after_cw) {
   constexpr int D = 33, WX = WXC, WY = WXC, BWW = BLK / 4;
   constexpr int WPB = (WX - 1) / 32;  // warps per block column
   constexpr int G = (WY + D - 1) / D;
@@ -514,7 +515,10 @@ __device__ __forceinline__ void sad_tile_work_warp(const SadLaunch& L, void* __r
   const long long pair = pair_i;
   const int bx0 = tx * L.TBX;
   const int nb = min(L.TBX, p.BX - bx0);
-  if (ib >= nb) return;  // warp-uniform
+  if (ib >= nb) {  // warp-uniform
+    after_cw();
+    return;
+  }
   const int dcur = L.tma ? (bx0 * BLK + p.cx) - floor16(bx0 * BLK + p.cx) : 0;
   // current blocks in registers: block row n at staged rows n*BLK .., bytes dcur + ib*BLK
   const uint32_t* cb = curw + (dcur >> 2) + ib * BWW;
@@ -535,6 +539,23 @@ __device__ __forceinline__ void sad_tile_work_warp(const SadLaunch& L, void* __r
 #pragma unroll
         for (int j = 0; j < BWW; ++j) cw[n][i][j] = cb[(n * BLK + i) * cpw + j];
   }
+  // the corner's current-block words (lane-dependent rows: not from cw), read
+  // before the staged rows are released
+  constexpr int PER = BLK * BWW / 32;  // words per lane: 2 (16x16) or 0 (8x8: 16 lanes, one word)
+  uint32_t ccw[NBY][PER >= 1 ? PER : 1];
+  if (wsub == WPB - 1) {
+#pragma unroll
+    for (int n = 0; n < NBY; ++n) {
+      if constexpr (PER >= 1) {
+        const int i = lane / (BWW / PER), j0 = PER * (lane % (BWW / PER));
+#pragma unroll
+        for (int q = 0; q < PER; ++q) ccw[n][q] = cb[(n * BLK + i) * cpw + j0 + q];
+      } else {
+        ccw[n][0] = lane < BLK * BWW ? cb[(n * BLK + lane / BWW) * cpw + lane % BWW] : 0u;
+      }
+    }
+  }
+  after_cw();
   const long long blk_index = (pair * p.BY + by) * (long long)p.BX + bx0 + ib;
   const uint32_t kmul = L.key_mul;
   uint32_t best[NBY];
@@ -608,16 +629,14 @@ __device__ __forceinline__ void sad_tile_work_warp(const SadLaunch& L, void* __r
     }
     if (wsub == WPB - 1) {
       // corner (dy = 32k, dx = 32k): BLK x BWW words over the 32 lanes
-      constexpr int PER = BLK * BWW / 32;  // words per lane: 2 (16x16) or 0 (8x8: 16 lanes, one word)
       uint32_t v = 0;
       if constexpr (PER >= 1) {
         const int i = lane / (BWW / PER), j0 = PER * (lane % (BWW / PER));
 #pragma unroll
-        for (int q = 0; q < PER; ++q)
-          v = vabsdiff4_acc(cb[(n * BLK + i) * cpw + j0 + q], cx0[(WY - 1 + n * BLK + i) * L.Ww + j0 + q], v);
+        for (int q = 0; q < PER; ++q) v = vabsdiff4_acc(ccw[n][q], cx0[(WY - 1 + n * BLK + i) * L.Ww + j0 + q], v);
       } else if (lane < BLK * BWW) {
         const int i = lane / BWW, j = lane % BWW;
-        v = vabsdiff4_acc(cb[(n * BLK + i) * cpw + j], cx0[(WY - 1 + n * BLK + i) * L.Ww + j], 0u);
+        v = vabsdiff4_acc(ccw[n][0], cx0[(WY - 1 + n * BLK + i) * L.Ww + j], 0u);
       }
       const uint32_t axx = __reduce_add_sync(0xffffffffu, v);
       if (lane == 0) best[n] = min(best[n], axx * kmul + static_cast<uint32_t>((WY - 1) * WX + (WX - 1)));
@@ -721,7 +740,7 @@ sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, voi
                       smem_u32(cur0 + (buf ^ 1) * cur_words),
                       reinterpret_cast<uint8_t*>(cur0 + (buf ^ 1) * cur_words), bar0 + 8u * (buf ^ 1));
     if constexpr (WARP)
-      sad_tile_work_warp<BLK, NBY, WXC>(L, out, aux, tile, curw, copies, keys, cnt);
+      sad_tile_work_warp<BLK, NBY, WXC>(L, out, aux, tile, curw, copies, keys, cnt, [] {});
     else
       sad_tile_work<BLK, D, NBY, WXC>(L, out, aux, tile, curw, copies, keys, cnt, [] {});
   }
@@ -729,19 +748,20 @@ sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, voi
 }
 
 // Barrier-free variant for TMA staging: the warps of a CTA run their tiles
-// without ever meeting at a CTA barrier in steady state.  Staging buffers
-// (raw window + current rows) are double-buffered and the shifted copies
+// without ever meeting at a CTA barrier in steady state.  The raw window is
+// single-buffered, the current rows double-buffered and the shifted copies
 // triple-buffered; after finishing tile k a warp builds its share of tile
 // k + 2's copies, then starts tile k + 1, whose copies every warp finished
 // one tile earlier.  So the copy building, the epilogue and the staging
 // waits of one warp overlap the VABSDIFF4 streams of the others instead of
 // being aligned across the SM by tile barriers.
-//   tma[b]  (b = k % 2): TMA of tile k landed in raw[b] / cur[b]
+//   tma[b]  (b = k % 2): TMA of tile k landed in raw / cur[b]
 //   full[c] (c = k % 3): all threads built their share of copies[c] for tile k
 //   done[c]:             all threads finished tile k's matching (copies[c] free)
 // The last warp to load its current blocks of tile k issues tile k + 2's TMA
-// into raw / cur[b] (every build from raw[b] for tile k came before full[c]).
-template <int BLK, int D, int NBY, int NT, int WXC>
+// into raw / cur[b]: every thread built its share of tile k + 1 (the last
+// reader of raw) before it started tile k.
+template <int BLK, int D, int NBY, int NT, int WXC, bool WARP = false>
 __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1)
 sad_async_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, void* __restrict__ out,
                  int32_t* __restrict__ aux, SadLaunch L, const __grid_constant__ CUtensorMap ref_map,
@@ -749,9 +769,9 @@ sad_async_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ re
   extern __shared__ __align__(128) uint8_t smem_b[];
   const int raw_words = static_cast<int>(L.raw_buf / 4);
   const int cur_words = static_cast<int>(L.cur_buf / 4);
-  // --- carve-up: raw[2] | cur[2] | copies[3 x 4] | keys[2] | cnt[2] | ctr[2] | mbarriers tma[2] full[3] done[3]
+  // --- carve-up: raw | cur[2] | copies[3 x 4] | keys[2] | cnt[2] | ctr[2] | mbarriers tma[2] full[3] done[3]
   uint32_t* raw0 = reinterpret_cast<uint32_t*>(smem_b + ((128u - (smem_u32(smem_b) & 127u)) & 127u));
-  uint32_t* cur0 = raw0 + 2 * raw_words;
+  uint32_t* cur0 = raw0 + raw_words;
   uint32_t* copies0 = cur0 + 2 * cur_words;
   const int nslot = NBY * L.TBX;
   uint32_t* keys0 = copies0 + 12 * L.CS;
@@ -783,31 +803,32 @@ sad_async_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ re
   const int first = blockIdx.x, step = gridDim.x;
   const int nk = first < L.n_tiles ? (L.n_tiles - 1 - first) / step + 1 : 0;  // tiles of this CTA
   auto tile_of = [&](int k) { return first + k * step; };
-  auto issue = [&](int k) {  // one thread: TMA of tile k into buffer k % 2
+  auto issue = [&](int k) {  // one thread: TMA of tile k into raw / cur[k % 2]
     const int b = k & 1;
-    issue_tile_tma<BLK>(L, &ref_map, &cur_map, tile_of(k), smem_u32(raw0 + b * raw_words),
-                        smem_u32(cur0 + b * cur_words), bar_tma + 8u * b);
+    issue_tile_tma<BLK>(L, &ref_map, &cur_map, tile_of(k), smem_u32(raw0), smem_u32(cur0 + b * cur_words),
+                        bar_tma + 8u * b);
   };
   auto arrive = [](uint32_t bar) { asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory"); };
   auto build = [&](int k) {  // this thread's share of tile k's copies
     const int b = k & 1, c = k % 3;
     if (k >= 3) sad_mbar_wait(bar_done + 8u * c, static_cast<uint32_t>((k - 3) / 3) & 1u);  // copies[c] free
     sad_mbar_wait(bar_tma + 8u * b, static_cast<uint32_t>(k >> 1) & 1u);
-    sad_build_copies<BLK>(L, tile_of(k), raw0 + b * raw_words, copies0 + c * 4 * L.CS, cp_r0, cp_w0);
+    sad_build_copies<BLK>(L, tile_of(k), raw0, copies0 + c * 4 * L.CS, cp_r0, cp_w0);
     arrive(bar_full + 8u * c);
   };
-  if (threadIdx.x == 0) {
-    if (nk > 0) issue(0);
-    if (nk > 1) issue(1);
-  }
+  if (threadIdx.x == 0 && nk > 0) issue(0);
   if (nk > 0) build(0);
-  if (nk > 1) build(1);
+  if (nk > 1) {
+    if (threadIdx.x == 0) {  // raw is free once every thread built tile 0
+      sad_mbar_wait(bar_full, 0u);
+      issue(1);
+    }
+    build(1);
+  }
   for (int k = 0; k < nk; ++k) {
     const int b = k & 1, c = k % 3;
     sad_mbar_wait(bar_full + 8u * c, static_cast<uint32_t>(k / 3) & 1u);
-    sad_tile_work<BLK, D, NBY, WXC>(
-        L, out, aux, tile_of(k), cur0 + b * cur_words, copies0 + c * 4 * L.CS, keys0 + b * nslot,
-        cnt0 + b * nslot, [&] {
+    auto refill = [&] {
           // the last warp done with cur[b] for tile k refills buffer b with tile k + 2
           __syncwarp();
           if ((threadIdx.x & 31) == 0) {
@@ -818,7 +839,13 @@ sad_async_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ re
               if (k + 2 < nk) issue(k + 2);
             }
           }
-        });
+        };
+    if constexpr (WARP)
+      sad_tile_work_warp<BLK, NBY, WXC>(L, out, aux, tile_of(k), cur0 + b * cur_words, copies0 + c * 4 * L.CS,
+                                        keys0 + b * nslot, cnt0 + b * nslot, refill);
+    else
+      sad_tile_work<BLK, D, NBY, WXC>(L, out, aux, tile_of(k), cur0 + b * cur_words, copies0 + c * 4 * L.CS,
+                                      keys0 + b * nslot, cnt0 + b * nslot, refill);
     arrive(bar_done + 8u * c);
     if (k + 2 < nk) build(k + 2);
   }
@@ -954,10 +981,10 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
   if (L.n_tiles == 0) return MERIT_OK;
   if (smem > smem_cap) return fail(MERIT_E_UNSUPPORTED_VIEW, "SAD footprint exceeds shared memory");
   // barrier-free variant (TMA staging): two staging buffers, three copy buffers
-  const size_t smem_async = 128 + 2ull * L.raw_buf + 2ull * L.cur_buf +
+  const size_t smem_async = 128 + 1ull * L.raw_buf + 2ull * L.cur_buf +
                             4ull * (12ull * L.CS + 4ull * L.nby * L.TBX + 2) + 8 + 64;
   const char* ae = getenv("MERIT_SAD_ASYNC");
-  const bool use_async = !warp_mode && L.tma && !(ae && ae[0] == '0') && smem_async <= smem_cap;
+  const bool use_async = L.tma && !(ae && ae[0] == '0') && smem_async <= smem_cap;
   auto kern = nt == 512 ? sad_kernel<BLK, D, 1, 512, 0> : sad_kernel<BLK, D, 1, 256, 0>;
   if constexpr (BLK == 8) {
     if (L.nby == 2) kern = nt == 512 ? sad_kernel<BLK, D, 2, 512, 0> : sad_kernel<BLK, D, 2, 256, 0>;
@@ -1001,6 +1028,15 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
       }
     }
 #undef MERIT_SAD_ASYNC_OF
+    if constexpr (D == 33) {
+      if constexpr (BLK == 16) {
+        if (kern == sad_kernel<16, 33, 1, 256, 33, true>) kern = sad_async_kernel<16, 33, 1, 256, 33, true>;
+        if (kern == sad_kernel<16, 33, 1, 512, 65, true>) kern = sad_async_kernel<16, 33, 1, 512, 65, true>;
+      } else {
+        if (kern == sad_kernel<8, 33, 2, 512, 65, true>) kern = sad_async_kernel<8, 33, 2, 512, 65, true>;
+        if (kern == sad_kernel<8, 33, 1, 512, 65, true>) kern = sad_async_kernel<8, 33, 1, 512, 65, true>;
+      }
+    }
   }
   const size_t smem_launch = use_async ? smem_async : smem;
   cudaError_t e = set_smem_attr(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1024,7 +1060,8 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
   e = launch_pdl(kern, dim3(static_cast<unsigned>(grid)), dim3(threads), smem_launch, s, 1, cur, ref, out, aux, L,
                  ref_map, cur_map);
   if (e != cudaSuccess) return cuda_check(e, "launch(sad)");
-  return launch_status(warp_mode ? "sad_kernel<warp per block>" : (use_async ? "sad_async_kernel" : "sad_kernel"));
+  return launch_status(warp_mode ? (use_async ? "sad_async_kernel<warp per block>" : "sad_kernel<warp per block>")
+                                 : (use_async ? "sad_async_kernel" : "sad_kernel"));
 }
 
 }  // namespace
