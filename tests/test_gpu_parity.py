@@ -12,6 +12,7 @@ import pytest
 from oracle import binding as O
 from paper_1911_03458_b200 import (FLAG_ARGMIN, FLAG_EXACT, FLAG_FAST_BF16, FLAG_NO_MAP, Boundary,
                                    Error, ErrorCode, Kernel, Plan, run_full, run_full_argmin)
+from paper_1911_03458_b200 import _capi
 from paper_1911_03458_b200 import workloads as W
 
 pytestmark = pytest.mark.gpu
@@ -133,6 +134,38 @@ def test_sad_staging_modes_unaligned_windows(cuda, monkeypatch, mode, blk):
         want = O.me_sad(cur, ref, blk, r)
         assert np.array_equal(sad, want), (h, wd, r)
         assert np.array_equal(mv, O.me_argmin(want, r)), (h, wd, r)
+
+
+# warp-per-block kernels (16x16 +/-16 and +/-32, 8x8 +/-32, >= 8 block columns)
+# on every staging path: TMA (ZERO_PAD), cp.async words (CLAMP), bytes
+# (unaligned width), with ragged tiles, odd block rows and a pair axis
+@pytest.mark.parametrize("h,wd,blk,r,boundary,pairs", [
+    (64, 160, 16, 16, Boundary.ZeroPad, 2),   # 10 block columns: a 2-block tail tile
+    (48, 128, 16, 16, Boundary.Clamp, 1),     # cp.async word staging
+    (40, 131, 16, 16, Boundary.ZeroPad, 1),   # unaligned width: byte staging
+    (96, 144, 16, 32, Boundary.ZeroPad, 1),   # two warps per block
+    (64, 128, 16, 32, Boundary.Clamp, 1),
+    (88, 96, 8, 32, Boundary.ZeroPad, 2),     # 8x8, 11 block rows: odd pair of rows
+    (72, 72, 8, 32, Boundary.Clamp, 1),
+])
+def test_sad_warp_per_block_paths(cuda, h, wd, blk, r, boundary, pairs):
+    if pairs > 1:
+        cur = np.empty((pairs, h, wd), np.uint8)
+        ref = np.empty((pairs, h, wd), np.uint8)
+        for i in range(pairs):
+            cur[i], ref[i] = W.gen_me_pair(h, wd, 40 + i, blk, min(r, 16), 4)
+    else:
+        cur, ref = W.gen_me_pair(h, wd, 40, blk, min(r, 16), 4)
+    w = W.me_view(h, wd, blk, r, pairs=pairs if pairs > 1 else None)
+    w.view_b.boundary = boundary
+    w.src_a, w.src_b = cur, ref
+    sad, mv = run_full_argmin(w)
+    assert "warp per block" in _capi.load().merit_dev_last_kernel().decode()
+    want = O.me_sad(cur, ref, blk, r, clamp=boundary == Boundary.Clamp)
+    assert np.array_equal(sad, want)
+    assert np.array_equal(mv, O.me_argmin(want, r))
+    w.dtype_out = W.Dtype.Real32
+    assert np.array_equal(run_full(w), want.astype(np.float32))
 
 
 def test_sad_ties_lowest_raster(cuda):
