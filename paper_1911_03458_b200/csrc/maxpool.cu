@@ -336,15 +336,21 @@ merit_status launch_maxpool(const merit_plan& plan, const void* a, void* out, vo
       const long long fit = st28 <= 200 * 1024 ? std::min<long long>(7, (227 * 1024) / (st28 + 1024)) : 0;
       const long long items28 = p.planes * ((p.Ho + 27) / 28);
       if (p.Ho >= 28 && fit > 0 && items28 <= num_sms() * fit) RBv = 28;
+      // smaller launches still: 14-row bands (29 input rows, 13 KB), one per
+      // 4-warp CTA, 12 resident per SM (C1: 2,048 bands, 6.47-6.65 us vs
+      // 6.72 us for the 28-row shape on the same box)
+      const size_t st14 = ((size_t)29 * p.W * 4 + 127) / 128 * 128;
+      const long long items14 = p.planes * ((p.Ho + 13) / 14);
+      if (p.Ho >= 14 && st14 <= 16 * 1024 && items14 <= num_sms() * 14LL) RBv = 14;
     }
     if (const char* re = getenv("MERIT_MP_RB")) {
       const int v = atoi(re);
-      RBv = (v == 4 || v == 16 || v == 28 || v == 56) ? v : 8;
+      RBv = (v == 4 || v == 14 || v == 16 || v == 28 || v == 56) ? v : 8;
     }
     const int nband = (p.Ho + RBv - 1) / RBv;
     const long long items = p.planes * nband;
     if (items >= (1LL << 31)) return fail(MERIT_E_UNSUPPORTED_VIEW, "too many max-pool bands for one launch");
-    int ctas = 7;
+    int ctas = RBv == 14 ? 14 : 7;  // 14-row bands: one band per CTA
     if (const char* ce = getenv("MERIT_MP_CTAS")) ctas = atoi(ce);
     const size_t stage = ((size_t)(2 * RBv + 1) * p.W * 4 + 127) / 128 * 128;
     int ns = RBv == 4 ? 8 : (RBv == 8 ? 4 : (RBv == 16 ? 2 : 1));
@@ -378,6 +384,11 @@ merit_status launch_maxpool(const merit_plan& plan, const void* a, void* out, vo
       if (RBv == 16) k = tm ? maxpool3s2_bulk_kernel<128, 16, true> : maxpool3s2_bulk_kernel<128, 16, false>;
       if (RBv == 28) k = tm ? maxpool3s2_bulk_kernel<128, 28, true> : maxpool3s2_bulk_kernel<128, 28, false>;
       if (RBv == 56) k = tm ? maxpool3s2_bulk_kernel<128, 56, true> : maxpool3s2_bulk_kernel<128, 56, false>;
+      if (RBv == 14) {  // 4 warps (MERIT_MP_NT=256: 8)
+        const char* ne = getenv("MERIT_MP_NT");
+        k = (ne && atoi(ne) == 256) ? (tm ? maxpool3s2_bulk_kernel<256, 14, true> : maxpool3s2_bulk_kernel<256, 14, false>)
+                                    : (tm ? maxpool3s2_bulk_kernel<128, 14, true> : maxpool3s2_bulk_kernel<128, 14, false>);
+      }
       // 28-row bands: 8 warps per CTA (a band's 392 16-byte output groups in
       // two passes instead of four shortens every CTA's compute-and-store
       // tail) and exactly 6 CTAs per SM (dynamic shared memory padded to 32
@@ -399,6 +410,10 @@ merit_status launch_maxpool(const merit_plan& plan, const void* a, void* out, vo
       pp.vec_out = (p.Wo % 4 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
       pp.pf = ns;
       if (const char* pe = getenv("MERIT_MP_PF")) pp.pf = atoi(pe) < 0 ? (1 << 30) : atoi(pe);
+      if (RBv == 14) {
+        const char* ne = getenv("MERIT_MP_NT");
+        nt = (ne && atoi(ne) == 256) ? 256 : 128;
+      }
       e = launch_pdl(k, dim3(static_cast<unsigned>(grid)), dim3(nt), smem, s, 1, in, o, pp, nband,
                      static_cast<int>(items), ns,
                      rmap);

@@ -50,6 +50,8 @@ def test_maxpool_c1_full_bit_exact(cuda):
     ((3, 5, 17, 23), 3, 2, 1, Boundary.Clamp),
     ((2, 3, 16, 16), 3, 2, 1, Boundary.Clamp),   # fast path, odd plane count
     ((1, 2, 9, 300), 3, 2, 1, Boundary.Clamp),   # W > 128: multi-segment fast path
+    ((2, 8, 60, 60), 3, 2, 1, Boundary.Clamp),   # 14-row bands, ragged last band, Wo % 4 != 0
+    ((1, 4, 112, 64), 3, 2, 1, Boundary.Clamp),  # 14-row bands, 16-byte output stores
     ((2, 2, 11, 13), 2, 1, 0, Boundary.Clamp),
     ((2, 2, 11, 13), 3, 3, 1, Boundary.ZeroPad),
     ((1, 1, 7, 7), 5, 1, 2, Boundary.Clamp),
