@@ -1,35 +1,46 @@
 #!/usr/bin/env python
 """Benchmark of the MERIT device operator (BASELINE.json metric).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl ours|reference]
 
-A "step" is one pass of the hot path over one batch of synthetic input of the
-configuration (default C2 = BASELINE.json configs[1]: block-matching motion
-estimation on a 1920x1080 uint8 frame pair, 16x16 blocks, +/-16, int32 SAD map
-+ argmin with lowest-raster tie-break).  Metric: MERIT-op throughput = ranged
-inner products (= elements of the reference operator's output,
-prod(p_shape), engine.hpp:24-28) per second, in G/s.
+Metric: MERIT-op throughput = ranged inner products (= elements of the
+reference operator's output, prod(p_shape), engine.hpp:24-28) per second, in
+G/s, plus the binding roofline fraction of the dominant kernel.
 
-* ``value``: device-resident inputs, the kernel timed with CUDA events over
-  exactly K steps between a barrier + synchronize on both sides; input /
-  output buffer sets rotate so the working set exceeds the 126 MB L2.
+A "step" is one pass of the hot path over one batch of the configuration.
+Default config C5 (BASELINE.json configs[4], the largest configuration that
+fits one GPU): motion estimation over 64 pairs of 3840x2160 uint8 frames,
+16x16 and 8x8 blocks (the reference runs them as two Workloads), +/-32,
+argmin with the lowest-raster tie-break.  --config C1..C4 selects the others.
+
+* ``value``: device-resident inputs, the K steps timed with CUDA events on the
+  launching stream between a barrier + synchronize on both sides, the max
+  over ranks; input sets rotate / exceed the 126 MB L2.
 * ``e2e``: the same steps through the C-ABI host-buffer call
-  (merit_dev_run_host: pinned H2D of the inputs, kernel, D2H of the SAD map +
-  motion vectors) — the reference's run_full calling convention.
+  (merit_dev_run_host: pinned H2D of the inputs, kernels, D2H of the
+  results) — the reference's run_full calling convention.
 * ``roofline``: the dominant kernel's achieved rate vs the measured peak.
-* ``cpu_baseline``: the UNMODIFIED reference engine (oracle/_ref) on a
-  bounded sample, one process per host core (rank 0, N=1 only).
+* ``cpu_baseline``: the UNMODIFIED reference (oracle/_ref) on a bounded
+  sample, one process per host core (rank 0, N=1 only): merit::run_full, and
+  the reference's brute-force oracle loop as a second, labelled figure.
 
-Multi-GPU (torchrun): one process per GPU, each rank processes its own frame
-pair(s) (weak scaling, no collective on the data path); the timed region is
-bracketed by barriers and the max over ranks is reported.
+Multi-GPU: ``--gpus N`` without a torchrun environment re-launches itself
+under torch.distributed.run with N ranks (one process per GPU).  Every rank
+runs its own shard with no collective on the data path: C1 /
+C3 / C4 / C5 split their batch of images / frame pairs, C2 splits its one
+frame pair into block-row bands, each with the Eq. 6 footprint of its band
+(its rows plus the 16-row search halo, paper_1911_03458_b200/shard.py).
+NCCL carries only the barriers and the max-over-ranks timing.  ``--dry-run``
+runs the rank logic on CPU (gloo) and prints each rank's shard.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -43,6 +54,17 @@ sys.path.insert(0, str(ROOT))
 METRIC = "MERIT-op throughput (Goutputs/s) and % of HBM/tensor roofline at 1-8 B200"
 UNIT = "Goutputs/s"
 PROFILES = ROOT / "profiles"
+DATA = "synthetic (seeded SplitMix64 generators, SURVEY §8(d))"
+
+# config.workload: the same string in both arms
+WORKLOAD = {
+    "C1": "C1 max-pool 3x3 s2 p1 (-inf pad) fp32 NCHW (8,64,112,112)",
+    "C2": "C2 motion estimation 1920x1080 u8 pair, 16x16 blocks, +/-16, int32 SAD map + argmin",
+    "C3": "C3 conv fp32 NCHW (32,64,56,56) * (64,64,3,3) s1 p1",
+    "C4": "C4 conv bf16 NCHW (256,128,56,56) * (256,128,3,3) s2 p1, fp32 accumulate",
+    "C5": "C5 motion estimation 64 x 3840x2160 u8 pairs, 16x16 + 8x8 blocks, +/-32, argmin",
+}
+BATCH = {"C1": 8, "C2": 67, "C3": 32, "C4": 256, "C5": 64}   # units split over ranks (C2: block rows)
 
 
 def load_peaks():
@@ -122,149 +144,130 @@ class ClockSampler:
                 "samples": len(self.samples), "window": window}
 
 
+# --------------------------------------------------------------- shards ----
+def shard_for(config: str, rank: int, world: int, with_inputs: bool = True, seed_offset: int = 0):
+    """This rank's part of the config: (workloads, meta).
+
+    workloads: the Workload(s) one step runs (C5: the 16x16 and the 8x8
+    blocks, two Workloads over the same frames, as the reference runs them).
+    meta: the shard range and a description.  The same function serves the
+    GPU run and the --dry-run rank check."""
+    from paper_1911_03458_b200 import workloads as W
+    from paper_1911_03458_b200.shard import shard_band, shard_range, shard_workload
+    total = BATCH[config]
+    lo, hi = shard_range(total, world, rank)
+    if config == "C2":
+        w = W.config_workload("C2", with_inputs=with_inputs, seed_offset=seed_offset)
+        s, (lo, hi) = shard_band(w, world, rank) if world > 1 else (w, (0, total))
+        return [s], {"range": [lo, hi], "what": f"block rows [{lo}, {hi}) of the 67 (+ the Eq. 6 halo rows)"}
+    if config == "C5":
+        n = hi - lo
+        w16 = W.config_workload("C5", with_inputs=with_inputs, pairs=n, seed_offset=lo + seed_offset)
+        w8 = W.me_view(2160, 3840, 8, 32, pairs=n)
+        w8.src_a, w8.src_b = w16.src_a, w16.src_b
+        return [w16, w8], {"range": [lo, hi], "what": f"frame pairs [{lo}, {hi}) of the 64"}
+    # C1 / C3 / C4: the batch axis
+    w = W.config_workload(config, with_inputs=with_inputs, seed_offset=seed_offset)
+    if world > 1:
+        fp32 = getattr(w, "fp32_inputs", None)
+        w, (lo, hi) = shard_workload(w, world, rank)
+        if fp32 is not None:
+            w.fp32_inputs = (fp32[0][lo:hi], fp32[1])
+    name = {"C1": "images", "C3": "images", "C4": "images"}[config]
+    return [w], {"range": [lo, hi], "what": f"{name} [{lo}, {hi}) of the {total}"}
+
+
 # ------------------------------------------------------------- workloads ---
 class Case:
-    """One benchmark configuration bound to a device: rotating buffer sets."""
+    """One benchmark configuration bound to a device: plans + rotating buffers."""
 
     def __init__(self, config: str, rank: int, world: int, device):
         import torch
         from paper_1911_03458_b200 import FLAG_ARGMIN, FLAG_NO_MAP, Plan
-        from paper_1911_03458_b200 import workloads as W
         self.config = config
         self.torch = torch
         self.device = device
-        flags = 0
+        ws, self.meta = shard_for(config, rank, world)
+        flags = {"C2": FLAG_ARGMIN, "C5": FLAG_ARGMIN | FLAG_NO_MAP}.get(config, 0)
+        self.plans = [Plan(w, flags) for w in ws]
+        self.workloads = ws
+        w0 = ws[0]
+        a_bytes = int(self.plans[0].info.src_a_bytes) + int(self.plans[0].info.src_b_bytes)
+        out_bytes = sum(int(p.info.out_bytes) + 4 * int(p.info.aux_elems) for p in self.plans)
+        # rotating input / output sets: together > 2 x the 126 MB L2
+        per_set = a_bytes + out_bytes
+        nsets = max(1, min(8, -(-300_000_000 // max(1, per_set))))
         self.sets = []
-        if config == "C2":
-            w = W.config_workload("C2", with_inputs=False)
-            flags = FLAG_ARGMIN
-            self.plan = Plan(w, flags)
-            nsets = 8   # 8 x (4.1 MB in + 35 MB SAD map) = 314 MB > 2 x L2
-            for s in range(nsets):
-                cur, ref = W.gen_me_pair(1080, 1920, 2 + rank * 1000 + s)
-                self.sets.append(self._bufs(cur, ref))
-            self.cpu_inputs = (cur, ref)
-            self.units = "1 frame pair (1920x1080 u8) per rank per step"
-            self.workload = "C2 motion estimation 1080p, 16x16 blocks, +/-16, SAD map + argmin"
-            self.rotation = f"{nsets} rotating input/output sets ({nsets * 39.3:.0f} MB > 126 MB L2)"
-            self.dtype = "u8 (int32 SAD)"
-        elif config == "C1":
-            # batch-sharded (SURVEY §8(e)): 8 / world images per rank
-            w = W.config_workload("C1", scale=world, with_inputs=False)
-            n_img = w.view_a.p_shape[0]
-            self.plan = Plan(w)
-            nsets = 6 * max(1, 8 // n_img)
-            for s in range(nsets):
-                x = W.gen_uniform([n_img, 64, 112, 112], 1 + rank * 1000 + s)
-                self.sets.append(self._bufs(x, np.zeros(1, np.float32)))
-            self.cpu_inputs = (x, np.zeros(1, np.float32))
-            self.units = f"{n_img} of the 8 images (N,64,112,112) per rank per step"
-            self.workload = "C1 maxpool 3x3 s2 p1 fp32 NCHW (8,64,112,112)"
-            self.rotation = f"{nsets} rotating input/output sets ({nsets * 4.0 * n_img:.0f} MB > 126 MB L2)"
-            self.dtype = "f32"
-        elif config in ("C3", "C4"):
-            # C4 is batch-sharded over the GPUs (BASELINE configs[3]): 256 / world
-            # images per rank; C3 runs its 32 images on every rank
-            w = W.config_workload(config, scale=world if config == "C4" else 1, with_inputs=True,
-                                  seed_offset=rank * 1000)
-            n_img = w.view_a.p_shape[0]
-            self.plan = Plan(w)
-            # rotating device copies so the sets together exceed 2x L2 (C4
-            # shards at 8 GPUs are 51 MB)
-            nsets = 4 if config == "C3" else max(1, -(-300 // int(1.6 * n_img)))
-            a0, b0 = w.src_a, w.src_b
-            for s in range(nsets):
-                a = a0 if s == 0 else (W.gen_uniform(list(a0.shape), 3 + rank * 1000 + s)
-                                       if config == "C3" else a0)
-                self.sets.append(self._bufs(a, b0))
-            self.plan.pack_b(self.sets[0][1])
+        for s in range(nsets):
+            if s == 0:
+                a, b = w0.src_a, w0.src_b
+            elif config in ("C1", "C3"):
+                a, b = (np.ascontiguousarray(np.roll(w0.src_a, s, axis=-1)), w0.src_b)
+            elif config == "C2":
+                a, b = np.roll(w0.src_a, s, axis=-1), np.roll(w0.src_b, s, axis=-1)
+            else:  # C4 / C5 sets exceed L2 on their own; C4 at 8 GPUs: 51 MB per rank -> copies
+                a, b = w0.src_a, w0.src_b
+            self.sets.append(self._bufs(a, b))
+        if config in ("C3", "C4"):
+            self.plans[0].pack_b(self.sets[0][1])
             torch.cuda.synchronize()
-            self.cpu_inputs = (a0, b0)
-            self.units = ("32 images (32,64,56,56) fp32 per rank per step" if config == "C3"
-                          else f"{n_img} of the 256 images (N,128,56,56) bf16 per rank per step")
-            self.workload = W.CONFIGS[config]
-            self.rotation = (f"{nsets} rotating sets ({nsets * 51.5:.0f} MB > 126 MB L2)" if config == "C3"
-                             else f"{nsets} rotating set(s) of {1.6 * n_img:.0f} MB (> 126 MB L2 in total)")
-            self.dtype = "f32 (3-term bf16 split, fp32 accumulate)" if config == "C3" else "bf16 (fp32 accumulate)"
-        elif config == "C5":
-            pairs = max(1, 64 // world)
-            w = W.config_workload("C5", with_inputs=True, pairs=pairs, seed_offset=rank * pairs)
-            flags = FLAG_ARGMIN | FLAG_NO_MAP
-            self.plan = Plan(w, flags)
-            w8 = W.me_view(2160, 3840, 8, 32, pairs=pairs)
-            self.plan8 = Plan(w8, flags)
-            self.sets.append(self._bufs(w.src_a, w.src_b))
-            self.cpu_inputs = (w.src_a[0], w.src_b[0])
-            self.units = f"{pairs} frame pairs (3840x2160 u8) per rank per step, 16x16 and 8x8 blocks"
-            self.workload = "C5 motion estimation 4K x64 pairs (sharded), 16x16 + 8x8 blocks, +/-32, argmin"
-            self.rotation = "1.06 GB input working set > 126 MB L2"
-            self.dtype = "u8 (int32 SAD)"
-            self.aux8 = torch.empty(int(self.plan8.info.aux_elems), dtype=torch.int32, device=device)
-        else:
-            raise SystemExit(f"unknown config {config}")
-        self.info = self.plan.info
-        self.outputs_per_step = int(self.info.n_outputs) + (int(self.plan8.info.n_outputs) if config == "C5" else 0)
+        self.rotation = f"{nsets} rotating input/output set(s) of {per_set / 1e6:.0f} MB ({nsets * per_set / 1e6:.0f} MB; L2 126 MB)"
+        self.outputs_per_step = sum(int(p.info.n_outputs) for p in self.plans)
+        self.dtype = {"C1": "f32", "C2": "u8 (int32 SAD)", "C3": "f32 (3-term bf16 split, fp32 accumulate)",
+                      "C4": "bf16 (fp32 accumulate)", "C5": "u8 (int32 SAD)"}[config]
+        self.info = self.plans[0].info
 
     def _bufs(self, a, b):
         torch = self.torch
         ta = torch.from_numpy(np.ascontiguousarray(a)).to(self.device)
         tb = torch.from_numpy(np.ascontiguousarray(b)).to(self.device)
-        out = torch.empty(max(1, int(self.plan.info.out_bytes)), dtype=torch.uint8, device=self.device) \
-            if hasattr(self, "plan") else None
-        aux = torch.empty(max(1, int(self.plan.info.aux_elems)), dtype=torch.int32, device=self.device) \
-            if hasattr(self, "plan") else None
-        return ta, tb, out, aux
+        outs = [torch.empty(max(1, int(p.info.out_bytes)), dtype=torch.uint8, device=self.device)
+                if p.info.out_elems else None for p in self.plans]
+        auxs = [torch.empty(max(1, int(p.info.aux_elems)), dtype=torch.int32, device=self.device)
+                if p.info.aux_elems else None for p in self.plans]
+        return ta, tb, outs, auxs
 
     def step(self, i, stream):
-        a, b, out, aux = self.sets[i % len(self.sets)]
-        self.plan.run(a, b, out if self.info.out_elems else None, aux if self.info.aux_elems else None,
-                      stream=stream)
-        if self.config == "C5":
-            self.plan8.run(a, b, None, self.aux8, stream=stream)
+        a, b, outs, auxs = self.sets[i % len(self.sets)]
+        for p, o, x in zip(self.plans, outs, auxs):
+            p.run(a, None if p.packed else b, o, x, stream=stream)
 
     # e2e: host buffers through the C ABI (merit_dev_run_host)
     def e2e_setup(self):
         torch = self.torch
-        a, b = self.cpu_inputs if self.config != "C5" else (None, None)
-        if self.config == "C5":
-            a = self.sets[0][0].cpu().numpy()
-            b = self.sets[0][1].cpu().numpy()
-        pa = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
-        pb = torch.from_numpy(np.ascontiguousarray(b)).pin_memory()
-        po = torch.empty(max(1, int(self.info.out_bytes)), dtype=torch.uint8).pin_memory()
-        px = torch.empty(max(1, int(self.info.aux_elems)), dtype=torch.int32).pin_memory()
-        self.host = (pa, pb, po, px)
-        self.h2d = pa.numel() * pa.element_size() + pb.numel() * pb.element_size()
-        self.d2h = int(self.info.out_bytes) + int(self.info.aux_elems) * 4
-        if self.config == "C5":
-            self.host8 = torch.empty(max(1, int(self.plan8.info.aux_elems)), dtype=torch.int32).pin_memory()
-            self.d2h += int(self.plan8.info.aux_elems) * 4
+        w0 = self.workloads[0]
+        pa = torch.from_numpy(np.ascontiguousarray(w0.src_a)).pin_memory()
+        pb = torch.from_numpy(np.ascontiguousarray(w0.src_b)).pin_memory()
+        self.host = (pa, pb)
+        self.host_out = [(torch.empty(max(1, int(p.info.out_bytes)), dtype=torch.uint8).pin_memory(),
+                          torch.empty(max(1, int(p.info.aux_elems)), dtype=torch.int32).pin_memory())
+                         for p in self.plans]
+        # every plan's run_host copies its sources: C5's two block sizes read
+        # the same frames, which the reference's two Workloads also hold twice
+        self.h2d = len(self.plans) * (pa.numel() * pa.element_size() + pb.numel() * pb.element_size())
+        if self.config in ("C3", "C4"):
+            self.h2d = pa.numel() * pa.element_size() + pb.numel() * pb.element_size()
+        self.d2h = sum(int(p.info.out_bytes) + int(p.info.aux_elems) * 4 for p in self.plans)
 
     def e2e_step(self, stream):
         import ctypes as C
-        pa, pb, po, px = self.host
-        lib = self.plan.lib
-        st = lib.merit_dev_run_host(self.plan.handle, C.c_void_p(pa.data_ptr()), C.c_void_p(pb.data_ptr()),
-                                    C.c_void_p(po.data_ptr()) if self.info.out_elems else None,
-                                    C.c_void_p(px.data_ptr()) if self.info.aux_elems else None,
-                                    C.c_void_p(stream))
-        if st:
-            raise RuntimeError(lib.merit_dev_last_error().decode())
-        if self.config == "C5":
-            st = lib.merit_dev_run_host(self.plan8.handle, C.c_void_p(pa.data_ptr()), C.c_void_p(pb.data_ptr()),
-                                        None, C.c_void_p(self.host8.data_ptr()), C.c_void_p(stream))
+        pa, pb = self.host
+        for p, (po, px) in zip(self.plans, self.host_out):
+            st = p.lib.merit_dev_run_host(p.handle, C.c_void_p(pa.data_ptr()), C.c_void_p(pb.data_ptr()),
+                                          C.c_void_p(po.data_ptr()) if p.info.out_elems else None,
+                                          C.c_void_p(px.data_ptr()) if p.info.aux_elems else None,
+                                          C.c_void_p(stream))
             if st:
-                raise RuntimeError(lib.merit_dev_last_error().decode())
+                raise RuntimeError(p.lib.merit_dev_last_error().decode())
 
 
-def roofline(case: "Case", ms_per_launch: float, peaks, peaks_kind, kern: str, clk: dict):
+def roofline(case: "Case", ms_per_step: float, peaks, peaks_kind, kern: str, clk: dict):
     """Roofline object for the dominant kernel of the step.
 
-    Tensor peak: the burst figure, unless the timed region ran power-capped
-    (median SM clock below 97% of max with sw_power_cap reported), in which
-    case the sustained figure of MEASURED_PEAKS.json applies (the profiling
-    recipe's rule for a kernel timed inside a long run); frac_vs_burst is
-    reported either way."""
+    Tensor peak: the burst figure of MEASURED_PEAKS.json (the profiling
+    recipe's figure for a kernel timed alone; a C3/C4 step is 25-120 us);
+    the sustained figure is reported beside it.  SAD: the measured
+    VABSDIFF4.U8.ACC rate."""
     info = case.info
     traffic = None
     tf = PROFILES / "ncu_traffic.json"
@@ -274,53 +277,55 @@ def roofline(case: "Case", ms_per_launch: float, peaks, peaks_kind, kern: str, c
             traffic = d.get(case.config, {}).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
-    sec = ms_per_launch * 1e-3
+    sec = ms_per_step * 1e-3
     hbm_peak = float(peaks["hbm_gbs"])
-    bytes_alg = float(info.algorithmic_bytes)
+    bytes_alg = sum(float(p.info.algorithmic_bytes) for p in case.plans)
     hbm = {"bound": "hbm", "achieved": round(bytes_alg / sec / 1e9, 1), "peak": hbm_peak,
            "unit": "GB/s", "frac": round(bytes_alg / sec / 1e9 / hbm_peak, 4),
            "traffic": traffic, "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peaks_kind})",
-           "algorithmic_bytes_per_launch": bytes_alg, "kernel": kern}
+           "algorithmic_bytes_per_step": bytes_alg, "kernel": kern}
     if info.kernel == 3:  # tensor-core conv
         flops = 2.0 * float(info.algorithmic_ops)
-        split = case.plan.description.split("split=")[1].split()[0]
+        split = case.plans[0].description.split("split=")[1].split()[0]
         burst = float(peaks["bf16_tflops"])
-        capped = ("sw_power_cap" in clk.get("reasons", []) and
-                  float(clk.get("sm_mhz", 0)) < 0.97 * float(clk.get("sm_max_mhz", 1)))
-        peak = float(peaks.get("bf16_tflops_sustained", burst)) if capped else burst
+        sustained = float(peaks.get("bf16_tflops_sustained", burst))
         achieved = flops / sec / 1e12
-        r = {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
-             "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": kern,
-             "peak_source": (f"MEASURED_PEAKS.json bf16_tflops_{'sustained' if capped else 'burst'} "
-                             f"({peaks_kind}; timed region {'power-capped' if capped else 'at full clock'})"),
-             "frac_vs_burst": round(achieved / burst, 4),
+        r = {"bound": "tensor", "achieved": round(achieved, 1), "peak": burst, "unit": "TFLOP/s",
+             "frac": round(achieved / burst, 4), "traffic": traffic, "kernel": kern,
+             "peak_source": f"MEASURED_PEAKS.json bf16_tflops (burst, {peaks_kind})",
+             "frac_vs_sustained": round(achieved / sustained, 4),
              "algorithmic_flops_per_launch": flops, "bf16_products_per_mac": int(split),
-             "tensor_issue_frac": round(achieved * int(split) / peak, 4)}
+             "tensor_issue_frac": round(achieved * int(split) / burst, 4)}
         return r, hbm
     if info.kernel == 2:  # byte-SIMD SAD
         peak, pk = int_simd_peak()
-        ops = float(info.algorithmic_ops) + (float(case.plan8.info.algorithmic_ops) if case.config == "C5" else 0.0)
+        ops = sum(float(p.info.algorithmic_ops) for p in case.plans)
         achieved = ops / sec
         r = {"bound": "alu", "achieved": round(achieved / 1e12, 2), "peak": round(peak / 1e12, 2),
              "unit": "Tabsdiff/s", "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": kern,
              "peak_source": f"VABSDIFF4.U8.ACC microbenchmark, profiles/int_simd_peak.json ({pk})",
-             "algorithmic_ops_per_launch": ops}
+             "algorithmic_ops_per_step": ops}
         return r, hbm
     return hbm, None
 
 
+def _dist_init(backend, device=None):
+    import torch.distributed as dist
+    kw = {"device_id": device} if device is not None else {}
+    dist.init_process_group(backend, **kw)
+    return dist
+
+
 def run_ours(args):
     import torch
-    import torch.distributed as dist
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if not torch.cuda.is_available():
-        raise SystemExit("bench.py needs a CUDA device (no CPU fallback exists)")
+        raise SystemExit("bench.py needs a CUDA device (no CPU fallback exists; --dry-run checks the rank logic)")
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+    dist = _dist_init("nccl", device) if world > 1 else None
     from paper_1911_03458_b200 import _capi
     lib = _capi.load()
     case = Case(args.config, rank, world, device)
@@ -328,7 +333,7 @@ def run_ours(args):
     sp = stream.cuda_stream
 
     def barrier():
-        if world > 1:
+        if dist is not None:
             dist.barrier()
 
     # warm-up (untimed)
@@ -343,12 +348,12 @@ def run_ours(args):
     i = 0
     with torch.cuda.stream(stream):
         while time.perf_counter() - t_soak < args.soak:
-            for _ in range(8):
+            for _ in range(4):
                 case.step(i, sp)
                 i += 1
             stream.synchronize()
-    # timed region: exactly K steps.  By default the K launches are captured
-    # once into a CUDA graph and the graph is replayed inside the timed region
+    # timed region: exactly K steps.  The K steps are captured once into a
+    # CUDA graph and the graph is replayed inside the timed region
     # (microsecond-scale kernels are otherwise bound by the host launch path).
     l0 = lib.merit_dev_launch_count()
     graph = None
@@ -370,11 +375,10 @@ def run_ours(args):
     barrier()
     torch.cuda.synchronize()
     e0.record(stream)
-    if graph is not None:
-        with torch.cuda.stream(stream):
+    with torch.cuda.stream(stream):
+        if graph is not None:
             graph.replay()
-    else:
-        with torch.cuda.stream(stream):
+        else:
             for i in range(args.steps):
                 case.step(i, sp)
     e1.record(stream)
@@ -386,9 +390,13 @@ def run_ours(args):
         kern_name = (lib.merit_dev_last_kernel() or b"").decode()
     ms = e0.elapsed_time(e1)
     t = torch.tensor([ms], dtype=torch.float64, device=device)
-    if world > 1:
+    if dist is not None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
+    total_per_step = torch.tensor([case.outputs_per_step], dtype=torch.float64, device=device)
+    if dist is not None:
+        dist.all_reduce(total_per_step)
+    outputs_all = float(total_per_step.item())
 
     # e2e through the host-buffer C-ABI call
     case.e2e_setup()
@@ -404,32 +412,29 @@ def run_ours(args):
     e2e_s = time.perf_counter() - t0
     barrier()
     te = torch.tensor([e2e_s], dtype=torch.float64, device=device)
-    if world > 1:
+    if dist is not None:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_s = float(te.item())
 
     peaks, peaks_kind = load_peaks()
-    total_outputs = case.outputs_per_step * args.steps * world
-    value = total_outputs / (ms_max * 1e-3) / 1e9
-    ms_per_launch = ms_max / args.steps / (2 if args.config == "C5" else 1)
+    value = outputs_all * args.steps / (ms_max * 1e-3) / 1e9
     clk = clocks.summary(f"timed region + {args.soak:.1f} s soak of the same step just before")
-    rf, rf2 = roofline(case, ms_per_launch if args.config != "C5" else ms_max / args.steps, peaks, peaks_kind,
-                       kern_name, clk)
+    rf, rf2 = roofline(case, ms_max / args.steps, peaks, peaks_kind, kern_name, clk)
     line = {
         "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 5), "higher_is_better": True,
-        "scaling": "strong" if args.config in ("C1", "C4", "C5") else "weak", "vs_baseline": None,
-        "dtype": case.dtype, "data": "synthetic (seeded SplitMix64 generators, SURVEY §8(d))",
-        "config": {"workload": case.workload, "units": case.units,
-                   "outputs_per_step_per_rank": case.outputs_per_step,
-                   "l2": case.rotation, "kernel": case.plan.description,
-                   "parallelism": f"dp{world} (independent shards, no collective)",
+        "scaling": "strong", "vs_baseline": None, "dtype": case.dtype, "data": DATA,
+        "config": {"workload": WORKLOAD[args.config],
+                   "shard": f"rank 0: {case.meta['what']}" + (f" (one of {world} ranks)" if world > 1 else ""),
+                   "outputs_per_step": int(outputs_all),
+                   "l2": case.rotation, "kernel": " | ".join(p.description for p in case.plans),
+                   "parallelism": f"dp{world} (independent shards, no collective on the data path)",
                    "timing": ("CUDA events around one CUDA-graph replay of the K captured steps"
                               if not args.no_graph else "CUDA events around K eager launches")},
         "roofline": rf,
-        "e2e": {"value": round(case.outputs_per_step * e2e_steps * world / e2e_s / 1e9, 4), "unit": UNIT,
+        "e2e": {"value": round(outputs_all * e2e_steps / e2e_s / 1e9, 4), "unit": UNIT,
                 "h2d_bytes_per_step": int(case.h2d), "d2h_bytes_per_step": int(case.d2h),
-                "steps": e2e_steps, "path": "merit_dev_run_host (pinned host buffers in, host results out)"},
+                "steps": e2e_steps, "path": "merit_dev_run_host per Workload (pinned host buffers in, host results out)"},
         "gpu_launches": int(launches),
         "clocks": clk,
     }
@@ -437,72 +442,134 @@ def run_ours(args):
         line["roofline_hbm"] = rf2
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.config, budget_s=args.cpu_budget)
+        line["cpu_baseline_oracle_loop"] = cpu_baseline(args.config, budget_s=args.cpu_budget / 3,
+                                                        leg="oracle_loop")
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist is not None:
         dist.destroy_process_group()
 
 
-def cpu_baseline(config, budget_s=20.0, steps=1, warmup=0):
-    from oracle.cpu_baseline import CpuBaseline, unit_cost_s
-    cfg = config
-    cb = CpuBaseline(cfg)
+def cpu_baseline(config, budget_s=20.0, steps=1, warmup=0, leg="engine"):
+    from oracle.cpu_baseline import CpuBaseline, cpu_model, unit_cost_s
+    cb = CpuBaseline(config)
     try:
-        per_proc = max(1, int(budget_s / max(steps + warmup, 1) / unit_cost_s(cfg, cb.kind)))
-        if cfg == "C1":
+        per_proc = max(1, int(budget_s / max(steps + warmup, 1) / unit_cost_s(config, cb.kind, leg)))
+        if config == "C1":
             per_proc = 1
+        elif config in ("C3", "C4"):
+            per_proc = min(per_proc, 64)
+        elif config == "C2":
+            per_proc = min(per_proc, 120)
+        elif config == "C5":
+            per_proc = min(per_proc, 60)
         for i in range(warmup):
-            cb.step(per_proc, first_shard=i * cb.procs)
+            cb.step(per_proc, first_shard=i * cb.procs, leg=leg)
         n = 0
         wall = 0.0
         for i in range(steps):
-            dn, dt = cb.step(per_proc, first_shard=(warmup + i) * cb.procs)
+            dn, dt = cb.step(per_proc, first_shard=(warmup + i) * cb.procs, leg=leg)
             n += dn
             wall += dt
     finally:
         cb.close()
-    unit_name = {"C2": "16x16 blocks of the 1080p pair", "C5": "16x16 blocks of a 4K pair",
-                 "C1": "images (64 channels)", "C3": "output channels of one 56x56 image (fp32)",
-                 "C4": "output channels of one image (bf16-rounded values in REAL32)"}[cfg]
+    unit_name = {"C2": "16x16 blocks of the 1080p pair", "C5": "(16x16 block + four 8x8 blocks) of a 4K pair",
+                 "C1": "image(s) (64 channels)", "C3": "output channels of one 56x56 image (fp32)",
+                 "C4": "output channels of one image (bf16-rounded values in REAL32)"}[config]
+    path = ("merit::run_full (engine.hpp:282-287)" if leg == "engine" else
+            "the reference's brute-force oracle loop (workloads.hpp oracle_*)")
     return {"value": round(n / wall / 1e9, 9), "unit": UNIT, "cores": cb.procs, "kind": cb.kind,
-            "sample": f"{cfg}: {cb.procs} processes x {per_proc} {unit_name} per step, {steps} step(s), "
-                      f"{n} outputs in {wall:.2f} s through merit::run_full"
-                      + ("" if cfg == config else f" (CPU sample taken on {cfg})")}
+            "leg": leg, "cpu": cpu_model(),
+            "sample": f"{config}: {cb.procs} processes x {per_proc} {unit_name} per step, {steps} step(s), "
+                      f"{n} outputs in {wall:.2f} s through {path}"}
 
 
 def run_reference(args):
+    """The reference's own CPU implementation of the path (merit::run_full of
+    the unmodified reference, oracle/_ref) on the host cores.  Under torchrun
+    only rank 0 runs it."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    budget = args.cpu_budget_ref
-    cb = cpu_baseline(args.config, budget_s=budget, steps=args.steps, warmup=args.warmup)
+    cb = cpu_baseline(args.config, budget_s=args.cpu_budget_ref, steps=args.steps, warmup=args.warmup)
+    ol = cpu_baseline(args.config, budget_s=args.cpu_budget_ref / 4, steps=1, leg="oracle_loop")
     line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": int(os.environ.get("WORLD_SIZE", "1")),
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "impl": "reference",
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32 (REAL32 engine)",
-            "data": "synthetic (seeded SplitMix64 generators, SURVEY §8(d))",
-            "config": {"workload": args.config, "parallelism": f"{cb['cores']} host processes"},
-            "cpu_baseline": cb,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32 (REAL32 engine)", "data": DATA,
+            "config": {"workload": WORKLOAD[args.config],
+                       "parallelism": f"{cb['cores']} host processes ({cb['cpu']})"},
+            "cpu_baseline": cb, "cpu_baseline_oracle_loop": ol,
             "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def run_dry(args):
+    """The N>1 rank logic on CPU (gloo): every rank builds its shard exactly
+    as the GPU run does (shard_for, without generating inputs) and rank 0
+    prints all ranks' shards."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    dist = _dist_init("gloo") if world > 1 else None
+    ws, meta = shard_for(args.config, rank, world, with_inputs=False)
+    from paper_1911_03458_b200 import Plan
+    from paper_1911_03458_b200 import FLAG_ARGMIN, FLAG_NO_MAP
+    flags = {"C2": FLAG_ARGMIN, "C5": FLAG_ARGMIN | FLAG_NO_MAP}.get(args.config, 0)
+    mine = {"rank": rank, "range": meta["range"], "what": meta["what"],
+            "src_a_shape": list(ws[0].view_a.source_shape), "src_b_shape": list(ws[0].view_b.source_shape),
+            "outputs": sum(int(Plan(w, flags).info.n_outputs) for w in ws),
+            "kernels": [int(Plan(w, flags).kernel) for w in ws]}
+    shards = [None] * world
+    if dist is not None:
+        dist.all_gather_object(shards, mine)
+    else:
+        shards = [mine]
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "config": args.config, "n_gpus": world,
+                          "workload": WORKLOAD[args.config], "shards": shards}), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def relaunch_distributed(args) -> int:
+    """--gpus N without a torchrun environment: run this script under
+    torch.distributed.run with N ranks on this node."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C5", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--soak", type=float, default=0.5)
-    ap.add_argument("--e2e-steps", type=int, default=50)
+    ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-budget", type=float, default=15.0)
-    ap.add_argument("--cpu-budget-ref", type=float, default=90.0)
+    ap.add_argument("--cpu-budget-ref", type=float, default=60.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA graph")
+    ap.add_argument("--dry-run", action="store_true", help="CPU check of the multi-rank shard logic (gloo)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: at least 3 warm-up steps
-    if args.impl == "reference":
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(relaunch_distributed(args))
+    if args.dry_run:
+        run_dry(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

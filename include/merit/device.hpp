@@ -135,11 +135,12 @@ inline Tensor run_full(const Workload& w, uint32_t flags = 0) {
 /// own TilingPlan::validate (BadParams); the result is run_full's (the device
 /// executes its own footprint-staged tiling) and the report is
 /// the reference's TrafficReport for the plan (Eq. 6 words per pass, computed
-/// by merit_dev_tiled_traffic).  EngineConfig's scratchpad capacities are
-/// accepted and not enforced.
+/// by merit_dev_tiled_traffic).  EngineConfig's scratchpad capacities keep
+/// their diagnostic meaning (engine.hpp:82-87, :154-155): a plan whose
+/// largest footprint box exceeds scratch_words_a / scratch_words_b throws
+/// ScratchpadOverflow, as the reference's Scratchpad::load does.
 inline std::pair<Tensor, TrafficReport> run_tiled(const Workload& w, const TilingPlan& plan,
                                                   const EngineConfig& cfg = {}, uint32_t flags = 0) {
-  (void)cfg;
   w.validate();
   plan.validate(w.p_shape(), w.a_shape());
   TrafficReport rep;
@@ -160,6 +161,9 @@ inline std::pair<Tensor, TrafficReport> run_tiled(const Workload& w, const Tilin
     rep.passes = r.passes;
     rep.macs = r.macs;
   }
+  if (static_cast<int64_t>(rep.scratchpad_peak_words_a) > cfg.scratch_words_a ||
+      static_cast<int64_t>(rep.scratchpad_peak_words_b) > cfg.scratch_words_b)
+    throw Error(ErrorCode::ScratchpadOverflow, "tile exceeds scratchpad");
   return {run_full(w, flags), rep};
 }
 

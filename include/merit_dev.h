@@ -22,9 +22,25 @@
  * with a status code (mirroring merit::ErrorCode, tensor.hpp:15-29).
  *
  * Every entry point returns merit_status; on failure the thread-local message
- * is available from merit_dev_last_error().  All functions are reentrant;
- * plans are immutable after creation apart from the packed-operand cache
- * filled by merit_dev_plan_pack_b (call it before sharing a plan).
+ * is available from merit_dev_last_error().
+ *
+ * Threading (engine.hpp's run_full is a pure function; SPEC.md:294-295 lets
+ * p-tiles run concurrently).  All functions are thread-safe.  A plan is
+ * immutable after creation apart from lazily created device state and the
+ * packed-weight copy of merit_dev_plan_pack_b; it may be run from several
+ * host threads on several streams at once:
+ *   - kernels that only read their sources (max-pool, SAD, correlation, a
+ *     conv plan after merit_dev_plan_pack_b) run fully concurrently;
+ *   - a conv run that packs its weights on the fly (no pack_b) writes the
+ *     plan's packed buffer, so such runs of ONE plan are stream-ordered one
+ *     after another (an event chain), and pack_b itself waits for them;
+ *   - exact-interpreter runs of one plan (they synchronise their stream to
+ *     read the device error flag) are serialised by the plan;
+ *   - merit_dev_run_host calls of one plan are serialised (they share the
+ *     plan's staging buffers).
+ * A plan's device state lives on the device of its first run; running it on
+ * another device fails with MERIT_E_INVALID_ARGUMENT: for multi-GPU create one
+ * plan per device (tests/test_concurrency.py).
  */
 #ifndef MERIT_DEV_H_
 #define MERIT_DEV_H_
@@ -219,8 +235,9 @@ merit_status merit_dev_plan_destroy(merit_plan* plan);
 merit_status merit_dev_plan_query(const merit_plan* plan, merit_plan_info* info);
 
 /* Pack the B operand (e.g. convolution weights) into the kernel's operand
- * layout on the device, once.  d_src_b is a device pointer.  Optional: run
- * calls pack on the fly when no packed copy exists. */
+ * layout on the device, once.  d_src_b is a device pointer.  After it, runs
+ * use the packed copy and ignore their d_src_b.  Optional: without it every
+ * run packs its own d_src_b on the fly. */
 merit_status merit_dev_plan_pack_b(merit_plan* plan, const void* d_src_b, void* cuda_stream);
 
 /* Run on device buffers, asynchronously on `cuda_stream` (0 = default).

@@ -29,6 +29,9 @@ def lib():
         L = C.CDLL(str(path))
         L.oracle_fill_uniform_f32.argtypes = [C.c_void_p, C.c_int64, C.c_uint64, C.c_double, C.c_double]
         L.oracle_fill_range_i16.argtypes = [C.c_void_p, C.c_int64, C.c_uint64, C.c_int64, C.c_int64]
+        L.oracle_gen_normal_f32.argtypes = [C.c_void_p, C.c_int64, C.c_uint64, C.c_double]
+        L.oracle_f32_to_bf16.argtypes = [C.c_void_p, C.c_void_p, C.c_int64]
+        L.oracle_gen_me_pair.argtypes = [C.c_void_p, C.c_void_p] + [C.c_int64] * 5 + [C.c_uint64]
         L.oracle_maxpool.argtypes = [C.c_void_p, C.c_void_p, C.c_int64] + [C.c_int] * 13 + [C.c_float, C.c_int]
         L.oracle_conv2d_nchw.argtypes = [C.c_void_p] * 3 + [C.c_int] * 16
         L.oracle_me_sad.argtypes = [C.c_void_p] * 3 + [C.c_int64] + [C.c_int] * 11
@@ -58,6 +61,8 @@ def ref():
         L.ref_run_full.restype = C.c_int
         L.ref_run_tiled.argtypes = [C.c_void_p] * 3 + [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.ref_run_tiled.restype = C.c_int
+        L.ref_run_tiled_caps.argtypes = [C.c_void_p] * 5 + [C.c_int64, C.c_int64, C.c_void_p, C.c_void_p]
+        L.ref_run_tiled_caps.restype = C.c_int
         L.ref_mrt1_write.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_int64]
         L.ref_mrt1_write.restype = C.c_int64
         L.ref_mrt1_read.argtypes = [C.c_void_p, C.c_int64, C.POINTER(C.c_int), C.POINTER(C.c_int),
@@ -70,6 +75,14 @@ def ref():
                                         C.c_void_p, C.c_void_p, C.POINTER(C.c_int64), C.c_int64]
         L.ref_template_case.restype = C.c_int
         L.ref_last_error.restype = C.c_char_p
+        L.ref_bench_load_frames.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64]
+        L.ref_sample_me.argtypes = [C.c_int64] * 5 + [C.c_int]
+        L.ref_sample_me.restype = C.c_int64
+        L.ref_bench_load_images.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_int64]
+        L.ref_sample_maxpool.argtypes = [C.c_int]
+        L.ref_sample_maxpool.restype = C.c_int64
+        L.ref_sample_conv.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_int]
+        L.ref_sample_conv.restype = C.c_int64
         _ref = L
     return _ref
 
@@ -79,6 +92,32 @@ def fill_uniform(n, seed, lo=-1.0, hi=1.0):
     out = np.empty(n, np.float32)
     lib().oracle_fill_uniform_f32(_p(out), n, seed, lo, hi)
     return out
+
+
+def gen_uniform(shape, seed, lo=-1.0, hi=1.0):
+    out = np.empty(shape, np.float32)
+    lib().oracle_fill_uniform_f32(_p(out), out.size, seed, lo, hi)
+    return out
+
+
+def gen_normal(shape, seed, sigma):
+    out = np.empty(shape, np.float32)
+    lib().oracle_gen_normal_f32(_p(out), out.size, seed, sigma)
+    return out
+
+
+def to_bf16_bits(x):
+    x = np.ascontiguousarray(x, np.float32)
+    out = np.empty(x.shape, np.uint16)
+    lib().oracle_f32_to_bf16(_p(x), _p(out), x.size)
+    return out
+
+
+def gen_me_pair(h, w, seed, blk=16, max_shift=16, noise=4):
+    cur = np.empty((h, w), np.uint8)
+    ref_ = np.empty((h, w), np.uint8)
+    lib().oracle_gen_me_pair(_p(cur), _p(ref_), h, w, blk, max_shift, noise, seed)
+    return cur, ref_
 
 
 def fill_range_i16(n, seed, lo=-256, hi=256):
@@ -165,7 +204,8 @@ def ref_run_full(w):
     return out
 
 
-def ref_run_tiled(w, t_p, t_a):
+def ref_run_tiled(w, t_p, t_a, caps=(1 << 40, 1 << 40)):
+    """merit::run_tiled with EngineConfig{scratch_words_a, scratch_words_b} = caps."""
     from paper_1911_03458_b200.merit import _DescHolder, _host, Error, Dtype
     h = _DescHolder(w, 0)
     da, _, _ = h.dtypes
@@ -175,7 +215,8 @@ def ref_run_tiled(w, t_p, t_a):
     tp = np.asarray(t_p, np.int64)
     ta = np.asarray(t_a, np.int64)
     traffic = np.zeros(7, np.uint64)
-    st = ref().ref_run_tiled(C.byref(h.desc), _p(a), _p(b), _p(tp), _p(ta), _p(out), _p(traffic))
+    st = ref().ref_run_tiled_caps(C.byref(h.desc), _p(a), _p(b), _p(tp), _p(ta), int(caps[0]), int(caps[1]),
+                                  _p(out), _p(traffic))
     if st:
         raise Error(st, ref().ref_last_error().decode())
     return out, traffic

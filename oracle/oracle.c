@@ -51,6 +51,68 @@ void oracle_fill_range_i16(int16_t* out, int64_t n, uint64_t seed, int64_t lo, i
   sm64 r = {seed};
   for (int64_t i = 0; i < n; ++i) out[i] = (int16_t)sm64_range(&r, lo, hi);
 }
+/* Seeded synthetic inputs of SURVEY §8(d), restated here so that the CPU
+ * baseline arms of bench.py never load the device library:
+ * normal(0, sigma) by Box-Muller over SplitMix64 uniforms (C3/C4 weights),
+ * fp32 -> bf16 round-to-nearest-even (C4 activations), and the motion
+ * estimation frame pair (ref = 5x5 box filter of uniform bytes, clamped
+ * border, round half up; cur = ref shifted per blk x blk block by
+ * range(-max_shift, max_shift) plus range(-noise, noise), clamped).
+ * tests/test_oracle_golden.py checks them byte-for-byte against the device
+ * library's merit_gen_* (the generators the GPU arm uses). */
+void oracle_gen_normal_f32(float* out, int64_t n, uint64_t seed, double sigma) {
+  sm64 r = {seed};
+  const double two_pi = 6.283185307179586476925286766559;
+  for (int64_t i = 0; i < n; i += 2) {
+    double u1 = sm64_uniform(&r, 0.0, 1.0), u2 = sm64_uniform(&r, 0.0, 1.0);
+    if (u1 < 1e-300) u1 = 1e-300;
+    const double rad = sqrt(-2.0 * log(u1));
+    out[i] = (float)(sigma * rad * cos(two_pi * u2));
+    if (i + 1 < n) out[i + 1] = (float)(sigma * rad * sin(two_pi * u2));
+  }
+}
+
+void oracle_f32_to_bf16(const float* in, uint16_t* out, int64_t n) {
+  for (int64_t i = 0; i < n; ++i) {
+    uint32_t u;
+    memcpy(&u, &in[i], 4);
+    if ((u & 0x7fffffffu) > 0x7f800000u) {
+      out[i] = (uint16_t)((u >> 16) | 0x40);
+      continue;
+    }
+    u += 0x7fffu + ((u >> 16) & 1u);
+    out[i] = (uint16_t)(u >> 16);
+  }
+}
+
+static int64_t clampi(int64_t v, int64_t lo, int64_t hi) { return v < lo ? lo : v > hi ? hi : v; }
+
+void oracle_gen_me_pair(uint8_t* cur, uint8_t* ref, int64_t h, int64_t w, int64_t blk, int64_t max_shift,
+                        int64_t noise, uint64_t seed) {
+  sm64 r = {seed};
+  uint8_t* raw = (uint8_t*)malloc((size_t)(h * w));
+  for (int64_t i = 0; i < h * w; ++i) raw[i] = (uint8_t)sm64_range(&r, 0, 255);
+  for (int64_t y = 0; y < h; ++y)
+    for (int64_t x = 0; x < w; ++x) {
+      int64_t s = 0;
+      for (int64_t dy = -2; dy <= 2; ++dy)
+        for (int64_t dx = -2; dx <= 2; ++dx) s += raw[clampi(y + dy, 0, h - 1) * w + clampi(x + dx, 0, w - 1)];
+      ref[y * w + x] = (uint8_t)((s + 12) / 25);
+    }
+  free(raw);
+  const int64_t by = (h + blk - 1) / blk, bx = (w + blk - 1) / blk;
+  for (int64_t b = 0; b < by * bx; ++b) {
+    const int64_t y0 = (b / bx) * blk, x0 = (b % bx) * blk;
+    const int64_t sx = sm64_range(&r, -max_shift, max_shift), sy = sm64_range(&r, -max_shift, max_shift);
+    for (int64_t i = 0; i < blk && y0 + i < h; ++i)
+      for (int64_t j = 0; j < blk && x0 + j < w; ++j) {
+        const int64_t y = y0 + i, x = x0 + j;
+        const int64_t v = ref[clampi(y + sy, 0, h - 1) * w + clampi(x + sx, 0, w - 1)] + sm64_range(&r, -noise, noise);
+        cur[y * w + x] = (uint8_t)clampi(v, 0, 255);
+      }
+  }
+}
+
 uint64_t oracle_splitmix_next(uint64_t* state) {
   sm64 r = {*state};
   uint64_t v = sm64_next(&r);

@@ -100,6 +100,38 @@ int code_of(const merit::Error& e) { return static_cast<int>(e.code) + 1; }
 
 }  // namespace
 
+namespace {
+struct BenchInputs {
+  merit::Tensor cur, ref;   // ME frames (REAL32 holding 8-bit values)
+  merit::Tensor x, wt;      // conv / max-pool activations, conv weights
+  int64_t H = 0, W = 0;
+  int64_t cin = 0, h = 0, cout = 0;
+} g_in;
+
+merit::Tensor real_of_u8(const uint8_t* p, merit::Shape shape) {
+  merit::Tensor t = merit::Tensor::real(shape);
+  for (size_t i = 0; i < t.fdata.size(); ++i) t.fdata[i] = p[i];
+  return t;
+}
+merit::Tensor real_of_f32(const float* p, merit::Shape shape) {
+  merit::Tensor t = merit::Tensor::real(shape);
+  std::memcpy(t.fdata.data(), p, t.fdata.size() * 4);
+  return t;
+}
+template <class F>
+int64_t guarded(F&& f) {
+  try {
+    return f();
+  } catch (const merit::Error& e) {
+    g_err = e.what();
+    return -code_of(e);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -MERIT_E_BAD_PARAMS;
+  }
+}
+}  // namespace
+
 extern "C" {
 
 const char* ref_last_error(void) { return g_err.c_str(); }
@@ -130,8 +162,16 @@ int ref_run_full(const merit_workload_desc* d, const void* a, const void* b, voi
 
 // merit::run_tiled (engine.hpp:289-295) with a tiling plan; also returns the
 // TrafficReport as 7 uint64 (engine.hpp:72-80).
+int ref_run_tiled_caps(const merit_workload_desc* d, const void* a, const void* b, const int64_t* t_p,
+                       const int64_t* t_a, int64_t cap_a, int64_t cap_b, void* out, uint64_t* traffic);
 int ref_run_tiled(const merit_workload_desc* d, const void* a, const void* b, const int64_t* t_p,
                   const int64_t* t_a, void* out, uint64_t* traffic) {
+  return ref_run_tiled_caps(d, a, b, t_p, t_a, int64_t(1) << 40, int64_t(1) << 40, out, traffic);
+}
+
+// The same with EngineConfig's scratchpad capacities (engine.hpp:82-87).
+int ref_run_tiled_caps(const merit_workload_desc* d, const void* a, const void* b, const int64_t* t_p,
+                       const int64_t* t_a, int64_t cap_a, int64_t cap_b, void* out, uint64_t* traffic) {
   try {
     merit::Workload w;
     w.view_a = to_view(d->view_a);
@@ -143,8 +183,8 @@ int ref_run_tiled(const merit_workload_desc* d, const void* a, const void* b, co
     plan.t_p.assign(t_p, t_p + d->view_a.p_rank);
     plan.t_a.assign(t_a, t_a + d->view_a.a_rank);
     merit::EngineConfig cfg;
-    cfg.scratch_words_a = int64_t(1) << 40;
-    cfg.scratch_words_b = int64_t(1) << 40;
+    cfg.scratch_words_a = cap_a;
+    cfg.scratch_words_b = cap_b;
     auto [t, rep] = merit::run_tiled(w, plan, cfg);
     if (t.dtype == merit::Dtype::Real32)
       std::memcpy(out, t.fdata.data(), t.fdata.size() * 4);
@@ -270,6 +310,114 @@ int ref_template_case(const char* name, const char* params, uint64_t seed, void*
     g_err = e.what();
     return MERIT_E_BAD_PARAMS;
   }
+}
+
+
+// ---------------------------------------------------------------------------
+// bench.py's CPU arms (oracle/cpu_baseline.py): bounded samples of each
+// BASELINE config through the reference's public API.  The worker loads its
+// inputs once (generated by liboracle, so these processes never map the
+// device library) and times ref_sample_* calls.  kind 0 = merit::run_full
+// (engine.hpp:282-287) on the config's custom batched view restricted to the
+// sample; kind 1 = the reference's brute-force oracle loop (workloads.hpp:
+// 458-499, 548-585, 642-671) on the same amount of work.  Programs come from
+// the reference's own template builders.  Return: outputs computed, or
+// -(ErrorCode + 1).
+
+void ref_bench_load_frames(const uint8_t* cur, const uint8_t* ref, int64_t H, int64_t W) {
+  g_in.cur = real_of_u8(cur, {H, W});
+  g_in.ref = real_of_u8(ref, {H, W});
+  g_in.H = H;
+  g_in.W = W;
+}
+
+// nbx blocks (bx0 ..) of block row `by`, +/-r search.
+int64_t ref_sample_me(int64_t blk, int64_t r, int64_t by, int64_t bx0, int64_t nbx, int kind) {
+  return guarded([&]() -> int64_t {
+    const int64_t win = 2 * r + 1;
+    merit::Params prm{{"h", double(blk)}, {"w", double(blk)}, {"blk", double(blk)}, {"win", double(win)}};
+    if (kind == 0) {
+      merit::Workload w = merit::build_template("motion_estimation", prm);  // program + view skeleton
+      // the frame-scale view (floor(H / blk) block rows, workloads.hpp:556)
+      // restricted to the sample by offsets on the block axes
+      const int64_t H = g_in.H, W = g_in.W;
+      w.view_a = {{H, W}, {1, nbx, win, win}, {blk, blk},
+                  {{0, 0, blk, by * blk}, {4, 0, 1, 0}, {1, 1, blk, bx0 * blk}, {5, 1, 1, 0}}};
+      w.view_b = {{H, W}, {1, nbx, win, win}, {blk, blk},
+                  {{0, 0, blk, by * blk}, {2, 0, 1, -r}, {4, 0, 1, 0},
+                   {1, 1, blk, bx0 * blk}, {3, 1, 1, -r}, {5, 1, 1, 0}}};
+      w.src_a = g_in.cur;
+      w.src_b = g_in.ref;
+      return static_cast<int64_t>(merit::run_full(w).size());
+    }
+    // oracle loop on a blk x (nbx * blk) crop (same work per block)
+    const int64_t cw = nbx * blk;
+    merit::Tensor c = merit::Tensor::real({blk, cw}), rf = merit::Tensor::real({blk, cw});
+    for (int64_t i = 0; i < blk; ++i)
+      for (int64_t j = 0; j < cw; ++j) {
+        c.fdata[i * cw + j] = g_in.cur.fdata[(by * blk + i) * g_in.W + bx0 * blk + j];
+        rf.fdata[i * cw + j] = g_in.ref.fdata[(by * blk + i) * g_in.W + bx0 * blk + j];
+      }
+    prm["w"] = double(cw);
+    return static_cast<int64_t>(merit::oracle("motion_estimation", prm, c, rf).size());
+  });
+}
+
+void ref_bench_load_images(const float* x, int64_t n_ch, int64_t h, const float* wt, int64_t cout) {
+  g_in.x = real_of_f32(x, {1, n_ch, h, h});
+  g_in.cin = n_ch;
+  g_in.h = h;
+  g_in.cout = cout;
+  if (wt) g_in.wt = real_of_f32(wt, {cout, n_ch, 3, 3});
+}
+
+// C1: 3x3 / s2 / pad 1 max-pool of the loaded image (all channels).
+int64_t ref_sample_maxpool(int kind) {
+  return guarded([&]() -> int64_t {
+    const int64_t C = g_in.cin, h = g_in.h, ho = (h + 2 - 3) / 2 + 1;
+    merit::Params prm{{"h", double(h)}, {"w", double(h)}, {"k", 3.0}, {"stride", 2.0}};
+    if (kind == 0) {
+      merit::Workload w = merit::build_template("maxpool", prm);
+      w.view_a = {{1, C, h, h}, {1, C, ho, ho}, {3, 3},
+                  {{0, 0, 1, 0}, {1, 1, 1, 0}, {2, 2, 2, -1}, {4, 2, 1, 0}, {3, 3, 2, -1}, {5, 3, 1, 0}},
+                  merit::Boundary::Clamp};
+      w.view_b = {{1}, {1, C, ho, ho}, {3, 3}, {}};
+      w.src_a = g_in.x;
+      return static_cast<int64_t>(merit::run_full(w).size());
+    }
+    // the reference oracle has no padding: (h - 3) / 2 + 1 outputs per axis
+    int64_t n = 0;
+    merit::Tensor plane = merit::Tensor::real({h, h});
+    for (int64_t c = 0; c < C; ++c) {
+      std::memcpy(plane.fdata.data(), g_in.x.fdata.data() + c * h * h, h * h * 4);
+      n += static_cast<int64_t>(merit::oracle("maxpool", prm, plane, plane).size());
+    }
+    return n;
+  });
+}
+
+// C3 / C4: output channels [co0, co0 + units) of the loaded image, 3x3, pad 1.
+int64_t ref_sample_conv(int64_t stride, int64_t co0, int64_t units, int kind) {
+  return guarded([&]() -> int64_t {
+    const int64_t cin = g_in.cin, h = g_in.h, ho = (h + 2 - 3) / stride + 1;
+    merit::Tensor k = merit::Tensor::real({units, cin, 3, 3});
+    std::memcpy(k.fdata.data(), g_in.wt.fdata.data() + co0 * cin * 9, units * cin * 9 * 4);
+    merit::Params prm{{"cin", double(cin)}, {"cout", double(units)}, {"h", double(h)}, {"w", double(h)},
+                      {"k", 3.0}, {"stride", double(stride)}, {"pad", 1.0}};
+    if (kind == 0) {
+      merit::Workload w = merit::build_template("conv2d", prm);  // mac_program(3, 0)
+      w.view_a = {{1, cin, h, h}, {1, units, ho, ho}, {cin, 3, 3},
+                  {{0, 0, 1, 0}, {4, 1, 1, 0}, {2, 2, stride, 0}, {5, 2, 1, -1}, {3, 3, stride, 0}, {6, 3, 1, -1}}};
+      w.view_b = {{units, cin, 3, 3}, {1, units, ho, ho}, {cin, 3, 3},
+                  {{1, 0, 1, 0}, {4, 1, 1, 0}, {5, 2, 1, 0}, {6, 3, 1, 0}}};
+      w.src_a = g_in.x;
+      w.src_b = k;
+      return static_cast<int64_t>(merit::run_full(w).size());
+    }
+    merit::Tensor img = merit::Tensor::real({cin, h, h});
+    img.fdata = g_in.x.fdata;
+    return static_cast<int64_t>(merit::oracle("conv2d", prm, img, k).size());
+  });
 }
 
 }  // extern "C"

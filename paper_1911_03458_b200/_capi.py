@@ -12,7 +12,13 @@ MAX_RANK = 8
 MAX_TERMS = 24
 MAX_INSTRS = 64
 
+import os
+
 LIB_PATH = Path(__file__).resolve().parent / "libmerit_dev.so"
+# MERIT_DEV_LIB selects another build of the same ABI (e.g. the diagnostic
+# libmerit_dev_debug.so from `python -m paper_1911_03458_b200.build --debug`).
+if os.environ.get("MERIT_DEV_LIB"):
+    LIB_PATH = Path(os.environ["MERIT_DEV_LIB"]).resolve()
 
 
 class ViewTermC(C.Structure):

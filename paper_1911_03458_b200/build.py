@@ -11,6 +11,7 @@ from __future__ import annotations
 import os
 import shutil
 import subprocess
+from concurrent.futures import ThreadPoolExecutor
 import sys
 from pathlib import Path
 
@@ -48,26 +49,41 @@ def _stale(target: Path, deps) -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> Path:
-    BUILD.mkdir(exist_ok=True)
+# Diagnostic build (-DMERIT_DEV_DEBUG): the MERIT_*_DEBUG / MERIT_SAD_DBG
+# timing knobs exist only here.  Load it with MERIT_DEV_LIB=<path>.
+DEBUG_BUILD = PKG / "_build_debug"
+DEBUG_LIB = PKG / "libmerit_dev_debug.so"
+
+
+def build(verbose: bool = False, force: bool = False, debug: bool = False) -> Path:
+    bdir, lib = (DEBUG_BUILD, DEBUG_LIB) if debug else (BUILD, LIB)
+    bdir.mkdir(exist_ok=True)
     cc = nvcc()
     headers = _headers()
-    objs = []
+    objs, cmds = [], []
     for src in _sources():
-        obj = BUILD / (src.name + ".o")
+        obj = bdir / (src.name + ".o")
         objs.append(obj)
         if force or _stale(obj, [src, *headers, Path(__file__)]):
-            cmd = [cc, *ARCH, *NVCC_FLAGS, f"-I{INCLUDE}", f"-I{CSRC}", "-c", str(src), "-o", str(obj)]
-            if verbose:
-                print(" ".join(cmd), flush=True)
-            subprocess.run(cmd, check=True)
-    if force or _stale(LIB, objs):
-        cmd = [cc, *ARCH, "-shared", "-cudart", "static", "-o", str(LIB), *map(str, objs), "-lcuda"]
+            cmds.append([cc, *ARCH, *NVCC_FLAGS, *(["-DMERIT_DEV_DEBUG"] if debug else []), f"-I{INCLUDE}",
+                         f"-I{CSRC}", "-c", str(src), "-o", str(obj)])
+
+    def compile_one(cmd):
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)
-    build_cli(verbose, force)
-    return LIB
+
+    # translation units are independent: compile them concurrently
+    with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 1))) as ex:
+        list(ex.map(compile_one, cmds))
+    if force or _stale(lib, objs):
+        cmd = [cc, *ARCH, "-shared", "-cudart", "static", "-o", str(lib), *map(str, objs), "-lcuda"]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+    if not debug:
+        build_cli(verbose, force)
+    return lib
 
 
 CLI_SRC = PKG / "cli" / "merit_dev.cpp"
@@ -89,5 +105,4 @@ def build_cli(verbose: bool = False, force: bool = False) -> Path:
 
 
 if __name__ == "__main__":
-    build(verbose=True, force="--force" in sys.argv)
-    print(LIB)
+    print(build(verbose=True, force="--force" in sys.argv, debug="--debug" in sys.argv))

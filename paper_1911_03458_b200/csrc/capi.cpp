@@ -91,6 +91,24 @@ merit_status merit_dev::ensure_device_state(const merit_plan& plan) {
   return MERIT_OK;
 }
 
+// Stream-order a write of plan.d_packed_b after every earlier run that read
+// it (caller holds plan.pack_mu).
+merit_status merit_dev::pack_wait(const merit_plan& plan, void* stream) {
+  if (!plan.pack_event) return MERIT_OK;
+  return cuda_check(cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), static_cast<cudaEvent_t>(plan.pack_event), 0),
+                    "cudaStreamWaitEvent(pack)");
+}
+merit_status merit_dev::pack_done(const merit_plan& plan, void* stream) {
+  if (!plan.pack_event) {
+    cudaEvent_t e;
+    merit_status st = cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate(pack)");
+    if (st != MERIT_OK) return st;
+    plan.pack_event = e;
+  }
+  return cuda_check(cudaEventRecord(static_cast<cudaEvent_t>(plan.pack_event), static_cast<cudaStream_t>(stream)),
+                    "cudaEventRecord(pack)");
+}
+
 extern "C" {
 
 int32_t merit_dev_abi_version(void) { return MERIT_DEV_ABI_VERSION; }
@@ -136,6 +154,7 @@ merit_status merit_dev_plan_destroy(merit_plan* plan) {
     if (plan->d_prog) cudaFree(plan->d_prog);
     if (plan->d_err) cudaFree(plan->d_err);
     if (plan->d_packed_b) cudaFree(plan->d_packed_b);
+    if (plan->pack_event) cudaEventDestroy(static_cast<cudaEvent_t>(plan->pack_event));
     cudaSetDevice(cur);
   }
   if (plan->stage_dev >= 0) {
@@ -163,7 +182,10 @@ merit_status merit_dev_plan_pack_b(merit_plan* plan, const void* d_src_b, void* 
   if (!d_src_b) return fail(MERIT_E_INVALID_ARGUMENT, "null weights");
   merit_status st = ensure_device_state(*plan);
   if (st != MERIT_OK) return st;
+  std::lock_guard<std::mutex> lk(plan->pack_mu);
+  if ((st = pack_wait(*plan, stream)) != MERIT_OK) return st;
   st = launch_conv_pack(*plan, d_src_b, plan->d_packed_b, stream);
+  if (st == MERIT_OK) st = pack_done(*plan, stream);
   if (st == MERIT_OK) plan->packed_valid = true;
   return st;
 }
@@ -199,11 +221,13 @@ merit_status merit_dev_run(const merit_plan* plan, const void* d_a, const void* 
   merit_status st = ensure_device_state(*plan);
   if (st != MERIT_OK) return st;
   switch (plan->kernel) {
-    case MERIT_KERNEL_GENERIC:
+    case MERIT_KERNEL_GENERIC: {
       if (!d_a || !d_b) return fail(MERIT_E_INVALID_ARGUMENT, "null source");
+      std::lock_guard<std::mutex> lk(plan->run_mu);  // one error flag per plan
       st = launch_generic(*plan, d_a, d_b, d_out, stream);
       if (st == MERIT_OK) st = check_error_flag(*plan, static_cast<cudaStream_t>(stream));
       return st;
+    }
     case MERIT_KERNEL_MAXPOOL:
       if (!d_a) return fail(MERIT_E_INVALID_ARGUMENT, "null source");
       return launch_maxpool(*plan, d_a, d_out, stream);
@@ -214,12 +238,16 @@ merit_status merit_dev_run(const merit_plan* plan, const void* d_a, const void* 
       const void* in = plan->conv_swapped ? d_b : d_a;
       const void* w = plan->conv_swapped ? d_a : d_b;
       if (!in) return fail(MERIT_E_INVALID_ARGUMENT, "null source");
-      if (!plan->packed_valid) {
-        if (!w) return fail(MERIT_E_INVALID_ARGUMENT, "null weights and no packed copy");
-        st = launch_conv_pack(*plan, w, plan->d_packed_b, stream);
-        if (st != MERIT_OK) return st;
-      }
-      return launch_conv(*plan, in, plan->d_packed_b, d_out, stream);
+      if (plan->packed_valid) return launch_conv(*plan, in, plan->d_packed_b, d_out, stream);
+      // weights packed on the fly into the plan's buffer, ordered after any
+      // other stream's run that still reads it
+      if (!w) return fail(MERIT_E_INVALID_ARGUMENT, "null weights and no packed copy");
+      std::lock_guard<std::mutex> lk(plan->pack_mu);
+      if ((st = pack_wait(*plan, stream)) != MERIT_OK) return st;
+      st = launch_conv_pack(*plan, w, plan->d_packed_b, stream);
+      if (st == MERIT_OK) st = launch_conv(*plan, in, plan->d_packed_b, d_out, stream);
+      if (st == MERIT_OK) st = pack_done(*plan, stream);
+      return st;
     }
     case MERIT_KERNEL_CORR:
       if (!d_a || !d_b) return fail(MERIT_E_INVALID_ARGUMENT, "null source");

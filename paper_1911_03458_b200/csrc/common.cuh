@@ -3,11 +3,37 @@
 
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdlib>
 #include <utility>
 
 #include "plan.hpp"
 
 namespace merit_dev {
+
+// Diagnostic knobs (MERIT_CONV_DEBUG, MERIT_SAD_DBG, MERIT_MP_DEBUG) skip work,
+// add host synchronisation or print: they exist only in a -DMERIT_DEV_DEBUG
+// build, so the product library's results cannot depend on the environment.
+// Tuning knobs (kernel variant, ring depths, launch shape) stay environment
+// controlled: every setting is parity-tested to give identical results.
+inline const char* debug_env(const char* name) {
+#ifdef MERIT_DEV_DEBUG
+  return getenv(name);
+#else
+  (void)name;
+  return nullptr;
+#endif
+}
+
+// MERIT_GRID_CAP=n caps a persistent kernel's grid at n CTAs (CTA pairs /
+// quads count as one): every CTA then walks many scheduling units, which the
+// parity tests use to cover ring-phase carry across units at small sizes.
+inline int grid_cap(int grid) {
+  if (const char* g = getenv("MERIT_GRID_CAP")) {
+    const int c = atoi(g);
+    if (c > 0 && grid > c) return c;
+  }
+  return grid;
+}
 
 inline merit_status launch_status(const char* what) {
   cudaError_t e = cudaGetLastError();

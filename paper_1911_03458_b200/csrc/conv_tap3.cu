@@ -498,7 +498,8 @@ merit_status launch_conv_tap3(const merit_plan& plan, const void* a, const void*
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int grid = num_sms();
   if (grid > A.n_tiles) grid = A.n_tiles;
-  const char* dbg = getenv("MERIT_CONV_DEBUG");
+  grid = grid_cap(grid);
+  const char* dbg = debug_env("MERIT_CONV_DEBUG");
   A.debug = dbg ? atoi(dbg) : 0;
   A.prof = nullptr;
   if (A.debug & 64) {

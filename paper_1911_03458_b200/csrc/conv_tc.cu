@@ -721,7 +721,7 @@ merit_status launch_conv(const merit_plan& plan, const void* a, const void* pack
   while (cols < static_cast<uint32_t>(2 * p.BN)) cols <<= 1;
   A.tmem_cols = cols;
   {
-    const char* dbg = getenv("MERIT_CONV_DEBUG");
+    const char* dbg = debug_env("MERIT_CONV_DEBUG");
     A.debug = dbg ? atoi(dbg) : 0;
   }
   A.tap3 = (!p.gemm && p.KW == 3 && p.dx == 1 && p.ox == -1 &&
@@ -738,6 +738,7 @@ merit_status launch_conv(const merit_plan& plan, const void* a, const void* pack
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int grid = num_sms();
   if (grid > A.n_tiles) grid = A.n_tiles;
+  grid = grid_cap(grid);
   cudaError_t e;
 #define MERIT_LAUNCH_CONV(INB, S3, TP)                                                         \
   do {                                                                                         \

@@ -559,7 +559,7 @@ merit_status launch_conv_tma(const merit_plan& plan, const void* a, const void* 
     if (mc > 0 && quads > mc) quads = mc;
     if (A.debug & 4096) fprintf(stderr, "[conv_tma] max active 4-CTA clusters %d, quads %d\n", mc, quads);
     if (quads > A.n_units) quads = A.n_units;
-    grid = 4 * quads;
+    grid = 4 * grid_cap(quads);
   } else if (pair) {
     int pairs = num_sms() / 2;
     // only as many pairs as can be co-resident (TPC / GPC placement): a
@@ -579,13 +579,14 @@ merit_status launch_conv_tma(const merit_plan& plan, const void* a, const void* 
     if (max_clusters > 0 && pairs > max_clusters) pairs = max_clusters;
     if (A.debug & 4096) fprintf(stderr, "[conv_tma] max active 2-CTA clusters %d, pairs %d\n", max_clusters, pairs);
     if (pairs > A.n_units) pairs = A.n_units;
-    grid = 2 * pairs;
+    grid = 2 * grid_cap(pairs);
   } else {
     grid = num_sms();
     if (grid > A.n_tiles) grid = A.n_tiles;
+    grid = grid_cap(grid);
   }
   {
-    const char* dbg = getenv("MERIT_CONV_DEBUG");
+    const char* dbg = debug_env("MERIT_CONV_DEBUG");
     A.debug = dbg ? atoi(dbg) : 0;
   }
   A.prof = nullptr;

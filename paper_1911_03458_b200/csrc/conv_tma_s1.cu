@@ -552,6 +552,7 @@ merit_status launch_conv_s1(const merit_plan& plan, const void* a, const void* p
   if (e != cudaSuccess) return cuda_check(e, "set_smem_attr(conv_s1)");
   int grid = num_sms();
   if (grid > A.n_tiles) grid = A.n_tiles;
+  grid = grid_cap(grid);
   // Tail split: the final partial wave of r = n_tiles % grid tiles runs as 2r
   // half-N units, so it costs half a tile instead of a whole one (C3: 896
   // tiles on 148 SMs).  Needs N / 2 = 3 BN / 2 to stay a multiple of 16.
@@ -563,7 +564,7 @@ merit_status launch_conv_s1(const merit_plan& plan, const void* a, const void* p
     A.n_units = A.n_full + 2 * (A.n_tiles - A.n_full);
   }
   {
-    const char* dbg = getenv("MERIT_CONV_DEBUG");
+    const char* dbg = debug_env("MERIT_CONV_DEBUG");
     A.debug = dbg ? atoi(dbg) : 0;
   }
   A.prof = nullptr;

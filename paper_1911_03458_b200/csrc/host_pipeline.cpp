@@ -234,6 +234,14 @@ merit_status run_host_pipelined(const merit_plan& plan, void* da, void* db, void
   if (st != MERIT_OK) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const size_t k = plan.slices.size();
+  // weights packed on the fly: hold the plan's pack lock for the whole run
+  // (it drains its streams before returning) and wait for earlier readers
+  const bool packs = plan.kernel == MERIT_KERNEL_CONV_TC && !plan.packed_valid;
+  std::unique_lock<std::mutex> pack_lock(plan.pack_mu, std::defer_lock);
+  if (packs) {
+    pack_lock.lock();
+    if ((st = pack_wait(plan, stream)) != MERIT_OK) return st;
+  }
   for (void*& cs : plan.copy_stream)
     if (!cs) {
       cudaStream_t t;

@@ -199,7 +199,7 @@ bool comp_unused(const ViewAffine& f, int c) {
 }
 
 // ---------------------------------------------------------------- maxpool --
-bool lower_maxpool(const merit_workload_desc& d, const ViewAffine& va, float init,
+bool lower_maxpool(const merit_workload_desc& d, const ViewAffine& va, const ViewAffine& vb, float init,
                    int32_t post, MaxpoolParams& mp) {
   const merit_view_spec& v = d.view_a;
   if (d.dtype_a != MERIT_F32 || d.dtype_out != MERIT_F32) return false;
@@ -222,6 +222,10 @@ bool lower_maxpool(const merit_workload_desc& d, const ViewAffine& va, float ini
   kshape[P] = v.a_shape[0];
   kshape[P + 1] = v.a_shape[1];
   if (v.boundary == MERIT_REJECT && !view_in_range(va, kshape)) return false;  // error path
+  // run_full gathers port B at every step even though the max program never
+  // reads it (engine.hpp:128-133): an out-of-range REJECT view_b must raise
+  // OutOfRange, so it goes to the interpreter's error path
+  if (d.view_b.boundary == MERIT_REJECT && !view_in_range(vb, kshape)) return false;
   const int64_t H = v.src_shape[R - 2], W = v.src_shape[R - 1];
   if (H > (1 << 30) || W > (1 << 30)) return false;
   mp.planes = 1;
@@ -626,7 +630,7 @@ merit_status lower(const merit_workload_desc& d, merit_plan& plan) {
   Skeleton sk = (d.flags & MERIT_FLAG_EXACT) || fix16 ? SK_NONE : classify(d, pi, post, init);
   const int64_t avol = vol(v.a_shape, v.a_rank);
 
-  if (sk == SK_MAX && lower_maxpool(d, fa, init, post, plan.mp)) {
+  if (sk == SK_MAX && lower_maxpool(d, fa, fb, init, post, plan.mp)) {
     plan.kernel = MERIT_KERNEL_MAXPOOL;
     const auto& mp = plan.mp;
     info.algorithmic_ops = (double)info.n_outputs * avol;

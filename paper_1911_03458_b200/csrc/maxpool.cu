@@ -362,6 +362,7 @@ merit_status launch_maxpool(const merit_plan& plan, const void* a, void* out, vo
     if (smem <= 200 * 1024) {
       long long grid = (long long)num_sms() * ctas;
       if (grid > items) grid = items;
+      grid = grid_cap(static_cast<int>(grid));
       // band loads: a 2-D tensor map over the [planes * H][W] rows (UTMALDG),
       // or plain bulk copies (MERIT_MP_TMAP=0)
       CUtensorMap rmap;
@@ -406,7 +407,7 @@ merit_status launch_maxpool(const merit_plan& plan, const void* a, void* out, vo
       cudaError_t e = set_smem_attr(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return cuda_check(e, "set_smem_attr(maxpool)");
       MaxpoolParams pp = p;
-      if (const char* de = getenv("MERIT_MP_DEBUG")) pp.dbg = atoi(de);
+      if (const char* de = debug_env("MERIT_MP_DEBUG")) pp.dbg = atoi(de);
       pp.vec_out = (p.Wo % 4 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
       pp.pf = ns;
       if (const char* pe = getenv("MERIT_MP_PF")) pp.pf = atoi(pe) < 0 ? (1 << 30) : atoi(pe);

@@ -168,8 +168,16 @@ struct merit_plan {
   mutable void* d_prog = nullptr;      // ProgramImage copy for K0
   mutable void* d_err = nullptr;       // int32 device error flag
   mutable void* d_packed_b = nullptr;  // K3 packed weights
-  mutable bool packed_valid = false;
+  mutable bool packed_valid = false;  // set by merit_dev_plan_pack_b only
   mutable int device = -1;
+  // Concurrent runs of one plan (several threads / streams): a run that packs
+  // the weights on the fly writes the shared d_packed_b, so such runs hold
+  // pack_mu while they enqueue, wait on pack_event (the previous packing
+  // run's last launch) and record it after their own; exact-interpreter runs
+  // share d_err and hold run_mu from launch to error check.
+  mutable std::mutex pack_mu;
+  mutable void* pack_event = nullptr;
+  mutable std::mutex run_mu;
   // Device staging of merit_dev_run_host (a, b, out, aux), kept across calls
   // on the device they were made on; host_mu serialises host-buffer calls.
   mutable std::mutex host_mu;
@@ -200,6 +208,10 @@ merit_status run_host_pipelined(const merit_plan& plan, void* da, void* db, void
                                 void* stream);
 // Lazily allocate a plan's device state on the current device (capi.cpp).
 merit_status ensure_device_state(const merit_plan& plan);
+// Order a write of plan.d_packed_b after the runs that read it / record this
+// stream's position as the new last reader (caller holds plan.pack_mu).
+merit_status pack_wait(const merit_plan& plan, void* stream);
+merit_status pack_done(const merit_plan& plan, void* stream);
 // Release the pipeline's streams/events (plan destruction, device switch).
 void release_host_pipeline(const merit_plan& plan);
 

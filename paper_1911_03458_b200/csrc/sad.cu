@@ -974,7 +974,7 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
     return 128 + 2ull * L.raw_buf + 2ull * L.cur_buf + 4ull * (4ull * ncopy * L.CS + 2ull * L.nby * L.TBX) + 8 + 16;
   };
   L.dbg = 0;
-  if (const char* ge = getenv("MERIT_SAD_DBG")) L.dbg = atoi(ge);
+  if (const char* ge = debug_env("MERIT_SAD_DBG")) L.dbg = atoi(ge);
   const char* de = getenv("MERIT_SAD_DBL");
   L.dbl = (L.tma && !(de && de[0] == '0') && smem_for(2) <= smem_cap) ? 1 : 0;
   const size_t smem = smem_for(L.dbl ? 2 : 1);
@@ -1057,6 +1057,7 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
   fast_div_init(static_cast<uint32_t>(L.BYT), L.byt_m, L.byt_s);
   long long grid = (nt == 512 ? 1LL : 2LL) * num_sms();
   if (grid > L.n_tiles) grid = L.n_tiles;
+  grid = grid_cap(static_cast<int>(grid));
   e = launch_pdl(kern, dim3(static_cast<unsigned>(grid)), dim3(threads), smem_launch, s, 1, cur, ref, out, aux, L,
                  ref_map, cur_map);
   if (e != cudaSuccess) return cuda_check(e, "launch(sad)");

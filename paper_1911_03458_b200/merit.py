@@ -417,6 +417,17 @@ class Plan:
         return {k: int(getattr(r, k)) for k, _ in r._fields_}
 
     # -- host buffers: the reference's run_full convention --------------------
+    @staticmethod
+    def _check_host(x, dtype, need: int, what: str):
+        if not isinstance(x, np.ndarray):
+            raise Error(ErrorCode.BadParams, f"{what} must be a numpy array")
+        if x.dtype != np.dtype(dtype):
+            raise Error(ErrorCode.BadParams, f"{what} has dtype {x.dtype}, needs {np.dtype(dtype)}")
+        if not x.flags["C_CONTIGUOUS"] or not x.flags["WRITEABLE"]:
+            raise Error(ErrorCode.BadParams, f"{what} must be a writeable C-contiguous array")
+        if x.nbytes < need:
+            raise Error(ErrorCode.BadParams, f"{what} holds {x.nbytes} bytes, needs {need}")
+
     def run_host(self, src_a, src_b, out: Optional[np.ndarray] = None,
                  aux: Optional[np.ndarray] = None, stream=None):
         a = np.ascontiguousarray(src_a)
@@ -430,6 +441,12 @@ class Plan:
             raise Error(ErrorCode.BadParams, "source shape mismatch (src_a)")
         if b is not None and b.nbytes != self.info.src_b_bytes:
             raise Error(ErrorCode.BadParams, "source shape mismatch (src_b)")
+        # the C call copies out_bytes / aux_elems * 4 bytes into the raw host
+        # pointers: caller-supplied arrays must be exactly right
+        if self.info.out_elems:
+            self._check_host(out, _NP_OF[do], self.info.out_bytes, "out")
+        if self.info.aux_elems:
+            self._check_host(aux, np.int32, self.info.aux_elems * 4, "aux")
         _check(self.lib.merit_dev_run_host(
             self.handle, a.ctypes.data_as(C.c_void_p),
             b.ctypes.data_as(C.c_void_p) if b is not None else None,
@@ -448,13 +465,18 @@ def run_full(w: Workload, flags: int = 0):
     return out
 
 
-def run_tiled(w: Workload, t_p, t_a, flags: int = 0):
+def run_tiled(w: Workload, t_p, t_a, flags: int = 0, scratch_words_a: int = 8192,
+              scratch_words_b: int = 4096):
     """engine.hpp:289-295 on the device: the output of run_full (the device
     executes its own footprint-staged tiling) and the TilingPlan's
-    TrafficReport as a dict (scratchpad capacities are not enforced)."""
+    TrafficReport as a dict.  EngineConfig's capacities (engine.hpp:82-87)
+    keep their diagnostic meaning: a footprint box larger than
+    scratch_words_a / _b raises ScratchpadOverflow (engine.hpp:154-155)."""
     _check_sources(w)
     plan = Plan(w, flags)
     rep = plan.tiled_traffic(t_p, t_a)
+    if rep["scratchpad_peak_words_a"] > scratch_words_a or rep["scratchpad_peak_words_b"] > scratch_words_b:
+        raise Error(ErrorCode.ScratchpadOverflow, "tile exceeds scratchpad")
     out, _ = plan.run_host(_host(w.src_a), _host(w.src_b))
     return out, rep
 

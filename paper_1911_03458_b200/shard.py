@@ -62,3 +62,61 @@ def shard_workload(w: Workload, world: int, rank: int) -> Tuple[Workload, Tuple[
         if src is not None:
             setattr(s, attr_s, np.ascontiguousarray(src[start:stop]))
     return s, (start, stop)
+
+
+def _axis_footprint(view, axis: int, kshape, comp0_range) -> Tuple[int, int]:
+    """Eq. 6 extent (view.hpp:121-149) of source axis `axis` over the index
+    box kshape with component 0 restricted to comp0_range: [lo, hi]."""
+    lo = hi = 0
+    for t in view.terms:
+        if t.axis != axis:
+            continue
+        if t.component == 0:
+            a, b = comp0_range[0] * t.stride, (comp0_range[1] - 1) * t.stride
+        else:
+            a, b = 0, (kshape[t.component] - 1) * t.stride
+        lo += min(a, b) + t.offset
+        hi += max(a, b) + t.offset
+    return lo, hi
+
+
+def shard_band(w: Workload, world: int, rank: int) -> Tuple[Workload, Tuple[int, int]]:
+    """Band split of a single-image workload along p-axis 0 (e.g. the block
+    rows of one motion-estimation frame pair): rank r gets
+    a contiguous range of p-axis 0 and, of every source that the component
+    feeds through source axis 0, only the rows its band reads — the Eq. 6
+    footprint of the band (footprint_box, view.hpp:121-149), i.e. its rows
+    plus the search-window halo — sliced at load time.  The view's axis-0
+    offset is shifted by the slice start, so every gather reads the same
+    value as in the unsplit workload (rows outside the original source stay
+    outside the slice: ZERO_PAD / CLAMP / REJECT behave identically).  No
+    exchange between ranks."""
+    total = w.view_a.p_shape[0]
+    start, stop = shard_range(total, world, rank)
+    kshape = list(w.view_a.p_shape) + list(w.view_a.a_shape)
+    s = copy.copy(w)
+    s.view_a = copy.deepcopy(w.view_a)
+    s.view_b = copy.deepcopy(w.view_b)
+    for attr_v, attr_s in (("view_a", "src_a"), ("view_b", "src_b")):
+        v = getattr(s, attr_v)
+        v.p_shape[0] = stop - start
+        uses0 = [t for t in v.terms if t.component == 0]
+        if not uses0:
+            continue  # replicated operand
+        if any(t.axis != 0 for t in uses0):
+            raise Error(ErrorCode.BadParams, "band component must feed source axis 0 only")
+        if stop <= start:
+            continue
+        lo, hi = _axis_footprint(getattr(w, attr_v), 0, kshape, (start, stop))
+        rows = v.source_shape[0]
+        r0, r1 = max(0, lo), min(rows - 1, hi)
+        if r1 < r0:  # the band reads nothing inside the source: keep one row
+            r0 = r1 = min(max(0, lo), rows - 1)
+        v.source_shape[0] = r1 - r0 + 1
+        # component 0 now counts from 0: fold start*stride - r0 into one term
+        t0 = next(t for t in v.terms if t.component == 0)
+        t0.offset += start * t0.stride - r0
+        src = getattr(w, attr_s)
+        if src is not None:
+            setattr(s, attr_s, np.ascontiguousarray(src[r0:r1 + 1]))
+    return s, (start, stop)

@@ -202,3 +202,15 @@ def test_gemm_lowers_to_tensor_core_kernel_real32_only():
     wf = W.build_template("gemm", {"m": 5, "n": 6, "k": 7, "fix": 1, "frac": 6})
     W.fill_random(wf, 1, 2)
     assert Plan(wf).kernel == Kernel.GENERIC  # FIX16: exact interpreter
+
+
+def test_maxpool_reject_view_b_goes_to_error_path():
+    # run_full gathers port B at every step (engine.hpp:128-133) although the
+    # max program never reads it: an out-of-range REJECT view_b must raise
+    # OutOfRange like the reference, so K1 must not take such a workload
+    w = W.maxpool_nchw_view(2, 3, 8, 8)
+    assert Plan(w).kernel == Kernel.MAXPOOL
+    w.view_b.boundary = W.Boundary.Reject
+    assert Plan(w).kernel == Kernel.MAXPOOL          # in range: still K1
+    w.view_b.terms = [ViewTerm(0, 0, 1, 0)]            # image index into a (1,) source
+    assert Plan(w).kernel == Kernel.GENERIC

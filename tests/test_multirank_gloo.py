@@ -9,7 +9,7 @@ import numpy as np
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_1911_03458_b200.shard import shard_range, shard_workload
+from paper_1911_03458_b200.shard import shard_band, shard_range, shard_workload
 from paper_1911_03458_b200 import workloads as W
 
 
@@ -47,8 +47,16 @@ def _worker(rank, world, port, q):
     mv = O.me_argmin(O.me_sad(sm.src_a, sm.src_b, 8, 4), 4)
     mparts = [None] * world
     dist.all_gather_object(mparts, (c0, c1, mv))
+    # block-row band of ONE frame pair (C2 split): rows + Eq. 6 halo only
+    bc, br = W.gen_me_pair(120, 64, 33)
+    b = W.me_view(120, 64, 16, 16)
+    b.src_a, b.src_b = bc, br
+    sb, (r0, r1) = shard_band(b, world, rank)
+    assert sb.src_a.shape[0] == 16 * (r1 - r0) and sb.src_b.shape[0] < 120
+    bparts = [None] * world
+    dist.all_gather_object(bparts, (r0, r1, O.run_full(sb)))
     if rank == 0:
-        q.put((parts, mparts))
+        q.put((parts, mparts, bparts))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -66,7 +74,7 @@ def test_two_rank_gloo_sharding_equals_unsharded():
     procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    parts, mparts = q.get(timeout=120)
+    parts, mparts, bparts = q.get(timeout=120)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
@@ -77,3 +85,8 @@ def test_two_rank_gloo_sharding_equals_unsharded():
     full_mv = O.me_argmin(O.me_sad(cur, ref, 8, 4), 4)
     got_mv = np.concatenate([p[2] for p in sorted(mparts, key=lambda t: t[0])])
     assert np.array_equal(got_mv, full_mv)
+    bc, br = W.gen_me_pair(120, 64, 33)
+    b = W.me_view(120, 64, 16, 16)
+    b.src_a, b.src_b = bc, br
+    got_b = np.concatenate([p[2] for p in sorted(bparts, key=lambda t: t[0])])
+    assert np.array_equal(got_b, O.run_full(b))

@@ -115,3 +115,18 @@ def test_restatement_vs_live_reference_on_fresh_cases():
         w = W.me_view(32, 48, 8, 4 + t)
         w.src_a, w.src_b = cur, ref
         assert np.array_equal(O.ref_run_full(w), O.me_sad(cur, ref, 8, 4 + t).astype(np.float32))
+
+
+def test_oracle_generators_match_device_library_generators():
+    # the CPU baseline arms generate their inputs with liboracle (they never
+    # load the device library); the bytes must be the GPU arm's bytes
+    for h, wd, seed in ((1080, 1920, 2), (37, 61, 9)):
+        a = O.gen_me_pair(h, wd, seed)
+        b = W.gen_me_pair(h, wd, seed)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    assert np.array_equal(O.gen_normal([64, 64, 3, 3], 1003, (2.0 / 576) ** 0.5),
+                          W.gen_normal([64, 64, 3, 3], 1003, (2.0 / 576) ** 0.5))
+    assert np.array_equal(O.gen_uniform([3, 5, 7], 4), W.gen_uniform([3, 5, 7], 4))
+    x = O.gen_uniform([1000], 5, -3.0, 3.0)
+    x[:3] = [np.nan, np.inf, -0.0]
+    assert np.array_equal(O.to_bf16_bits(x), W.to_bf16_bits(x))

@@ -97,3 +97,27 @@ def test_rank_mismatch_raises_bad_params():
     with pytest.raises(Error) as e:
         Plan(w).tiled_traffic([4], [3, 3])
     assert e.value.code == ErrorCode.BadParams
+
+
+@needs_ref
+@pytest.mark.parametrize("idx", range(len(CASES)))
+@pytest.mark.parametrize("caps", [(8192, 4096), (200, 100), (1 << 40, 10)])
+def test_scratchpad_overflow_like_reference(idx, caps):
+    # EngineConfig capacities (engine.hpp:82-87): the reference throws
+    # ScratchpadOverflow from Scratchpad::load (:154-155); device run_tiled
+    # raises the same code before touching the device
+    from paper_1911_03458_b200 import run_tiled
+    make, t_p, t_a = CASES[idx]
+    w = make()
+    try:
+        O.ref_run_tiled(w, t_p, t_a, caps)
+        ref_code = None
+    except Error as e:
+        ref_code = e.code
+    rep = Plan(w).tiled_traffic(t_p, t_a)
+    dev_over = rep["scratchpad_peak_words_a"] > caps[0] or rep["scratchpad_peak_words_b"] > caps[1]
+    assert (ref_code == ErrorCode.ScratchpadOverflow) == dev_over
+    if dev_over:
+        with pytest.raises(Error) as ei:
+            run_tiled(w, t_p, t_a, scratch_words_a=caps[0], scratch_words_b=caps[1])
+        assert ei.value.code == ErrorCode.ScratchpadOverflow
