@@ -198,7 +198,8 @@ typedef enum merit_kernel_kind {
   MERIT_KERNEL_MAXPOOL = 1,
   MERIT_KERNEL_SAD = 2,
   MERIT_KERNEL_CONV_TC = 3,
-  MERIT_KERNEL_CORR = 4
+  MERIT_KERNEL_CORR = 4,
+  MERIT_KERNEL_MULTI = 5   /* multi-workload plan run member by member */
 } merit_kernel_kind;
 
 /* What a plan needs and produces. */
@@ -212,8 +213,12 @@ typedef struct merit_plan_info {
   int64_t src_a_bytes;
   int64_t src_b_bytes;
   int64_t n_outputs;       /* ranged inner products computed = prod(p_shape) */
-  double algorithmic_ops;  /* MACs / abs-diffs / compares per run */
+  double algorithmic_ops;  /* MACs / abs-diffs / compares per run, counted as
+                              the reference's run_full executes them */
   double algorithmic_bytes;/* compulsory HBM bytes per run */
+  double executed_ops;     /* the ops the device executes per run: equal to
+                              algorithmic_ops unless a fused multi-workload
+                              plan shares work between members */
   int32_t launches_per_run;/* kernel launches issued by merit_dev_run */
   int32_t _pad;
   char description[256];
@@ -240,6 +245,29 @@ merit_status merit_dev_plan_query(const merit_plan* plan, merit_plan_info* info)
  * run packs its own d_src_b on the fly. */
 merit_status merit_dev_plan_pack_b(merit_plan* plan, const void* d_src_b, void* cuda_stream);
 
+/* Several workloads over the SAME two source tensors as one plan: what a
+ * caller of the reference does with one run_full per workload
+ * (engine.hpp:282-287), e.g. the 16x16 and 8x8 block searches of C5.
+ * Every member is validated and lowered like merit_dev_plan_create; all
+ * members must have the same source shapes and dtypes (BAD_PARAMS
+ * otherwise).  merit_dev_run / _run_host take the shared sources once and
+ * write the members' outputs back to back in member order: d_out holds
+ * every member's output, d_aux every member's argmin records (offsets from
+ * merit_dev_plan_member).  Members that the device can compute in one pass
+ * are fused into one launch:
+ *   L1 block matching with BxB and 2Bx2B blocks (B = 8) over the same frames,
+ *   window (+/-32) and boundary, argmin without SAD maps: one byte-SIMD pass
+ *   computes the BxB SADs and sums 2 x 2 of them into the 2Bx2B SAD at every
+ *   displacement (exact integers, results identical to separate runs).
+ * Otherwise the members run one after another on the stream
+ * (info.kernel = MERIT_KERNEL_MULTI).  Host-only, like plan creation. */
+merit_status merit_dev_plan_create_multi(const merit_workload_desc* descs, int32_t n, merit_plan** out_plan);
+/* Member i of a multi-workload plan (or member 0 = the plan itself for a
+ * single-workload plan): its own plan info and the byte / int32-element
+ * offsets of its output and argmin records in the plan's d_out / d_aux. */
+merit_status merit_dev_plan_member(const merit_plan* plan, int32_t i, merit_plan_info* info,
+                                   int64_t* out_offset_bytes, int64_t* aux_offset_elems);
+
 /* Run on device buffers, asynchronously on `cuda_stream` (0 = default).
  * d_out receives Workload::output_shape() elements of dtype_out (may be null
  * with MERIT_FLAG_NO_MAP); d_aux receives the argmin records (may be null
@@ -263,6 +291,7 @@ typedef struct merit_host_slice {
   int64_t a_need, b_need;
   int64_t out_lo, out_hi;
   int64_t aux_lo, aux_hi;
+  int64_t aux2_lo, aux2_hi;  /* a second aux range (fused multi-workload plans) */
 } merit_host_slice;
 merit_status merit_dev_plan_slices(const merit_plan* plan, merit_host_slice* slices, int64_t cap,
                                    int64_t* n_slices);

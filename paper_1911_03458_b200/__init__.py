@@ -6,11 +6,11 @@ reference's operator API (``merit.py``) plus the workload templates and the
 BASELINE configurations (``workloads.py``).
 """
 from .merit import (AluInstr, Boundary, Dst, Dtype, Error, ErrorCode, Kernel, LookupTable, Op,
-                    Operand, Plan, StrategyProgram, ViewSpec, ViewTerm, Workload, run_full,
-                    run_full_argmin, run_tiled, FLAG_ARGMIN, FLAG_EXACT, FLAG_FAST_BF16, FLAG_NO_MAP)
+                    Operand, Plan, PlanGroup, StrategyProgram, ViewSpec, ViewTerm, Workload, run_full,
+                    run_full_argmin, run_full_many, run_tiled, FLAG_ARGMIN, FLAG_EXACT, FLAG_FAST_BF16, FLAG_NO_MAP)
 from . import workloads
 
 __all__ = ["AluInstr", "Boundary", "Dst", "Dtype", "Error", "ErrorCode", "Kernel", "LookupTable",
-           "Op", "Operand", "Plan", "StrategyProgram", "ViewSpec", "ViewTerm", "Workload",
-           "run_full", "run_full_argmin", "run_tiled", "workloads", "FLAG_ARGMIN", "FLAG_EXACT",
+           "Op", "Operand", "Plan", "PlanGroup", "StrategyProgram", "ViewSpec", "ViewTerm", "Workload",
+           "run_full", "run_full_argmin", "run_full_many", "run_tiled", "workloads", "FLAG_ARGMIN", "FLAG_EXACT",
            "FLAG_FAST_BF16", "FLAG_NO_MAP"]

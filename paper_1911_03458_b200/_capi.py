@@ -64,6 +64,7 @@ class PlanInfoC(C.Structure):
                 ("out_bytes", C.c_int64), ("aux_elems", C.c_int64), ("src_a_bytes", C.c_int64),
                 ("src_b_bytes", C.c_int64), ("n_outputs", C.c_int64),
                 ("algorithmic_ops", C.c_double), ("algorithmic_bytes", C.c_double),
+                ("executed_ops", C.c_double),
                 ("launches_per_run", C.c_int32), ("_pad", C.c_int32),
                 ("description", C.c_char * 256)]
 
@@ -76,7 +77,7 @@ class TrafficReportC(C.Structure):  # merit_traffic_report (engine.hpp:72-80)
 
 class HostSliceC(C.Structure):  # merit_host_slice (pipelined merit_dev_run_host)
     _fields_ = [("a_need", C.c_int64), ("b_need", C.c_int64), ("out_lo", C.c_int64), ("out_hi", C.c_int64),
-                ("aux_lo", C.c_int64), ("aux_hi", C.c_int64)]
+                ("aux_lo", C.c_int64), ("aux_hi", C.c_int64), ("aux2_lo", C.c_int64), ("aux2_hi", C.c_int64)]
 
 
 # Exported symbols and their prototypes (kept in sync with include/merit_dev.h;
@@ -87,6 +88,9 @@ PROTOTYPES = {
     "merit_dev_last_error": (C.c_char_p, []),
     "merit_dev_plan_create": (C.c_int, [C.POINTER(WorkloadDescC), C.POINTER(C.c_void_p)]),
     "merit_dev_plan_destroy": (C.c_int, [C.c_void_p]),
+    "merit_dev_plan_create_multi": (C.c_int, [C.POINTER(WorkloadDescC), C.c_int32, C.POINTER(C.c_void_p)]),
+    "merit_dev_plan_member": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(PlanInfoC), C.POINTER(C.c_int64),
+                                        C.POINTER(C.c_int64)]),
     "merit_dev_plan_query": (C.c_int, [C.c_void_p, C.POINTER(PlanInfoC)]),
     "merit_dev_plan_pack_b": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "merit_dev_run": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,

@@ -12,6 +12,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <cstdio>
 
 #include "plan.hpp"
 
@@ -145,6 +146,125 @@ merit_status merit_dev_plan_create(const merit_workload_desc* desc, merit_plan**
   return MERIT_OK;
 }
 
+// ----------------------------------------------------- multi-workload plans --
+namespace {
+// The 8x8 + 16x16 (fine, coarse) pair of L1 block-matching members the fused
+// SAD kernel computes in one pass: same frames, window, offsets and
+// boundary, argmin without maps, the coarse grid exactly 2 x 2 fine blocks.
+bool fusable_sad(const merit_plan& fine, const merit_plan& coarse) {
+  if (fine.kernel != MERIT_KERNEL_SAD || coarse.kernel != MERIT_KERNEL_SAD) return false;
+  const SadParams &f = fine.sad, &c = coarse.sad;
+  return f.BH == 8 && f.BW == 8 && c.BH == 16 && c.BW == 16 && f.pairs == c.pairs && f.Hc == c.Hc &&
+         f.Wc == c.Wc && f.Hr == c.Hr && f.Wr == c.Wr && f.WY == 65 && f.WX == 65 && c.WY == 65 && c.WX == 65 &&
+         f.oy == c.oy && f.ox == c.ox && f.cy == 0 && f.cx == 0 && c.cy == 0 && c.cx == 0 &&
+         f.boundary == c.boundary && f.ref_is_b == c.ref_is_b && f.argmin && c.argmin && !f.write_map &&
+         !c.write_map && f.BY == 2 * c.BY && f.BX == 2 * c.BX && f.by_count == 0 && c.by_count == 0 &&
+         f.by_begin == 0 && c.by_begin == 0;
+}
+}  // namespace
+
+merit_status merit_dev_plan_create_multi(const merit_workload_desc* descs, int32_t n, merit_plan** out_plan) {
+  if (!descs || !out_plan || n < 1) return fail(MERIT_E_INVALID_ARGUMENT, "null argument or empty workload list");
+  *out_plan = nullptr;
+  merit_plan* g = new (std::nothrow) merit_plan();
+  if (!g) return fail(MERIT_E_INVALID_ARGUMENT, "out of host memory");
+  for (int32_t i = 0; i < n; ++i) {
+    merit_plan* m = nullptr;
+    merit_status st = merit_dev_plan_create(&descs[i], &m);
+    if (st != MERIT_OK) {
+      const std::string msg = "workload " + std::to_string(i) + ": " + g_last_error;
+      delete g;
+      return fail(st, msg);
+    }
+    g->members.push_back(m);
+  }
+  // shared sources (Workload::validate's shape check, engine.hpp:35-36, across members)
+  const merit_workload_desc& d0 = descs[0];
+  for (int32_t i = 1; i < n; ++i) {
+    const merit_workload_desc& d = descs[i];
+    bool same = d.dtype_a == d0.dtype_a && d.dtype_b == d0.dtype_b &&
+                d.view_a.src_rank == d0.view_a.src_rank && d.view_b.src_rank == d0.view_b.src_rank;
+    for (int k = 0; same && k < d.view_a.src_rank; ++k) same = d.view_a.src_shape[k] == d0.view_a.src_shape[k];
+    for (int k = 0; same && k < d.view_b.src_rank; ++k) same = d.view_b.src_shape[k] == d0.view_b.src_shape[k];
+    if (!same) {
+      delete g;
+      return fail(MERIT_E_BAD_PARAMS, "multi-workload plans share their two source tensors (shape / dtype mismatch)");
+    }
+  }
+  merit_plan_info& info = g->info;
+  std::memset(&info, 0, sizeof(info));
+  info.src_a_bytes = g->members[0]->info.src_a_bytes;
+  info.src_b_bytes = g->members[0]->info.src_b_bytes;
+  int64_t out_off = 0, aux_off = 0;
+  for (merit_plan* m : g->members) {
+    g->member_out_off.push_back(out_off);
+    g->member_aux_off.push_back(aux_off);
+    out_off += m->info.out_bytes;
+    aux_off += m->info.aux_elems;
+    info.out_elems += m->info.out_elems;
+    info.n_outputs += m->info.n_outputs;
+    info.algorithmic_ops += m->info.algorithmic_ops;
+    info.executed_ops += m->info.executed_ops;
+    info.launches_per_run += m->info.launches_per_run;
+  }
+  info.out_bytes = out_off;
+  info.aux_elems = aux_off;
+  info.out_rank = 1;
+  info.out_shape[0] = info.out_elems;
+  info.algorithmic_bytes = (double)info.src_a_bytes + (double)info.src_b_bytes + (double)out_off + 4.0 * aux_off;
+  info.kernel = MERIT_KERNEL_MULTI;
+  // fusion: the fine / coarse block-matching pair
+  int fi = -1, ci = -1;
+  if (n == 2) {
+    if (fusable_sad(*g->members[0], *g->members[1])) fi = 0, ci = 1;
+    else if (fusable_sad(*g->members[1], *g->members[0])) fi = 1, ci = 0;
+  }
+  if (fi >= 0) {
+    const merit_plan& f = *g->members[fi];
+    g->kernel = MERIT_KERNEL_SAD;
+    g->sad = f.sad;
+    g->sad.fuse2 = 1;
+    g->sad.BY2 = g->members[ci]->sad.BY;
+    g->sad.BX2 = g->members[ci]->sad.BX;
+    g->fused_aux_off = g->member_aux_off[fi];
+    g->sad.aux2_delta = g->member_aux_off[ci] - g->member_aux_off[fi];
+    info.kernel = MERIT_KERNEL_SAD;
+    info.launches_per_run = 1;
+    info.executed_ops = f.info.algorithmic_ops;  // the coarse SADs are sums of fine ones
+    std::snprintf(info.description, sizeof(info.description),
+                  "sad fused %dx%d + %dx%d pairs=%lld frame=%dx%d blocks=%dx%d+%dx%d window=%dx%d off=%d,%d %s "
+                  "+argmin (no map)",
+                  f.sad.BH, f.sad.BW, 2 * f.sad.BH, 2 * f.sad.BW, (long long)f.sad.pairs, f.sad.Hc, f.sad.Wc,
+                  f.sad.BY, f.sad.BX, g->sad.BY2, g->sad.BX2, f.sad.WY, f.sad.WX, f.sad.oy, f.sad.ox,
+                  f.sad.boundary == MERIT_CLAMP ? "clamp" : "zero");
+  } else {
+    g->kernel = MERIT_KERNEL_MULTI;
+    std::snprintf(info.description, sizeof(info.description), "multi %d workloads (run one after another)", n);
+  }
+  g->desc = d0;
+  g->desc.program = {};
+  g_last_error.clear();
+  *out_plan = g;
+  return MERIT_OK;
+}
+
+merit_status merit_dev_plan_member(const merit_plan* plan, int32_t i, merit_plan_info* info, int64_t* out_off,
+                                   int64_t* aux_off) {
+  if (!plan) return fail(MERIT_E_INVALID_ARGUMENT, "null plan");
+  const int32_t nm = plan->members.empty() ? 1 : static_cast<int32_t>(plan->members.size());
+  if (i < 0 || i >= nm) return fail(MERIT_E_INVALID_ARGUMENT, "member index out of range");
+  if (plan->members.empty()) {
+    if (info) *info = plan->info;
+    if (out_off) *out_off = 0;
+    if (aux_off) *aux_off = 0;
+    return MERIT_OK;
+  }
+  if (info) *info = plan->members[i]->info;
+  if (out_off) *out_off = plan->member_out_off[i];
+  if (aux_off) *aux_off = plan->member_aux_off[i];
+  return MERIT_OK;
+}
+
 merit_status merit_dev_plan_destroy(merit_plan* plan) {
   if (!plan) return MERIT_OK;
   if (plan->device >= 0) {
@@ -218,7 +338,24 @@ merit_status merit_dev_run(const merit_plan* plan, const void* d_a, const void* 
   const merit_plan_info& info = plan->info;
   if (info.out_elems > 0 && !d_out) return fail(MERIT_E_INVALID_ARGUMENT, "null output");
   if (info.aux_elems > 0 && !d_aux) return fail(MERIT_E_INVALID_ARGUMENT, "null aux output");
-  merit_status st = ensure_device_state(*plan);
+  merit_status st = MERIT_OK;
+  if (!plan->members.empty()) {
+    // multi-workload plan: one fused launch, or the members in order
+    if (plan->kernel == MERIT_KERNEL_SAD) {
+      if (!d_a || !d_b) return fail(MERIT_E_INVALID_ARGUMENT, "null source");
+      if ((st = ensure_device_state(*plan)) != MERIT_OK) return st;
+      st = launch_sad(*plan, d_a, d_b, nullptr, static_cast<int32_t*>(d_aux) + plan->fused_aux_off, stream);
+      if (st != MERIT_E_UNSUPPORTED_VIEW) return st;  // else: not fusable for these buffers
+    }
+    for (size_t i = 0; i < plan->members.size(); ++i) {
+      st = merit_dev_run(plan->members[i], d_a, d_b,
+                         d_out ? static_cast<char*>(d_out) + plan->member_out_off[i] : nullptr,
+                         d_aux ? static_cast<int32_t*>(d_aux) + plan->member_aux_off[i] : nullptr, stream);
+      if (st != MERIT_OK) return st;
+    }
+    return MERIT_OK;
+  }
+  st = ensure_device_state(*plan);
   if (st != MERIT_OK) return st;
   switch (plan->kernel) {
     case MERIT_KERNEL_GENERIC: {

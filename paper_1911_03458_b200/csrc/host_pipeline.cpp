@@ -133,9 +133,14 @@ void build_slices(const merit_plan& plan) {
     const int64_t ref_bytes = q.ref_is_b ? in.src_b_bytes : in.src_a_bytes;
     if (q.pairs >= 2) {
       const int64_t n = q.pairs;
-      if (cur_bytes % n || ref_bytes % n || out_b % n || aux_b % n) return;
+      // fused plans: the fine level's records at fused_aux_off, the coarse
+      // level's at fused_aux_off + aux2_delta (int32 elements), per pair each
+      const int64_t x8 = q.fuse2 ? 12 * (int64_t)q.BY * q.BX : 0, x16 = q.fuse2 ? 12 * (int64_t)q.BY2 * q.BX2 : 0;
+      if (cur_bytes % n || ref_bytes % n || out_b % n || (!q.fuse2 && aux_b % n)) return;
+      if (q.fuse2 && aux_b != n * (x8 + x16)) return;
       const int64_t k = slice_count(plan, n);
-      const int64_t cu = cur_bytes / n, ru = ref_bytes / n, ou = out_b / n, xu = aux_b / n;
+      const int64_t cu = cur_bytes / n, ru = ref_bytes / n, ou = out_b / n, xu = q.fuse2 ? x8 : aux_b / n;
+      const int64_t base8 = q.fuse2 ? 4 * plan.fused_aux_off : 0, base16 = q.fuse2 ? base8 + 4 * q.aux2_delta : 0;
       for (int64_t i = 0; i < k; ++i) {
         int64_t u0, u1;
         split(n, k, i, u0, u1);
@@ -149,13 +154,19 @@ void build_slices(const merit_plan& plan) {
         (q.ref_is_b ? s.b_need : s.a_need) = u1 * ru;
         s.out_off = s.out_lo = u0 * ou;
         s.out_hi = u1 * ou;
-        s.aux_off = s.aux_lo = u0 * xu;
-        s.aux_hi = u1 * xu;
+        s.aux_off = s.aux_lo = base8 + u0 * xu;
+        s.aux_hi = base8 + u1 * xu;
+        if (q.fuse2) {
+          s.aux2_lo = base16 + u0 * x16;
+          s.aux2_hi = base16 + u1 * x16;
+          s.sub->sad.aux2_delta = (s.aux2_lo - s.aux_lo) / 4;
+        }
         v.push_back(s);
       }
     } else {
       // block-row bands of the single pair; pointers are not offset (the
       // kernel writes global block indices)
+      if (q.fuse2) return;  // a fused single pair runs unsliced
       const int64_t n = q.BY;
       if (n < 2 || cur_bytes % q.Hc || ref_bytes % q.Hr || out_b % n || aux_b % n) return;
       const int64_t k = slice_count(plan, n);
@@ -300,6 +311,8 @@ merit_status run_host_pipelined(const merit_plan& plan, void* da, void* db, void
       e = cudaMemcpyAsync(ho + sl.out_lo, co + sl.out_lo, sl.out_hi - sl.out_lo, cudaMemcpyDeviceToHost, d2h);
     if (e == cudaSuccess && in.aux_elems > 0 && sl.aux_hi > sl.aux_lo)
       e = cudaMemcpyAsync(hx + sl.aux_lo, cx + sl.aux_lo, sl.aux_hi - sl.aux_lo, cudaMemcpyDeviceToHost, d2h);
+    if (e == cudaSuccess && in.aux_elems > 0 && sl.aux2_hi > sl.aux2_lo)
+      e = cudaMemcpyAsync(hx + sl.aux2_lo, cx + sl.aux2_lo, sl.aux2_hi - sl.aux2_lo, cudaMemcpyDeviceToHost, d2h);
   }
   if (e == cudaSuccess && st == MERIT_OK) e = cudaEventRecord(ev(1), d2h);
   if (e == cudaSuccess && st == MERIT_OK) e = cudaStreamWaitEvent(s, ev(1), 0);
@@ -324,11 +337,12 @@ extern "C" merit_status merit_dev_plan_slices(const merit_plan* plan, merit_host
   for (int64_t i = 0; i < cap && i < *n_slices; ++i) {
     const merit_dev::HostSlice& s = plan->slices[i];
     out[i] = {std::min<int64_t>(s.a_need, plan->info.src_a_bytes), std::min<int64_t>(s.b_need, plan->info.src_b_bytes),
-              s.out_lo, s.out_hi, s.aux_lo, s.aux_hi};
+              s.out_lo, s.out_hi, s.aux_lo, s.aux_hi, s.aux2_lo, s.aux2_hi};
   }
   return MERIT_OK;
 }
 
 merit_plan::~merit_plan() {
   for (merit_dev::HostSlice& s : slices) delete s.sub;
+  for (merit_plan* m : members) merit_dev_plan_destroy(m);
 }

@@ -718,6 +718,7 @@ merit_status lower(const merit_workload_desc& d, merit_plan& plan) {
   }
   info.kernel = plan.kernel;
   info.out_bytes = info.out_elems * elem_size(d.dtype_out);
+  info.executed_ops = info.algorithmic_ops;
   if (plan.kernel == MERIT_KERNEL_CONV_TC) info.launches_per_run = 1;
   return MERIT_OK;
 }

@@ -94,6 +94,12 @@ struct SadParams {
   // Block-row band of one launch (pipelined host-buffer runs): block rows
   // [by_begin, by_begin + by_count) of every pair; by_count 0 = all BY rows.
   int32_t by_begin = 0, by_count = 0;
+  // Fused coarse level (multi-workload plans): also the argmin of the
+  // 2BH x 2BW blocks made of 2 x 2 of these blocks, same window and frames,
+  // written at d_aux + aux2_delta int32 elements (merged grid BY2 x BX2).
+  int32_t fuse2 = 0;
+  int32_t BY2 = 0, BX2 = 0;
+  int64_t aux2_delta = 0;
 };
 
 // K3: implicit-GEMM convolution on tcgen05 (mac_program over conv views).
@@ -148,6 +154,7 @@ struct HostSlice {
   int64_t a_need = 0, b_need = 0;       // source prefix (bytes) that must have landed
   int64_t out_lo = 0, out_hi = 0;       // bytes written (D2H ranges)
   int64_t aux_lo = 0, aux_hi = 0;
+  int64_t aux2_lo = 0, aux2_hi = 0;     // fused plans: the coarse level's records
 };
 }  // namespace merit_dev
 
@@ -190,6 +197,12 @@ struct merit_plan {
   mutable std::vector<merit_dev::HostSlice> slices;
   mutable void* copy_stream[2] = {nullptr, nullptr};
   mutable std::vector<void*> copy_events;
+  // Multi-workload plans (merit_dev_plan_create_multi): the owned member
+  // plans, their output (bytes) / argmin (int32 elements) offsets, and for a
+  // fused plan (kernel SAD, sad.fuse2) the fine level's record offset.
+  std::vector<merit_plan*> members;
+  std::vector<int64_t> member_out_off, member_aux_off;
+  int64_t fused_aux_off = 0;
   ~merit_plan();
 };
 

@@ -678,7 +678,184 @@ __device__ __forceinline__ void sad_tile_work_warp(const SadLaunch& L, void* __r
   }
 }
 
-template <int BLK, int D, int NBY, int NT, int WXC, bool WARP = false>
+
+// Fused 8x8 + 16x16 matching (multi-workload plans, merit_dev_plan_create_multi):
+// the +/-32 search of 8x8 blocks (WX = WY = 65, two block rows per tile, as
+// sad_tile_work_warp<8, 2, 65>) also yields the SAD of every 16x16 block made
+// of 2 x 2 of them at every displacement — the four 8x8 SADs at the same
+// (dy, dx) sum to it exactly (integers) — so the 16x16 workload costs a few
+// adds and a shuffle per displacement instead of a second pass over the
+// frames.  Lane mapping: the 16 warps of the CTA are (block-column pair q,
+// dx quarter h) = (w / 4, w % 4); lanes 0-15 own 8x8 block column 2q,
+// lanes 16-31 block column 2q + 1, both at dx = 16 h + (lane & 15), so lanes
+// l and l ^ 16 hold the left and right halves of one 16x16 block at the same
+// displacement: u = (top + bottom)(l) + (top + bottom)(l ^ 16).  The 65th
+// column dx = 64 is split over the lanes by dy = 16 h + (lane & 15), the
+// corner (64, 64) is shared by warp h = 3.  Argmin: REDUX over each
+// half-warp (8x8) and the whole warp (16x16), then one shared atomic per
+// warp and slot; the fourth warp to arrive writes the record.
+template <typename AfterCw>
+__device__ __forceinline__ void sad_tile_work_fused(const SadLaunch& L, int32_t* __restrict__ aux, int tile,
+                                                    const uint32_t* curw, const uint32_t* copies, uint32_t* keys,
+                                                    uint32_t* cnt, AfterCw after_cw) {
+  constexpr int BLK = 8, NBY = 2, D = 33, WX = 65, WY = 65, BWW = 2, G = 2;
+  const SadParams& p = L.p;
+  const int cpw = L.cur_pitch / 4;
+  const int warp = static_cast<int>(threadIdx.x) >> 5;
+  const int q = warp >> 2, h = warp & 3;
+  const int lane = static_cast<int>(threadIdx.x) & 31;
+  const int half = lane >> 4, l16 = lane & 15;
+  const int ib = 2 * q + half;     // this lane's 8x8 block column in the tile
+  const int dxl = 16 * h + l16;    // this lane's column
+  const unsigned hmask = half ? 0xffff0000u : 0x0000ffffu;
+  int t2, tx;
+  sad_tile_coords(tile, L.n_full_tiles, L.n_full_x, L.ntx_m, L.ntx_s, t2, tx);
+  const int pair_i = static_cast<int>(fast_div(t2, L.byt_m, L.byt_s));
+  const int by = L.by0 + (t2 - pair_i * L.BYT) * NBY;  // first 8x8 block row of the tile (even)
+  const long long pair = pair_i;
+  const int bx0 = tx * L.TBX;
+  const int nb = min(L.TBX, p.BX - bx0);  // even (BX = 2 BX2)
+  if (2 * q >= nb) {  // warp-uniform
+    after_cw();
+    return;
+  }
+  const int dcur = (bx0 * BLK + p.cx) - floor16(bx0 * BLK + p.cx);
+  const uint32_t* cb = curw + (dcur >> 2) + ib * BWW;
+  uint32_t cw[NBY][BLK][BWW];
+#pragma unroll
+  for (int n = 0; n < NBY; ++n)
+#pragma unroll
+    for (int i = 0; i < BLK; ++i)
+#pragma unroll
+      for (int j = 0; j < BWW; ++j) cw[n][i][j] = cb[(n * BLK + i) * cpw + j];
+  // corner words: 8 rows x 2 words of this half's block, one per lane
+  uint32_t ccw[NBY];
+  if (h == 3) {
+#pragma unroll
+    for (int n = 0; n < NBY; ++n) ccw[n] = cb[(n * BLK + (l16 >> 1)) * cpw + (l16 & 1)];
+  }
+  after_cw();
+  const long long blk_index = (pair * p.BY + by) * (long long)p.BX + bx0 + ib;
+  const uint32_t kmul = L.key_mul;
+  uint32_t best[NBY], best2 = 0xffffffffu;
+#pragma unroll
+  for (int n = 0; n < NBY; ++n) best[n] = 0xffffffffu;
+  const int col = ib * BLK + dxl;
+#pragma unroll 1
+  for (int ig = 0; ig < G; ++ig) {
+    const uint32_t* cp = copies + (col & 3) * L.CS + (col >> 2) + ig * D * L.Ww;
+    uint32_t acc[NBY][D];
+#pragma unroll
+    for (int n = 0; n < NBY; ++n)
+#pragma unroll
+      for (int d = 0; d < D; ++d) acc[n][d] = 0;
+#pragma unroll
+    for (int r = 0; r < D + NBY * BLK - 1; ++r) {
+      uint32_t rwv[BWW];
+#pragma unroll
+      for (int j = 0; j < BWW; ++j) rwv[j] = cp[j];
+      cp += L.Ww;
+#pragma unroll
+      for (int n = 0; n < NBY; ++n)
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+          const int i = r - d - n * BLK;
+          if (i >= 0 && i < BLK) {
+#pragma unroll
+            for (int j = 0; j < BWW; ++j) acc[n][d] = vabsdiff4_acc(cw[n][i][j], rwv[j], acc[n][d]);
+          }
+        }
+    }
+    // the last group of the 65-row window has 32 rows (65 = 33 + 32)
+    const int nd = ig == 0 ? D : D - 1;
+    uint32_t bn0 = 0xffffffffu, bn1 = 0xffffffffu, bn2 = 0xffffffffu;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      if (d < nd) {
+        const uint32_t c = static_cast<uint32_t>(d * WX);
+        bn0 = min(bn0, acc[0][d] * kmul + c);
+        bn1 = min(bn1, acc[1][d] * kmul + c);
+        // 16x16: this half's top + bottom, plus the other half's (lane ^ 16)
+        const uint32_t sv = acc[0][d] + acc[1][d];
+        const uint32_t so = __shfl_xor_sync(0xffffffffu, sv, 16);
+        bn2 = min(bn2, sv * kmul + (so * kmul + c));
+      }
+    }
+    const uint32_t k0 = static_cast<uint32_t>(ig * D * WX + dxl);
+    best[0] = min(best[0], bn0 + k0);
+    best[1] = min(best[1], bn1 + k0);
+    best2 = min(best2, bn2 + k0);
+  }
+  // the last column dx = 64 (byte column ib*8 + 64: shifted copy 0): this
+  // lane takes dy = 16 h + (lane & 15); block row n reads staged rows dy + 8 n ..
+  const int colx = ib * BLK + (WX - 1);
+  const uint32_t* cx0 = copies + (colx & 3) * L.CS + (colx >> 2);
+  {
+    uint32_t ax[NBY];
+#pragma unroll
+    for (int n = 0; n < NBY; ++n) {
+      ax[n] = 0;
+      const uint32_t* cx = cx0 + (dxl + n * BLK) * L.Ww;
+#pragma unroll
+      for (int i = 0; i < BLK; ++i) {
+#pragma unroll
+        for (int j = 0; j < BWW; ++j) ax[n] = vabsdiff4_acc(cw[n][i][j], cx[j], ax[n]);
+        cx += L.Ww;
+      }
+    }
+    const uint32_t c = static_cast<uint32_t>(dxl * WX + (WX - 1));
+    best[0] = min(best[0], ax[0] * kmul + c);
+    best[1] = min(best[1], ax[1] * kmul + c);
+    const uint32_t sv = ax[0] + ax[1];
+    const uint32_t so = __shfl_xor_sync(0xffffffffu, sv, 16);
+    best2 = min(best2, (sv + so) * kmul + c);
+  }
+  if (h == 3) {
+    // corner (64, 64): each half's 8x8 block from its 16 lanes, the 16x16 block from all 32
+    uint32_t v[NBY];
+#pragma unroll
+    for (int n = 0; n < NBY; ++n)
+      v[n] = vabsdiff4_acc(ccw[n], cx0[(WY - 1 + n * BLK + (l16 >> 1)) * L.Ww + (l16 & 1)], 0u);
+    const uint32_t c = static_cast<uint32_t>((WY - 1) * WX + (WX - 1));
+    const uint32_t s0 = __reduce_add_sync(hmask, v[0]);
+    const uint32_t s1 = __reduce_add_sync(hmask, v[1]);
+    const uint32_t s2 = __reduce_add_sync(0xffffffffu, v[0] + v[1]);
+    if (l16 == 0) {
+      best[0] = min(best[0], s0 * kmul + c);
+      best[1] = min(best[1], s1 * kmul + c);
+    }
+    if (lane == 0) best2 = min(best2, s2 * kmul + c);
+  }
+  if (by >= L.by1) return;
+  // 8x8 records: 4 warps (h) x 16 lanes per block
+  auto fold = [&](uint32_t key, int slot, int32_t* a) {
+    atomicMin(&keys[slot], key);
+    __threadfence_block();
+    if (atomicAdd(&cnt[slot], 1u) == 3u) {
+      __threadfence_block();
+      const uint32_t fin = atomicExch(&keys[slot], 0xffffffffu);
+      cnt[slot] = 0u;
+      const int k = static_cast<int>(fin & 0xffffu);
+      const int dy = k / WX, dx = k - (k / WX) * WX;
+      a[0] = dy + p.oy - p.cy;
+      a[1] = dx + p.ox - p.cx;
+      a[2] = static_cast<int32_t>(fin >> 16);
+    }
+  };
+#pragma unroll
+  for (int n = 0; n < NBY; ++n) {
+    const uint32_t key = __reduce_min_sync(hmask, best[n]);
+    if (l16 == 0) fold(key, n * L.TBX + ib, aux + (blk_index + n * (long long)p.BX) * 3);
+  }
+  // 16x16 record of block (by / 2, (bx0 + 2 q) / 2)
+  const uint32_t key2 = __reduce_min_sync(0xffffffffu, best2);
+  if (lane == 0) {
+    const long long b2 = (pair * p.BY2 + by / 2) * (long long)p.BX2 + (bx0 >> 1) + q;
+    fold(key2, NBY * L.TBX + q, aux + p.aux2_delta + b2 * 3);
+  }
+}
+
+template <int BLK, int D, int NBY, int NT, int WXC, int MODE = 0>
 __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1)
 sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, void* __restrict__ out,
            int32_t* __restrict__ aux, SadLaunch L, const __grid_constant__ CUtensorMap ref_map,
@@ -739,7 +916,7 @@ sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, voi
                       reinterpret_cast<uint8_t*>(raw0 + (buf ^ 1) * raw_words),
                       smem_u32(cur0 + (buf ^ 1) * cur_words),
                       reinterpret_cast<uint8_t*>(cur0 + (buf ^ 1) * cur_words), bar0 + 8u * (buf ^ 1));
-    if constexpr (WARP)
+    if constexpr (MODE == 1)
       sad_tile_work_warp<BLK, NBY, WXC>(L, out, aux, tile, curw, copies, keys, cnt, [] {});
     else
       sad_tile_work<BLK, D, NBY, WXC>(L, out, aux, tile, curw, copies, keys, cnt, [] {});
@@ -761,7 +938,7 @@ sad_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, voi
 // The last warp to load its current blocks of tile k issues tile k + 2's TMA
 // into raw / cur[b]: every thread built its share of tile k + 1 (the last
 // reader of raw) before it started tile k.
-template <int BLK, int D, int NBY, int NT, int WXC, bool WARP = false>
+template <int BLK, int D, int NBY, int NT, int WXC, int MODE = 0>
 __global__ void __launch_bounds__(NT, NT <= 256 ? 2 : 1)
 sad_async_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ ref, void* __restrict__ out,
                  int32_t* __restrict__ aux, SadLaunch L, const __grid_constant__ CUtensorMap ref_map,
@@ -773,7 +950,7 @@ sad_async_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ re
   uint32_t* raw0 = reinterpret_cast<uint32_t*>(smem_b + ((128u - (smem_u32(smem_b) & 127u)) & 127u));
   uint32_t* cur0 = raw0 + raw_words;
   uint32_t* copies0 = cur0 + 2 * cur_words;
-  const int nslot = NBY * L.TBX;
+  const int nslot = NBY * L.TBX + (MODE == 2 ? L.TBX / 2 : 0);  // fused: + the 16x16 slots
   uint32_t* keys0 = copies0 + 12 * L.CS;
   uint32_t* cnt0 = keys0 + 2 * nslot;
   uint32_t* ctr = cnt0 + 2 * nslot;
@@ -840,7 +1017,10 @@ sad_async_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ re
             }
           }
         };
-    if constexpr (WARP)
+    if constexpr (MODE == 2)
+      sad_tile_work_fused(L, aux, tile_of(k), cur0 + b * cur_words, copies0 + c * 4 * L.CS, keys0 + b * nslot,
+                          cnt0 + b * nslot, refill);
+    else if constexpr (MODE == 1)
       sad_tile_work_warp<BLK, NBY, WXC>(L, out, aux, tile_of(k), cur0 + b * cur_words, copies0 + c * 4 * L.CS,
                                         keys0 + b * nslot, cnt0 + b * nslot, refill);
     else
@@ -899,7 +1079,10 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
   // tiles, every lane busy (sad_tile_work_warp)
   const char* wme = getenv("MERIT_SAD_WARP");
   const bool warp_mode = D == 33 && (BLK == 16 ? (p.WX == 33 || p.WX == 65) : p.WX == 65) && p.WY == p.WX &&
-                         p.BX >= 8 && !(wme && wme[0] == '0');
+                         p.BX >= 8 && (!(wme && wme[0] == '0') || p.fuse2);
+  if (p.fuse2 && !(BLK == 8 && warp_mode && p.write_map == 0 && p.argmin && p.BX == 2 * p.BX2 &&
+                   p.BY == 2 * p.BY2))
+    return fail(MERIT_E_UNSUPPORTED_VIEW, "fused 8x8 + 16x16 SAD needs the +/-32 warp kernel");
   if (warp_mode) {
     nt = 8 * (p.WX - 1);  // 8 blocks x (WX - 1) / 32 warps
     L.TBX = 8;
@@ -981,10 +1164,13 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
   if (L.n_tiles == 0) return MERIT_OK;
   if (smem > smem_cap) return fail(MERIT_E_UNSUPPORTED_VIEW, "SAD footprint exceeds shared memory");
   // barrier-free variant (TMA staging): two staging buffers, three copy buffers
+  const size_t nslot_h = static_cast<size_t>(L.nby * L.TBX + (p.fuse2 ? L.TBX / 2 : 0));
   const size_t smem_async = 128 + 1ull * L.raw_buf + 2ull * L.cur_buf +
-                            4ull * (12ull * L.CS + 4ull * L.nby * L.TBX + 2) + 8 + 64;
+                            4ull * (12ull * L.CS + 4ull * nslot_h + 2) + 8 + 64;
   const char* ae = getenv("MERIT_SAD_ASYNC");
-  const bool use_async = L.tma && !(ae && ae[0] == '0') && smem_async <= smem_cap;
+  const bool use_async = L.tma && (!(ae && ae[0] == '0') || p.fuse2) && smem_async <= smem_cap;
+  if (p.fuse2 && !(use_async && L.nby == 2 && L.by0 % 2 == 0 && L.by1 % 2 == 0))
+    return fail(MERIT_E_UNSUPPORTED_VIEW, "fused 8x8 + 16x16 SAD needs TMA staging of two-row tiles");
   auto kern = nt == 512 ? sad_kernel<BLK, D, 1, 512, 0> : sad_kernel<BLK, D, 1, 256, 0>;
   if constexpr (BLK == 8) {
     if (L.nby == 2) kern = nt == 512 ? sad_kernel<BLK, D, 2, 512, 0> : sad_kernel<BLK, D, 2, 256, 0>;
@@ -1035,6 +1221,7 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
       } else {
         if (kern == sad_kernel<8, 33, 2, 512, 65, true>) kern = sad_async_kernel<8, 33, 2, 512, 65, true>;
         if (kern == sad_kernel<8, 33, 1, 512, 65, true>) kern = sad_async_kernel<8, 33, 1, 512, 65, true>;
+        if (p.fuse2) kern = sad_async_kernel<8, 33, 2, 512, 65, 2>;
       }
     }
   }
@@ -1061,6 +1248,7 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
   e = launch_pdl(kern, dim3(static_cast<unsigned>(grid)), dim3(threads), smem_launch, s, 1, cur, ref, out, aux, L,
                  ref_map, cur_map);
   if (e != cudaSuccess) return cuda_check(e, "launch(sad)");
+  if (p.fuse2) return launch_status("sad_async_kernel<fused 8x8 + 16x16>");
   return launch_status(warp_mode ? (use_async ? "sad_async_kernel<warp per block>" : "sad_kernel<warp per block>")
                                  : (use_async ? "sad_async_kernel" : "sad_kernel"));
 }

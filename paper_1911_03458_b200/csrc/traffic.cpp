@@ -39,6 +39,7 @@ extern "C" merit_status merit_dev_tiled_traffic(const merit_plan* plan, const in
                                                 merit_traffic_report* report) {
   using namespace merit_dev;
   if (!plan || !t_p || !t_a || !report) return fail(MERIT_E_INVALID_ARGUMENT, "null argument");
+  if (!plan->members.empty()) return fail(MERIT_E_INVALID_ARGUMENT, "run_tiled takes a single-workload plan");
   const merit_view_spec& va = plan->desc.view_a;
   const merit_view_spec& vb = plan->desc.view_b;
   const int pr = va.p_rank, ar = va.a_rank;

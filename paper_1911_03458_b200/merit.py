@@ -95,6 +95,7 @@ class Kernel(enum.IntEnum):  # merit_kernel_kind
     SAD = 2
     CONV_TC = 3
     CORR = 4
+    MULTI = 5
 
 
 FLAG_EXACT = 1
@@ -454,6 +455,75 @@ class Plan:
             aux.ctypes.data_as(C.c_void_p) if aux is not None else None,
             C.c_void_p(stream or 0)))
         return out, aux
+
+
+class PlanGroup(Plan):
+    """Several workloads over the same two sources as one plan
+    (merit_dev_plan_create_multi): what a reference caller does with one
+    run_full per workload.  Members the device computes in one pass are fused
+    (the 8x8 + 16x16 block searches of C5); ``run`` takes the shared sources
+    once and writes the members' outputs / argmin records back to back
+    (``members[i]["out_offset"]`` bytes, ``["aux_offset"]`` int32 elements)."""
+
+    def __init__(self, ws: Sequence[Workload], flags: int = 0):
+        self.lib = _capi.load()
+        ws = list(ws)
+        if not ws:
+            raise Error(ErrorCode.InvalidArgument, "empty workload list")
+        self._holders = [_DescHolder(w, flags) for w in ws]
+        self._holder = self._holders[0]
+        arr = (_capi.WorkloadDescC * len(ws))(*[h.desc for h in self._holders])
+        h = C.c_void_p()
+        _check(self.lib.merit_dev_plan_create_multi(arr, len(ws), C.byref(h)))
+        self.handle = h
+        info = _capi.PlanInfoC()
+        _check(self.lib.merit_dev_plan_query(self.handle, C.byref(info)))
+        self.info = info
+        self.kernel = Kernel(info.kernel)
+        self.description = info.description.decode()
+        self.dtypes = self._holder.dtypes
+        self.out_shape = (int(info.out_elems),)
+        self.members = []
+        for i, w in enumerate(ws):
+            mi = _capi.PlanInfoC()
+            oo, ao = C.c_int64(), C.c_int64()
+            _check(self.lib.merit_dev_plan_member(self.handle, i, C.byref(mi), C.byref(oo), C.byref(ao)))
+            self.members.append({"info": mi, "out_offset": oo.value, "aux_offset": ao.value,
+                                 "out_shape": tuple(mi.out_shape[k] for k in range(mi.out_rank)),
+                                 "dtype_out": self._holders[i].dtypes[2]})
+
+    def run_host(self, src_a, src_b, out=None, aux=None, stream=None):
+        """merit_dev_run_host: [(out_i or None, aux_i or None) per member]."""
+        a = np.ascontiguousarray(src_a)
+        b = np.ascontiguousarray(src_b)
+        if a.nbytes != self.info.src_a_bytes or b.nbytes != self.info.src_b_bytes:
+            raise Error(ErrorCode.BadParams, "source shape mismatch")
+        obuf = np.empty(max(1, int(self.info.out_bytes)), np.uint8)
+        xbuf = np.empty(max(1, int(self.info.aux_elems)), np.int32)
+        _check(self.lib.merit_dev_run_host(
+            self.handle, a.ctypes.data_as(C.c_void_p), b.ctypes.data_as(C.c_void_p),
+            obuf.ctypes.data_as(C.c_void_p) if self.info.out_elems else None,
+            xbuf.ctypes.data_as(C.c_void_p) if self.info.aux_elems else None, C.c_void_p(stream or 0)))
+        res = []
+        for m in self.members:
+            mi = m["info"]
+            o = None
+            if mi.out_elems:
+                o = obuf[m["out_offset"]:m["out_offset"] + mi.out_bytes].view(_NP_OF[m["dtype_out"]])
+                o = o.reshape(m["out_shape"]).copy()
+            x = xbuf[m["aux_offset"]:m["aux_offset"] + mi.aux_elems].reshape(-1, 3).copy() if mi.aux_elems else None
+            res.append((o, x))
+        return res
+
+
+def run_full_many(ws: Sequence[Workload], flags: int = 0):
+    """run_full (engine.hpp:282-287) of several workloads over the same two
+    sources, as one device plan: [(output or None, argmin records or None)]."""
+    ws = list(ws)
+    for w in ws:
+        _check_sources(w)
+    g = PlanGroup(ws, flags)
+    return g.run_host(_host(ws[0].src_a), _host(ws[0].src_b))
 
 
 def run_full(w: Workload, flags: int = 0):

@@ -90,14 +90,21 @@ def shard_band(w: Workload, world: int, rank: int) -> Tuple[Workload, Tuple[int,
     offset is shifted by the slice start, so every gather reads the same
     value as in the unsplit workload (rows outside the original source stay
     outside the slice: ZERO_PAD / CLAMP / REJECT behave identically).  No
-    exchange between ranks."""
+    exchange between ranks.
+
+    The shard records where its source slices start in the original sources
+    (``shard.row_origin = (rows of src_a, rows of src_b)``): outputs are
+    identical, but anything expressed in source coordinates — e.g. the
+    argmin records' motion vector, ref row - cur row — is relative to the
+    slices and shifts by row_origin[ref] - row_origin[cur]."""
     total = w.view_a.p_shape[0]
     start, stop = shard_range(total, world, rank)
     kshape = list(w.view_a.p_shape) + list(w.view_a.a_shape)
     s = copy.copy(w)
+    origin = [0, 0]
     s.view_a = copy.deepcopy(w.view_a)
     s.view_b = copy.deepcopy(w.view_b)
-    for attr_v, attr_s in (("view_a", "src_a"), ("view_b", "src_b")):
+    for side, (attr_v, attr_s) in enumerate((("view_a", "src_a"), ("view_b", "src_b"))):
         v = getattr(s, attr_v)
         v.p_shape[0] = stop - start
         uses0 = [t for t in v.terms if t.component == 0]
@@ -116,7 +123,9 @@ def shard_band(w: Workload, world: int, rank: int) -> Tuple[Workload, Tuple[int,
         # component 0 now counts from 0: fold start*stride - r0 into one term
         t0 = next(t for t in v.terms if t.component == 0)
         t0.offset += start * t0.stride - r0
+        origin[side] = r0
         src = getattr(w, attr_s)
         if src is not None:
             setattr(s, attr_s, np.ascontiguousarray(src[r0:r1 + 1]))
+    s.row_origin = tuple(origin)
     return s, (start, stop)

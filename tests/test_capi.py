@@ -214,3 +214,53 @@ def test_maxpool_reject_view_b_goes_to_error_path():
     assert Plan(w).kernel == Kernel.MAXPOOL          # in range: still K1
     w.view_b.terms = [ViewTerm(0, 0, 1, 0)]            # image index into a (1,) source
     assert Plan(w).kernel == Kernel.GENERIC
+
+
+def _me_pair_views(h, wd, r, pairs=None):
+    w16 = W.me_view(h, wd, 16, r, pairs=pairs)
+    w8 = W.me_view(h, wd, 8, r, pairs=pairs)
+    return w16, w8
+
+
+def test_multi_plan_fuses_c5_block_sizes():
+    from paper_1911_03458_b200 import PlanGroup
+    w16, w8 = _me_pair_views(2160, 3840, 32, pairs=4)
+    g = PlanGroup([w16, w8], FLAG_ARGMIN | FLAG_NO_MAP)
+    assert g.kernel == Kernel.SAD and "fused" in g.description
+    b16, b8 = 4 * 135 * 240, 4 * 270 * 480
+    assert g.info.aux_elems == 3 * (b16 + b8) and g.info.out_elems == 0
+    assert [m["aux_offset"] for m in g.members] == [0, 3 * b16]
+    assert g.info.n_outputs == (b16 + b8) * 65 * 65
+    assert g.info.algorithmic_ops == (b16 * 256 + b8 * 64) * 65 * 65
+    assert g.info.executed_ops == b8 * 64 * 65 * 65    # the 16x16 SADs are sums of 8x8 ones
+    assert g.info.launches_per_run == 1
+    # member order does not matter
+    g2 = PlanGroup([w8, w16], FLAG_ARGMIN | FLAG_NO_MAP)
+    assert g2.kernel == Kernel.SAD and [m["aux_offset"] for m in g2.members] == [0, 3 * b8]
+    # host pipelining slices by frame pairs; every record range lands once
+    sl = g.host_slices()
+    assert len(sl) >= 2
+    fine = sorted((s["aux_lo"], s["aux_hi"]) for s in sl)
+    coarse = sorted((s["aux2_lo"], s["aux2_hi"]) for s in sl)
+    assert fine[0][0] == 4 * 3 * b16 and fine[-1][1] == 4 * 3 * (b16 + b8)
+    assert coarse[0][0] == 0 and coarse[-1][1] == 4 * 3 * b16
+    for lst in (fine, coarse):
+        assert all(a[1] == b[0] for a, b in zip(lst, lst[1:]))
+
+
+def test_multi_plan_unfusable_runs_members():
+    from paper_1911_03458_b200 import PlanGroup
+    # +/-16 window: no fused kernel; H = 72: 9 rows of 8x8 blocks are not 2 x 4
+    for h, r in ((2160, 16), (72, 32)):
+        w16, w8 = _me_pair_views(h, 256, r)
+        g = PlanGroup([w16, w8], FLAG_ARGMIN | FLAG_NO_MAP)
+        assert g.kernel == Kernel.MULTI and g.info.launches_per_run == 2
+    # maps requested: separate launches too
+    w16, w8 = _me_pair_views(2160, 3840, 32)
+    assert PlanGroup([w16, w8], FLAG_ARGMIN).kernel == Kernel.MULTI
+    # a conv and a max-pool over different sources: BadParams
+    c = W.conv_nchw_view(1, 8, 10, 10, 4)
+    m = W.maxpool_nchw_view(1, 8, 10, 10)
+    with pytest.raises(Error) as ei:
+        PlanGroup([c, m])
+    assert ei.value.code == ErrorCode.BadParams
