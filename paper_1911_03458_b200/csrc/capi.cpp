@@ -75,7 +75,8 @@ merit_status merit_dev::ensure_device_state(const merit_plan& plan) {
     if ((st = cuda_check(cudaMalloc(&plan.d_err, 16), "cudaMalloc(err)")) != MERIT_OK) return st;
     if ((st = cuda_check(cudaMemset(plan.d_err, 0, 16), "cudaMemset(err)")) != MERIT_OK) return st;
   }
-  if (plan.kernel == MERIT_KERNEL_GENERIC && !plan.d_prog) {
+  const bool narrow = plan.kernel == MERIT_KERNEL_SAD && plan.sad.narrow;
+  if ((plan.kernel == MERIT_KERNEL_GENERIC || narrow) && !plan.d_prog) {
     if ((st = cuda_check(cudaMalloc(&plan.d_prog, sizeof(ProgramImage)), "cudaMalloc(prog)")) !=
         MERIT_OK)
       return st;
@@ -83,6 +84,11 @@ merit_status merit_dev::ensure_device_state(const merit_plan& plan) {
                                     cudaMemcpyHostToDevice),
                          "cudaMemcpy(prog)")) != MERIT_OK)
       return st;
+  }
+  if (narrow && !plan.d_narrow) {
+    // u8 copies of both frames + the validity flag
+    const size_t bytes = (plan.info.src_a_bytes + plan.info.src_b_bytes) / 4 + 64;
+    if ((st = cuda_check(cudaMalloc(&plan.d_narrow, bytes), "cudaMalloc(narrow)")) != MERIT_OK) return st;
   }
   if (plan.kernel == MERIT_KERNEL_CONV_TC && !plan.d_packed_b) {
     if ((st = cuda_check(cudaMalloc(&plan.d_packed_b, plan.conv.packed_b_bytes),
@@ -274,6 +280,7 @@ merit_status merit_dev_plan_destroy(merit_plan* plan) {
     if (plan->d_prog) cudaFree(plan->d_prog);
     if (plan->d_err) cudaFree(plan->d_err);
     if (plan->d_packed_b) cudaFree(plan->d_packed_b);
+    if (plan->d_narrow) cudaFree(plan->d_narrow);
     if (plan->pack_event) cudaEventDestroy(static_cast<cudaEvent_t>(plan->pack_event));
     cudaSetDevice(cur);
   }
@@ -368,9 +375,16 @@ merit_status merit_dev_run(const merit_plan* plan, const void* d_a, const void* 
     case MERIT_KERNEL_MAXPOOL:
       if (!d_a) return fail(MERIT_E_INVALID_ARGUMENT, "null source");
       return launch_maxpool(*plan, d_a, d_out, stream);
-    case MERIT_KERNEL_SAD:
+    case MERIT_KERNEL_SAD: {
       if (!d_a || !d_b) return fail(MERIT_E_INVALID_ARGUMENT, "null source");
-      return launch_sad(*plan, d_a, d_b, d_out, d_aux, stream);
+      if (!plan->sad.narrow) return launch_sad(*plan, d_a, d_b, d_out, d_aux, stream);
+      // the plan's u8 frame copies are shared: stream-ordered like on-the-fly packing
+      std::lock_guard<std::mutex> lk(plan->pack_mu);
+      if ((st = pack_wait(*plan, stream)) != MERIT_OK) return st;
+      st = launch_sad_narrowed(*plan, d_a, d_b, d_out, stream);
+      if (st == MERIT_OK) st = pack_done(*plan, stream);
+      return st;
+    }
     case MERIT_KERNEL_CONV_TC: {
       const void* in = plan->conv_swapped ? d_b : d_a;
       const void* w = plan->conv_swapped ? d_a : d_b;

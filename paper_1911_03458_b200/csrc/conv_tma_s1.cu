@@ -61,6 +61,7 @@ struct S1Args {
   uint32_t b_plane;    // BN * 128: one tap, one split plane
   uint32_t b_slot;     // 3 taps x nsplit planes
   int nr, na, nb;
+  int resident;        // nb == n_groups: every group's weights stay in their B slot (loaded once per CTA)
   unsigned long long* prof;  // MERIT_CONV_DEBUG & 64: per-warp [total, wait1, wait2, wait3]
   int debug;
 };
@@ -286,7 +287,20 @@ conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
     // packed (conv_pack_kernel) k-block (ky, cb, kx) = [hi][lo] planes of
     // BN rows; the slot holds [hi: kx 0 | 1 | 2][lo: kx 0 | 1 | 2], i.e. one
     // K-major SW128 image of N = 3 BN rows per split plane.
-    if (lane == 0) {
+    if (lane == 0 && A.resident) {
+      // weights resident: every group's full stacked-tap image into its own
+      // slot once; half units address their rows inside it (MMA warp)
+      constexpr int nsp = SPLIT3 ? 2 : 1;
+      if (blockIdx.x < A.n_units) {
+        for (int g = 0; g < A.n_groups; ++g) {
+          mbar_expect_tx(b_full(g), 3u * nsp * A.b_plane);
+          for (int kx = 0; kx < 3; ++kx)
+            for (int sp = 0; sp < nsp; ++sp)
+              bulk_g2s(bring + g * A.b_slot + (sp * 3 + kx) * A.b_plane,
+                       A.wpk + ((long long)(g * 3 + kx) * nsp + sp) * A.b_plane, A.b_plane, b_full(g));
+        }
+      }
+    } else if (lane == 0) {
       constexpr int nsp = SPLIT3 ? 2 : 1;
       int st = 0;
       uint32_t ph = 0;
@@ -325,13 +339,43 @@ conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * acc_cols;
       for (int g = 0; g < A.n_groups; ++g) {
+        if (A.resident) bs = g, bph = 0;  // loaded once: phase 0 stays complete
         if (!(A.debug & 2048)) {  // 2048: timing experiment, MMAs without operand waits
           twait_s1(a_full(as), aph, w1, pon_w);
           twait_s1(b_full(bs), bph, w2, pon_w);
         }
         tc_fence_after();
         const uint64_t bd = sw128_desc(bring + bs * A.b_slot);
-        if constexpr (TMEMA) {
+        if (A.resident && half >= 0) {
+          // half unit on the resident full image: one N = BN / 2 MMA per tap
+          // (rows kx * BN + half * BN / 2 of each split plane) into columns kx * BN / 2
+          const uint32_t hb = static_cast<uint32_t>(p.BN / 2);
+          const uint32_t lo16 = (3u * A.b_plane) >> 4;
+#pragma unroll
+          for (int kx = 0; kx < 3; ++kx) {
+            const uint64_t bk = bd + ((static_cast<uint32_t>(kx * p.BN + half * (p.BN / 2)) * 128u) >> 4);
+            const uint32_t dk = d_tmem + static_cast<uint32_t>(kx) * hb;
+            const uint32_t idk = make_idesc(p.BN / 2);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              if constexpr (TMEMA) {
+                const uint32_t ta = tmem_base + kTmemA + static_cast<uint32_t>(as) * 64u;
+                tc_mma_ts_w(dk, ta + 8 * k, bk + 2 * k, idk, (g > 0 || k > 0) ? 1u : 0u);
+                if (SPLIT3) {
+                  tc_mma_ts_w(dk, ta + 8 * k, bk + lo16 + 2 * k, idk, 1u);
+                  tc_mma_ts_w(dk, ta + 32 + 8 * k, bk + 2 * k, idk, 1u);
+                }
+              } else {
+                const uint64_t ad = sw128_desc(aring + as * A.a_slot);
+                tc_mma_w(dk, ad + 2 * k, bk + 2 * k, idk, (g > 0 || k > 0) ? 1u : 0u);
+                if (SPLIT3) {
+                  tc_mma_w(dk, ad + 2 * k, bk + lo16 + 2 * k, idk, 1u);
+                  tc_mma_w(dk, ad + (kAPlane >> 4) + 2 * k, bk + 2 * k, idk, 1u);
+                }
+              }
+            }
+          }
+        } else if constexpr (TMEMA) {
           const uint32_t ta = tmem_base + kTmemA + static_cast<uint32_t>(as) * 64u;
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
@@ -352,8 +396,10 @@ conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
             }
           }
         }
-        tc_commit_w(b_empty(bs));
-        if (++bs == A.nb) { bs = 0; bph ^= 1; }
+        if (!A.resident) {
+          tc_commit_w(b_empty(bs));
+          if (++bs == A.nb) { bs = 0; bph ^= 1; }
+        }
         tc_commit_w(a_empty(as));
         if (++as == A.na) { as = 0; aph ^= 1; }
       }
@@ -516,18 +562,26 @@ merit_status launch_conv_s1(const merit_plan& plan, const void* a, const void* p
   auto used_bytes = [&]() {
     return A.na * (size_t)A.a_slot + A.nb * (size_t)A.b_slot + A.nr * (size_t)A.raw_bytes;
   };
+  // Weights resident when every (ky, channel block) group fits a B slot next
+  // to a 4-deep raw ring (C3: 3 x 48 KB): loaded once per CTA instead of
+  // once per tile (C3: 144 KB x 896 tiles = 129 MB of L2 -> SM traffic)
+  const char* rese = getenv("MERIT_S1_RESIDENT");
+  A.resident = !(rese && rese[0] == '0') && A.n_groups <= kMaxRing &&
+               A.n_groups * (size_t)A.b_slot + 4 * (size_t)A.raw_bytes + 2 * (size_t)A.a_slot <= budget;
+  if (A.resident) A.nb = A.n_groups;
   for (;;) {  // grow: raw (even), A, B
     const size_t used = used_bytes();
     if (A.nr < 4 && used + 2 * A.raw_bytes <= budget) { A.nr += 2; continue; }
     if (!tmema && A.na < 3 && used + A.a_slot <= budget) { ++A.na; continue; }
-    if (A.nb < 3 && used + A.b_slot <= budget) { ++A.nb; continue; }
+    if (!A.resident && A.nb < 3 && used + A.b_slot <= budget) { ++A.nb; continue; }
+    if (A.resident && A.nr < kMaxRing && used + 2 * A.raw_bytes <= budget) { A.nr += 2; continue; }
     break;
   }
   if (const char* re = getenv("MERIT_S1_RINGS")) {  // "na,nb,nr" (tuning)
     int na, nb, nr;
     if (sscanf(re, "%d,%d,%d", &na, &nb, &nr) == 3 && na >= 1 && nb >= 1 && nr >= 2 && nr % 2 == 0 &&
         na <= kMaxRing && nb <= kMaxRing && nr <= kMaxRing) {
-      A.na = tmema ? 2 : na; A.nb = nb; A.nr = nr;
+      A.na = tmema ? 2 : na; A.nb = A.resident ? A.n_groups : nb; A.nr = nr;
     }
   }
   if (used_bytes() > budget) return fail(MERIT_E_UNSUPPORTED_VIEW, "stride-1 conv rings exceed shared memory");

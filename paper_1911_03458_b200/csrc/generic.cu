@@ -25,6 +25,7 @@ struct GenArgs {
   const void* b;
   void* out;
   int32_t* err;
+  const int32_t* run_if;  // non-null: run only if *run_if != 0 (fallback of a narrowed SAD plan)
 };
 
 __device__ __forceinline__ void raise_err(int32_t* err, int code) { atomicCAS(err, 0, code); }
@@ -115,6 +116,7 @@ __global__ void generic_kernel(GenArgs A) {
   pdl_launch_dependents();
   pdl_wait();
   if (row >= g.rows) return;
+  if (A.run_if && *A.run_if == 0) return;
   long long k[kMaxK];
   // p index of this row (row-major, tensor.hpp:59-65)
   long long r = row;
@@ -270,8 +272,9 @@ __global__ void generic_kernel(GenArgs A) {
 }  // namespace
 
 merit_status launch_generic(const merit_plan& plan, const void* a, const void* b, void* out,
-                            void* stream) {
+                            void* stream, const int32_t* run_if) {
   GenArgs args;
+  args.run_if = run_if;
   args.g = plan.gen;
   args.prog = static_cast<const ProgramImage*>(plan.d_prog);
   args.a = a;

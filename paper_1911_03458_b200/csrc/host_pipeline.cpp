@@ -127,7 +127,7 @@ void build_slices(const merit_plan& plan) {
       s.out_hi = u1 * ou;
       v.push_back(s);
     }
-  } else if (plan.kernel == MERIT_KERNEL_SAD) {
+  } else if (plan.kernel == MERIT_KERNEL_SAD && !plan.sad.narrow) {  // narrowed plans run unsliced
     const SadParams& q = plan.sad;
     const int64_t cur_bytes = q.ref_is_b ? in.src_a_bytes : in.src_b_bytes;
     const int64_t ref_bytes = q.ref_is_b ? in.src_b_bytes : in.src_a_bytes;

@@ -305,7 +305,12 @@ bool match_sad_views(const merit_view_spec& vc, const ViewAffine& fc,
 bool lower_sad(const merit_workload_desc& d, const ViewAffine& fa, const ViewAffine& fb,
                int32_t post, SadParams& sp) {
   if (post != POST_ADD_ZERO) return false;
-  if (d.dtype_a != MERIT_U8 || d.dtype_b != MERIT_U8) return false;
+  // 8-bit frames, or REAL32 frames (what the reference's Tensor holds,
+  // tensor.hpp:67) narrowed on the device with an exact fallback; argmin
+  // records need the 8-bit path (the fallback interpreter writes maps only)
+  const bool narrow = d.dtype_a == MERIT_F32 && d.dtype_b == MERIT_F32 && d.dtype_out == MERIT_F32 &&
+                      !(d.flags & (MERIT_FLAG_ARGMIN | MERIT_FLAG_NO_MAP));
+  if (!narrow && (d.dtype_a != MERIT_U8 || d.dtype_b != MERIT_U8)) return false;
   if (d.dtype_out != MERIT_I32 && d.dtype_out != MERIT_F32) return false;
   if (!same_shape(d.view_a.p_shape, d.view_a.p_rank, d.view_b.p_shape, d.view_b.p_rank))
     return false;
@@ -319,6 +324,7 @@ bool lower_sad(const merit_workload_desc& d, const ViewAffine& fa, const ViewAff
   sp.argmin = (d.flags & MERIT_FLAG_ARGMIN) ? 1 : 0;
   sp.write_map = (sp.argmin && (d.flags & MERIT_FLAG_NO_MAP)) ? 0 : 1;
   sp.out_f32 = d.dtype_out == MERIT_F32;
+  sp.narrow = narrow ? 1 : 0;
   return true;
 }
 
@@ -689,8 +695,9 @@ merit_status lower(const merit_workload_desc& d, merit_plan& plan) {
   if (plan.kernel != MERIT_KERNEL_SAD && (d.flags & (MERIT_FLAG_ARGMIN | MERIT_FLAG_NO_MAP)))
     return fail(MERIT_E_UNSUPPORTED_PROGRAM,
                 "argmin is only available for L1 block-matching workloads on the SAD kernel");
-  if (plan.kernel == MERIT_KERNEL_GENERIC) {
-    // Exact interpreter.  Any storage dtype widens to the mode's value type.
+  if (plan.kernel == MERIT_KERNEL_GENERIC || (plan.kernel == MERIT_KERNEL_SAD && plan.sad.narrow)) {
+    // Exact interpreter (also the fallback of a narrowed SAD plan).  Any
+    // storage dtype widens to the mode's value type.
     if (!fix16 && d.dtype_out != MERIT_F32)
       return fail(MERIT_E_UNSUPPORTED_PROGRAM, "REAL32 generic execution writes f32 outputs");
     GenericParams& g = plan.gen;
@@ -708,17 +715,24 @@ merit_status lower(const merit_workload_desc& d, merit_plan& plan) {
     g.uses_b = 1;
     g.va = fa;
     g.vb = fb;
-    info.algorithmic_ops = (double)info.n_outputs * avol;
-    info.algorithmic_bytes = (double)info.src_a_bytes + (double)info.src_b_bytes +
-                             (double)info.out_elems * elem_size(d.dtype_out);
-    std::snprintf(info.description, sizeof(info.description),
-                  "generic %s rows=%lld a_vol=%lld outputs=%d", fix16 ? "fix16" : "real32",
-                  (long long)g.rows, (long long)avol, pg.outputs);
+    if (plan.kernel == MERIT_KERNEL_GENERIC) {
+      info.algorithmic_ops = (double)info.n_outputs * avol;
+      info.algorithmic_bytes = (double)info.src_a_bytes + (double)info.src_b_bytes +
+                               (double)info.out_elems * elem_size(d.dtype_out);
+      std::snprintf(info.description, sizeof(info.description),
+                    "generic %s rows=%lld a_vol=%lld outputs=%d", fix16 ? "fix16" : "real32",
+                    (long long)g.rows, (long long)avol, pg.outputs);
+    } else {
+      const size_t n = std::strlen(info.description);
+      std::snprintf(info.description + n, sizeof(info.description) - n,
+                    " (f32 frames narrowed to u8 on device, exact fallback)");
+    }
     (void)program_uses_port;
   }
   info.kernel = plan.kernel;
   info.out_bytes = info.out_elems * elem_size(d.dtype_out);
   info.executed_ops = info.algorithmic_ops;
+  if (plan.kernel == MERIT_KERNEL_SAD && plan.sad.narrow) info.launches_per_run = 3;
   if (plan.kernel == MERIT_KERNEL_CONV_TC) info.launches_per_run = 1;
   return MERIT_OK;
 }

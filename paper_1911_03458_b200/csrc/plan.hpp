@@ -100,6 +100,9 @@ struct SadParams {
   int32_t fuse2 = 0;
   int32_t BY2 = 0, BX2 = 0;
   int64_t aux2_delta = 0;
+  // REAL32 frames (the reference Tensor's only float type): narrowed to u8 on
+  // the device before matching, exact-interpreter fallback (launch_sad_narrowed)
+  int32_t narrow = 0;
 };
 
 // K3: implicit-GEMM convolution on tcgen05 (mac_program over conv views).
@@ -175,6 +178,7 @@ struct merit_plan {
   mutable void* d_prog = nullptr;      // ProgramImage copy for K0
   mutable void* d_err = nullptr;       // int32 device error flag
   mutable void* d_packed_b = nullptr;  // K3 packed weights
+  mutable void* d_narrow = nullptr;    // narrowed SAD plans: u8 copies of both frames
   mutable bool packed_valid = false;  // set by merit_dev_plan_pack_b only
   mutable int device = -1;
   // Concurrent runs of one plan (several threads / streams): a run that packs
@@ -230,7 +234,13 @@ void release_host_pipeline(const merit_plan& plan);
 
 // Kernel launchers (defined in the .cu files).  All asynchronous on `stream`.
 merit_status launch_generic(const merit_plan& plan, const void* a, const void* b, void* out,
-                            void* stream);
+                            void* stream, const int32_t* run_if = nullptr);
+// REAL32 block matching on the SAD kernel (SadParams::narrow): narrow both
+// frames to 8 bits on the device, match, and re-run the exact interpreter
+// (stream-ordered, device-side condition) if any pixel is not an integer in
+// [0, 255].  Results are the engine's bit for bit either way.
+merit_status launch_sad_narrowed(const merit_plan& plan, const void* a, const void* b, void* out,
+                                 void* stream);
 merit_status launch_maxpool(const merit_plan& plan, const void* a, void* out, void* stream);
 // Rows per thread of the SAD kernel variant for a window, 0 if none fits.
 int sad_rows_per_thread(int BH, int WY, int WX);

@@ -26,6 +26,7 @@
 //  * Argmin: per-thread min over its D rows, then a shared-memory atomicMin
 //    on the packed key (sad << 16 | dy*WX + dx): lowest SAD, then lowest
 //    raster index — the tie-break BASELINE.json asks for.
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 
@@ -1267,6 +1268,51 @@ int sad_rows_per_thread(int BH, int WY, int WX) {
   }
   if (want == 11 || want == 22 || want == 33) return want;
   return WY <= 33 ? 11 : (WY <= 66 ? 33 : 22);  // measured on C5 (+/-32): 33 beats 22 by 3%
+}
+
+namespace {
+// f32 -> u8 for both frames of a narrowed plan; *bad |= 1 if any value is
+// not an integer in [0, 255] (NaN fails the comparisons).
+__global__ void narrow_u8_kernel(const float* __restrict__ a, uint8_t* __restrict__ ua, long long na,
+                                 const float* __restrict__ b, uint8_t* __restrict__ ub, long long nb,
+                                 int32_t* __restrict__ bad) {
+  pdl_launch_dependents();
+  pdl_wait();
+  bool ok = true;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; i < na + nb; i += stride) {
+    const float v = i < na ? a[i] : b[i - na];
+    const bool good = v >= 0.f && v <= 255.f && v == rintf(v);
+    ok = ok && good;
+    const uint8_t u = good ? static_cast<uint8_t>(v) : 0;
+    if (i < na) ua[i] = u; else ub[i - na] = u;
+  }
+  if (__any_sync(0xffffffffu, !ok) && (threadIdx.x & 31) == 0) atomicOr(bad, 1);
+}
+}  // namespace
+
+merit_status launch_sad_narrowed(const merit_plan& plan, const void* a, const void* b, void* out, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const long long na = plan.info.src_a_bytes / 4, nb = plan.info.src_b_bytes / 4;
+  uint8_t* ua = static_cast<uint8_t*>(plan.d_narrow);
+  uint8_t* ub = ua + ((na + 127) / 128) * 128;
+  int32_t* bad = reinterpret_cast<int32_t*>(ub + ((nb + 127) / 128) * 128);
+  merit_status st = cuda_check(cudaMemsetAsync(bad, 0, 4, s), "cudaMemsetAsync(narrow flag)");
+  if (st != MERIT_OK) return st;
+  long long blocks = (na + nb + 255) / 256;
+  if (blocks > 8LL * num_sms()) blocks = 8LL * num_sms();
+  cudaError_t e = launch_pdl(narrow_u8_kernel, dim3(static_cast<unsigned>(std::max(1LL, blocks))), dim3(256), 0, s,
+                             1, static_cast<const float*>(a), ua, na, static_cast<const float*>(b), ub, nb, bad);
+  if (e != cudaSuccess) return cuda_check(e, "launch(narrow)");
+  if ((st = launch_status("narrow_u8_kernel")) != MERIT_OK) return st;
+  SadParams p = plan.sad;
+  merit_plan sub;  // the same plan on the u8 copies
+  sub.kernel = MERIT_KERNEL_SAD;
+  sub.sad = p;
+  sub.info = plan.info;
+  if ((st = launch_sad(sub, ua, ub, out, nullptr, stream)) != MERIT_OK) return st;
+  // exact interpreter on the f32 frames, only if a pixel did not narrow
+  return launch_generic(plan, a, b, out, stream, bad);
 }
 
 merit_status launch_sad(const merit_plan& plan, const void* a, const void* b, void* out, void* aux,

@@ -61,6 +61,23 @@ int main() {
   check("gemm", {{"m", 5}, {"n", 6}, {"k", 7}, {"fix", 1}, {"frac", 6}}, 16);
   check("correlation", {{"c", 3}, {"h", 8}, {"w", 7}, {"d", 3}}, 17);
   check("motion_estimation", {{"h", 16}, {"w", 24}, {"blk", 4}, {"win", 5}}, 18);
+  // REAL32 frames holding 8-bit pixels (the reference Tensor's only float
+  // type): the header swap reaches the byte-SIMD SAD kernel (K2)
+  {
+    for (const auto& [blk, win] : {std::pair<int, int>{16, 33}, {8, 65}}) {
+      Workload w = build_template("motion_estimation", {{"h", 64}, {"w", 96}, {"blk", double(blk)}, {"win", double(win)}});
+      SplitMix64 r{77u + uint64_t(blk)};
+      for (float& v : w.src_a.fdata) v = float(r.range(0, 255));
+      for (size_t i = 0; i < w.src_b.fdata.size(); ++i) w.src_b.fdata[i] = float(r.range(0, 255));
+      const Tensor want = run_full(w);
+      const int kern = device::lowered_kernel(w);
+      const Tensor got = device::run_full(w);
+      const bool ok = kern == MERIT_KERNEL_SAD && got.shape == want.shape &&
+                      std::memcmp(got.fdata.data(), want.fdata.data(), got.fdata.size() * 4) == 0;
+      std::printf("%s motion_estimation-u8-valued blk=%d kernel=%d\n", ok ? "PASS" : "FAIL", blk, kern);
+      if (!ok) ++failures;
+    }
+  }
   check("motion_estimation", {{"h", 8}, {"w", 8}, {"blk", 4}, {"win", 3}, {"fix", 1}}, 19);
   check("bilateral", {{"h", 9}, {"w", 8}, {"k", 5}}, 20);
   check("maxpool", {{"h", 9}, {"w", 11}, {"k", 3}, {"stride", 2}}, 21);

@@ -464,3 +464,29 @@ def test_device_buffer_checks(cuda):
         plan.run(a[:10], None, out)                      # too small
     with pytest.raises(Error):
         plan.run(a.cpu(), None, out)                     # host tensor
+
+
+# ------------------------------------------- REAL32 frames on the SAD kernel --
+@pytest.mark.parametrize("integer", [True, False])
+@pytest.mark.parametrize("blk,r", [(16, 16), (8, 32), (16, 3)])
+def test_sad_real32_frames_narrowed_bit_exact(cuda, integer, blk, r):
+    # the reference's Tensor is REAL32 / FIX16 only (tensor.hpp:67), so a
+    # reference caller's motion-estimation frames arrive as floats: they are
+    # narrowed to 8 bits on the device and matched by K2; a frame holding any
+    # non-integer (or out-of-range) value re-runs on the exact interpreter.
+    # Either way the result is the engine's, bit for bit.
+    cur, ref = W.gen_me_pair(48, 96, 51, blk, 8, 4)
+    w = W.me_view(48, 96, blk, r)
+    w.src_a = cur.astype(np.float32)
+    w.src_b = ref.astype(np.float32)
+    if not integer:
+        w.src_b[5, 7] = 12.5
+    w.dtype_a = w.dtype_b = w.dtype_out = W.Dtype.Real32
+    plan = Plan(w)
+    assert plan.kernel == Kernel.SAD and "narrowed" in plan.description
+    got = run_full(w)
+    want = O.run_full(w)
+    assert got.dtype == np.float32
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+    if integer:
+        assert np.array_equal(got, O.me_sad(cur, ref, blk, r).astype(np.float32))
