@@ -87,6 +87,7 @@ struct SadLaunch {
   int dbg;                    // timing experiments (MERIT_SAD_DBG): 1 skip the copy builder, 2 skip the epilogue
   uint32_t key_mul;           // 65536 as a launch parameter: argmin keys acc * key_mul + d * WX
                               // stay IMADs (FMA pipe) instead of folding into ALU shift-adds
+  uint32_t one;               // 1 as a launch parameter: sums written as IMADs (FMA pipe)
 };
 
 // n / d for n < 2^31 by multiply-high (Granlund-Montgomery): s = ceil(log2 d),
@@ -742,14 +743,18 @@ __device__ __forceinline__ void sad_tile_work_fused(const SadLaunch& L, int32_t*
 #pragma unroll
   for (int n = 0; n < NBY; ++n) best[n] = 0xffffffffu;
   const int col = ib * BLK + dxl;
+  const uint32_t one = L.one;
 #pragma unroll 1
   for (int ig = 0; ig < G; ++ig) {
     const uint32_t* cp = copies + (col & 3) * L.CS + (col >> 2) + ig * D * L.Ww;
+    // the last group of the 65-row window has 32 rows (65 = 33 + 32)
+    const int nd = ig == 0 ? D : D - 1;
     uint32_t acc[NBY][D];
 #pragma unroll
     for (int n = 0; n < NBY; ++n)
 #pragma unroll
       for (int d = 0; d < D; ++d) acc[n][d] = 0;
+    uint32_t bn0 = 0xffffffffu, bn1 = 0xffffffffu, bn2 = 0xffffffffu;
 #pragma unroll
     for (int r = 0; r < D + NBY * BLK - 1; ++r) {
       uint32_t rwv[BWW];
@@ -766,20 +771,42 @@ __device__ __forceinline__ void sad_tile_work_fused(const SadLaunch& L, int32_t*
             for (int j = 0; j < BWW; ++j) acc[n][d] = vabsdiff4_acc(cw[n][i][j], rwv[j], acc[n][d]);
           }
         }
-    }
-    // the last group of the 65-row window has 32 rows (65 = 33 + 32)
-    const int nd = ig == 0 ? D : D - 1;
-    uint32_t bn0 = 0xffffffffu, bn1 = 0xffffffffu, bn2 = 0xffffffffu;
-#pragma unroll
-    for (int d = 0; d < D; ++d) {
-      if (d < nd) {
-        const uint32_t c = static_cast<uint32_t>(d * WX);
-        bn0 = min(bn0, acc[0][d] * kmul + c);
-        bn1 = min(bn1, acc[1][d] * kmul + c);
-        // 16x16: this half's top + bottom, plus the other half's (lane ^ 16)
-        const uint32_t sv = acc[0][d] + acc[1][d];
+      // displacement d is complete once its bottom block's last row
+      // (r = d + 2 BLK - 1) is in: fold its keys here, so the key IMADs,
+      // the shuffle and the mins interleave with the VABSDIFF4 stream and the
+      // two accumulators die early
+      // (two displacements per fold: 3-way mins)
+      const int d = r - (NBY * BLK - 1);
+      auto keys = [&](int dd, uint32_t& k0v, uint32_t& k1v, uint32_t& k2v) {
+        const uint32_t c = static_cast<uint32_t>(dd * WX);
+        k0v = acc[0][dd] * kmul + c;
+        k1v = acc[1][dd] * kmul + c;
+        // 16x16: this half's top + bottom (an IMAD: FMA pipe), plus the other half's (lane ^ 16)
+        const uint32_t sv = acc[0][dd] * one + acc[1][dd];
         const uint32_t so = __shfl_xor_sync(0xffffffffu, sv, 16);
-        bn2 = min(bn2, sv * kmul + (so * kmul + c));
+        k2v = sv * kmul + (so * kmul + c);
+      };
+      if (d >= 1 && d < D && (d & 1)) {
+        if (d < nd) {
+          uint32_t a0, a1, a2, b0, b1, b2;
+          keys(d - 1, a0, a1, a2);
+          keys(d, b0, b1, b2);
+          bn0 = __vimin3_u32(bn0, a0, b0);
+          bn1 = __vimin3_u32(bn1, a1, b1);
+          bn2 = __vimin3_u32(bn2, a2, b2);
+        } else if (d - 1 < nd) {
+          uint32_t a0, a1, a2;
+          keys(d - 1, a0, a1, a2);
+          bn0 = min(bn0, a0);
+          bn1 = min(bn1, a1);
+          bn2 = min(bn2, a2);
+        }
+      } else if (d == D - 1 && (d & 1) == 0 && d < nd) {  // odd D: the last one alone
+        uint32_t a0, a1, a2;
+        keys(d, a0, a1, a2);
+        bn0 = min(bn0, a0);
+        bn1 = min(bn1, a1);
+        bn2 = min(bn2, a2);
       }
     }
     const uint32_t k0 = static_cast<uint32_t>(ig * D * WX + dxl);
@@ -1232,6 +1259,7 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
   if (e != cudaSuccess) return cuda_check(e, "set_smem_attr(sad)");
   const int threads = (L.items + 31) / 32 * 32;
   L.key_mul = 65536u;
+  L.one = 1u;
   L.cp_sr = threads / L.Ww;
   L.cp_sw = threads - L.cp_sr * L.Ww;
   L.n_full_x = p.BX / L.TBX;
