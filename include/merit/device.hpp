@@ -167,6 +167,26 @@ inline std::pair<Tensor, TrafficReport> run_tiled(const Workload& w, const Tilin
   return {run_full(w, flags), rep};
 }
 
+/// The DRAM traffic a device run of the workload actually causes (the GPU's
+/// counters through CUPTI, L2 flushed first): the measured counterpart of
+/// run_tiled's TrafficReport (engine.hpp:72-80).  Allocates device copies of
+/// the sources and the output, runs once, returns merit_measured_traffic.
+inline merit_measured_traffic measure_traffic(const Workload& w, uint32_t flags = 0) {
+  w.validate();
+  detail::Desc D;
+  detail::fill(D, w, flags);
+  detail::PlanGuard g;
+  merit_status st = merit_dev_plan_create(&D.d, &g.p);
+  if (st != MERIT_OK) detail::raise(st);
+  const bool fa = w.src_a.dtype == Dtype::Fix16, fb = w.src_b.dtype == Dtype::Fix16;
+  const void* ha = fa ? static_cast<const void*>(w.src_a.qdata.data()) : static_cast<const void*>(w.src_a.fdata.data());
+  const void* hb = fb ? static_cast<const void*>(w.src_b.qdata.data()) : static_cast<const void*>(w.src_b.fdata.data());
+  merit_measured_traffic r{};
+  st = merit_dev_measure_traffic_host(g.p, ha, hb, &r);
+  if (st != MERIT_OK) detail::raise(st);
+  return r;
+}
+
 /// Which device kernel a workload lowers to (MERIT_KERNEL_*), without running it.
 inline int lowered_kernel(const Workload& w, uint32_t flags = 0) {
   detail::Desc D;

@@ -316,6 +316,35 @@ typedef struct merit_traffic_report {
 merit_status merit_dev_tiled_traffic(const merit_plan* plan, const int64_t* t_p, const int64_t* t_a,
                                      merit_traffic_report* report);
 
+/* The measured counterpart of the TrafficReport: run the plan on device
+ * buffers with the GPU's performance counters armed (CUPTI range profiler,
+ * one user range around the run, user replay: the run repeats once per
+ * counter pass) after a read-only L2 flush, and report the DRAM bytes the
+ * run actually moved (all of its launches).  Where the reference counts the
+ * words its scratchpad loads pass by pass (engine.hpp:233-241), this is what
+ * HBM served.  Output lines still dirty in L2 when the run ends are not
+ * written yet, and evictions of unrelated lines may add a few MB of writes.
+ * range_time_ns is the GPU time spanned by the range (launch gaps included,
+ * not a kernel time).  Synchronous; fails with MERIT_E_UNSUPPORTED_PROGRAM
+ * when CUPTI (libcupti.so, the copy already in the process if any, else
+ * loaded at the first call) or profiling permission is missing. */
+typedef struct merit_measured_traffic {
+  double dram_read_bytes;
+  double dram_write_bytes;
+  double range_time_ns;
+  int64_t ranges;     /* profiled ranges (1) */
+  int64_t launches;   /* kernel launches the library issued per run */
+  int32_t passes;     /* replay passes (runs) the metrics needed */
+  int32_t _pad;
+} merit_measured_traffic;
+merit_status merit_dev_measure_traffic(const merit_plan* plan, const void* d_src_a, const void* d_src_b,
+                                       void* d_out, void* d_aux, void* cuda_stream,
+                                       merit_measured_traffic* report);
+/* The same from host sources (copied to device buffers the call allocates
+ * and frees; outputs are discarded). */
+merit_status merit_dev_measure_traffic_host(const merit_plan* plan, const void* h_src_a, const void* h_src_b,
+                                            merit_measured_traffic* report);
+
 /* Deterministic input synthesis shared by tests and the benchmark
  * (workloads.hpp:74-105 SplitMix64 / fill_random, and the seeded frame
  * generator of SURVEY §8(d)).  Host-only. */

@@ -80,6 +80,11 @@ class HostSliceC(C.Structure):  # merit_host_slice (pipelined merit_dev_run_host
                 ("aux_lo", C.c_int64), ("aux_hi", C.c_int64), ("aux2_lo", C.c_int64), ("aux2_hi", C.c_int64)]
 
 
+class MeasuredTrafficC(C.Structure):  # merit_measured_traffic
+    _fields_ = [("dram_read_bytes", C.c_double), ("dram_write_bytes", C.c_double), ("range_time_ns", C.c_double),
+                ("ranges", C.c_int64), ("launches", C.c_int64), ("passes", C.c_int32), ("_pad", C.c_int32)]
+
+
 # Exported symbols and their prototypes (kept in sync with include/merit_dev.h;
 # tests/test_capi_symbols.py checks every declared symbol is exported).
 PROTOTYPES = {
@@ -107,6 +112,9 @@ PROTOTYPES = {
     "merit_dev_last_kernel": (C.c_char_p, []),
     "merit_dev_tiled_traffic": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(TrafficReportC)]),
     "merit_dev_plan_slices": (C.c_int, [C.c_void_p, C.POINTER(HostSliceC), C.c_int64, C.POINTER(C.c_int64)]),
+    "merit_dev_measure_traffic": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                            C.POINTER(MeasuredTrafficC)]),
+    "merit_dev_measure_traffic_host": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(MeasuredTrafficC)]),
 }
 
 _lib = None

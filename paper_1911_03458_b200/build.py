@@ -77,7 +77,7 @@ def build(verbose: bool = False, force: bool = False, debug: bool = False) -> Pa
     with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 1))) as ex:
         list(ex.map(compile_one, cmds))
     if force or _stale(lib, objs):
-        cmd = [cc, *ARCH, "-shared", "-cudart", "static", "-o", str(lib), *map(str, objs), "-lcuda"]
+        cmd = [cc, *ARCH, "-shared", "-cudart", "static", "-o", str(lib), *map(str, objs), "-lcuda", "-ldl"]
         if verbose:
             print(" ".join(cmd), flush=True)
         subprocess.run(cmd, check=True)

@@ -564,9 +564,11 @@ merit_status launch_conv_s1(const merit_plan& plan, const void* a, const void* p
   };
   // Weights resident when every (ky, channel block) group fits a B slot next
   // to a 4-deep raw ring (C3: 3 x 48 KB): loaded once per CTA instead of
-  // once per tile (C3: 144 KB x 896 tiles = 129 MB of L2 -> SM traffic)
+  // once per tile (C3: 144 KB x 896 tiles = 129 MB of L2 -> SM traffic);
+  // measured at C3: 25.2-25.5 us resident vs 24.2 us streamed (the B slots
+  // are not the bottleneck), so opt-in (MERIT_S1_RESIDENT=1)
   const char* rese = getenv("MERIT_S1_RESIDENT");
-  A.resident = !(rese && rese[0] == '0') && A.n_groups <= kMaxRing &&
+  A.resident = (rese && rese[0] == '1') && A.n_groups <= kMaxRing &&
                A.n_groups * (size_t)A.b_slot + 4 * (size_t)A.raw_bytes + 2 * (size_t)A.a_slot <= budget;
   if (A.resident) A.nb = A.n_groups;
   for (;;) {  // grow: raw (even), A, B

@@ -417,6 +417,17 @@ class Plan:
                                                 ta.ctypes.data_as(C.c_void_p), C.byref(r)))
         return {k: int(getattr(r, k)) for k, _ in r._fields_}
 
+    def measure_traffic(self, d_src_a, d_src_b, d_out=None, d_aux=None, stream=None) -> dict:
+        """merit_dev_measure_traffic: one run on device buffers with the GPU's
+        DRAM counters armed (CUPTI), after an L2 flush: the bytes HBM served
+        and the kernel time, summed over the plan's launches."""
+        r = _capi.MeasuredTrafficC()
+        _check(self.lib.merit_dev_measure_traffic(self.handle, self._ptr(d_src_a), self._ptr(d_src_b),
+                                                  self._ptr(d_out), self._ptr(d_aux), C.c_void_p(stream or 0),
+                                                  C.byref(r)))
+        return {k: (float(getattr(r, k)) if k.startswith(("dram", "range_time")) else int(getattr(r, k)))
+                for k, _ in r._fields_ if k != "_pad"}
+
     # -- host buffers: the reference's run_full convention --------------------
     @staticmethod
     def _check_host(x, dtype, need: int, what: str):
@@ -536,17 +547,28 @@ def run_full(w: Workload, flags: int = 0):
 
 
 def run_tiled(w: Workload, t_p, t_a, flags: int = 0, scratch_words_a: int = 8192,
-              scratch_words_b: int = 4096):
+              scratch_words_b: int = 4096, measure: bool = False):
     """engine.hpp:289-295 on the device: the output of run_full (the device
     executes its own footprint-staged tiling) and the TilingPlan's
     TrafficReport as a dict.  EngineConfig's capacities (engine.hpp:82-87)
     keep their diagnostic meaning: a footprint box larger than
-    scratch_words_a / _b raises ScratchpadOverflow (engine.hpp:154-155)."""
+    scratch_words_a / _b raises ScratchpadOverflow (engine.hpp:154-155).
+    measure=True adds ``rep["measured"]``: the DRAM bytes the device run
+    actually moved, from the GPU's counters (Plan.measure_traffic)."""
     _check_sources(w)
     plan = Plan(w, flags)
     rep = plan.tiled_traffic(t_p, t_a)
     if rep["scratchpad_peak_words_a"] > scratch_words_a or rep["scratchpad_peak_words_b"] > scratch_words_b:
         raise Error(ErrorCode.ScratchpadOverflow, "tile exceeds scratchpad")
+    if measure:
+        import torch
+        a = torch.from_numpy(np.ascontiguousarray(_host(w.src_a))).cuda()
+        b = torch.from_numpy(np.ascontiguousarray(_host(w.src_b))).cuda()
+        o = torch.empty(max(1, int(plan.info.out_bytes)), dtype=torch.uint8, device="cuda")
+        x = torch.empty(max(1, int(plan.info.aux_elems)), dtype=torch.int32, device="cuda")
+        rep["measured"] = plan.measure_traffic(a, b, o, x if plan.info.aux_elems else None)
+        out = o[:int(plan.info.out_bytes)].cpu().numpy().view(_NP_OF[plan.dtypes[2]]).reshape(plan.out_shape)
+        return out, rep
     out, _ = plan.run_host(_host(w.src_a), _host(w.src_b))
     return out, rep
 

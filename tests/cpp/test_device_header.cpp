@@ -119,6 +119,20 @@ int main() {
                 ok ? "PASS" : "FAIL", (unsigned long long)grep.scratchpad_peak_words_a,
                 (unsigned long long)grep.passes, worst);
     if (!ok) ++failures;
+    // measured counterpart (GPU counters): the device reads the image once,
+    // the reference's plan charges every tile its 20 x 12 footprint box
+    // (on a 516 x 516 image: below ~1 MB the counters' fixed noise dominates)
+    Workload big = build_template("conv2d", {{"h", 516}, {"w", 516}, {"k", 5}, {"pad", 0}});
+    fill_random(big.src_a, 3);
+    fill_random(big.src_b, 4);
+    auto [bout, brep] = run_tiled(big, plan, cfg);
+    (void)bout;
+    const merit_measured_traffic m = device::measure_traffic(big);
+    const double words = m.dram_read_bytes / 4.0;
+    const bool okm = m.ranges == 1 && words < double(brep.dram_read_words_a) && words >= 0.85 * double(big.src_a.size());
+    std::printf("%s measured DRAM read words %.0f vs reference tiled count %llu (image %zu words)\n", okm ? "PASS" : "FAIL",
+                words, (unsigned long long)brep.dram_read_words_a, big.src_a.size());
+    if (!okm) ++failures;
     // an invalid plan fails with the reference's error code
     TilingPlan bad{{16, 8}, {5, 4}};
     bool rt = false, dt = false;
