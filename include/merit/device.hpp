@@ -111,6 +111,14 @@ struct PlanGuard {
 }  // namespace detail
 
 /// engine.hpp:282-287 on the device: validate, lower, run, copy back.
+///
+/// Numerics: max-pool, L1 / SAD, correlation, FIX16 and every program on the
+/// exact interpreter are bit-identical to merit::run_full.  REAL32 MAC
+/// convolutions run on the tensor cores with a 3-term bf16 split and fp32
+/// accumulation: |got - ref| <= 1e-4 (1 + |ref|) against the double oracle —
+/// looser than the 1e-5 of the reference's own REAL32 acceptance tests
+/// (SPEC.md:61,570).  Pass flags = MERIT_FLAG_EXACT for the engine's own
+/// summation order and rounding (bit-identical, on the interpreter).
 inline Tensor run_full(const Workload& w, uint32_t flags = 0) {
   w.validate();  // the reference's own checks first (engine.hpp:30-38)
   detail::Desc D;
