@@ -744,7 +744,11 @@ __device__ __forceinline__ void sad_tile_work_fused(const SadLaunch& L, int32_t*
   for (int n = 0; n < NBY; ++n) best[n] = 0xffffffffu;
   const int col = ib * BLK + dxl;
   const uint32_t one = L.one;
+#ifdef MERIT_SAD_FUSED_UNROLL  // experiment: both dy groups unrolled (compile-time nd)
+#pragma unroll
+#else
 #pragma unroll 1
+#endif
   for (int ig = 0; ig < G; ++ig) {
     const uint32_t* cp = copies + (col & 3) * L.CS + (col >> 2) + ig * D * L.Ww;
     // the last group of the 65-row window has 32 rows (65 = 33 + 32)

@@ -12,7 +12,7 @@ tags.update(a.split("=") for a in sys.argv[3:])
 d = Path(__file__).resolve().parents[1] / "profiles" / rnd
 out = [f"# profiles/{rnd} — measurements (B200, sm_100a)", "",
        "Files: `bench_C*.json` = the `python bench.py --config C*` line (default settings);",
-       "`bench_reference_C2.json` = `bench.py --impl reference` (the reference engine on the host cores);",
+       "`bench_reference_C*.json` = `bench.py --impl reference --config C*` (the reference on the host cores);",
        "`<tag>_c*_full.json` = summary of one `ncu --set full --clock-control none` capture of the dominant kernel",
        "(`tools/refresh_profiles.sh`, summarised by `tools/ncu_summary.py`);",
        "`<tag>_c*_launches.json` = the `--metrics gpu__time_duration.sum` launch list of the same short bench command.",
@@ -29,8 +29,15 @@ for c in ["C1", "C2", "C3", "C4", "C5"]:
                f"{b['roofline']['frac']:.3f} ({b['roofline']['bound']}) | {f['duration_us']:.1f} | "
                f"{f['sm_clock_hz'] / 1e9:.2f} GHz | {f['tensor_pipe_active_pct']} | {f['alu_pipe_active_pct']} | "
                f"{f['issue_active_pct']} | {f['dram_bytes_per_launch']:.3e} | {st} |")
-r = json.loads((d / "bench_reference_C2.json").read_text().strip().splitlines()[-1])
-out += ["", f"Reference arm (C2): {r['value']:.3e} Goutputs/s on {r['cpu_baseline']['cores']} host cores "
-        f"({r['cpu_baseline']['kind']}; sample: {r['cpu_baseline']['sample']}).", ""]
+for rc in ["C5", "C2"]:
+    rp = d / f"bench_reference_{rc}.json"
+    if not rp.exists():
+        continue
+    r = json.loads(rp.read_text().strip().splitlines()[-1])
+    ol = r.get("cpu_baseline_oracle_loop", {})
+    out += ["", f"Reference arm ({rc}): {r['value']:.3e} Goutputs/s on {r['cpu_baseline']['cores']} host cores "
+            f"({r['cpu_baseline'].get('cpu', '')}; {r['cpu_baseline']['kind']}; sample: {r['cpu_baseline']['sample']})."
+            + (f"  The reference's oracle loop on the same cores: {ol['value']:.3e} Goutputs/s ({ol['sample']})." if ol else "")]
+out.append("")
 (d / "README.md").write_text("\n".join(out) + "\n")
 print("\n".join(out[-9:]))

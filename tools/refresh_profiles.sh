@@ -9,7 +9,7 @@ set -u
 TAG=$1; shift
 CONFIGS=${*:-C1 C2 C3 C4 C5}
 mkdir -p gpurun_out
-declare -A KERN=([C1]=maxpool [C2]=sad_ [C3]=conv_s1 [C4]=conv_tma [C5]=sad_)
+declare -A KERN=([C1]=maxpool [C2]=sad_ [C3]=conv_s1 [C4]=conv_tma [C5]=sad_async)
 for C in $CONFIGS; do
   c=$(echo "$C" | tr 'C' 'c')
   timeout 900 python bench.py --config "$C" > "gpurun_out/bench_${TAG}_${C}.json" 2> "gpurun_out/bench_${TAG}_${C}.err" || { echo "$C bench failed"; continue; }
@@ -21,6 +21,8 @@ for C in $CONFIGS; do
     -o "gpurun_out/prof_${TAG}_${c}" -f $SHORT > "gpurun_out/ncu_full_${TAG}_${c}.log" 2>&1
   echo "$C done"
 done
-if [[ " $CONFIGS " == *" C2 "* ]]; then
-  timeout 900 python bench.py --impl reference --config C2 > "gpurun_out/bench_${TAG}_ref_C2.json" 2>&1
-fi
+for C in $CONFIGS; do
+  if [[ "$C" == "C5" || "$C" == "C2" ]]; then
+    timeout 900 python bench.py --impl reference --config "$C" > "gpurun_out/bench_${TAG}_ref_${C}.json" 2>&1
+  fi
+done
