@@ -164,9 +164,10 @@ typedef struct merit_program {
 /* Element types of the buffers crossing the ABI.  F32 and I16 are the
  * reference's REAL32 / FIX16 (tensor.hpp:67); BF16 and U8 are device
  * storage types for the same values (bf16-rounded activations, 8-bit frames);
- * I32 is an exact integer SAD output. */
+ * I32 / U16 are exact integer SAD outputs. */
 typedef enum merit_dtype {
-  MERIT_F32 = 0, MERIT_I16 = 1, MERIT_BF16 = 2, MERIT_U8 = 3, MERIT_I32 = 4
+  MERIT_F32 = 0, MERIT_I16 = 1, MERIT_BF16 = 2, MERIT_U8 = 3, MERIT_I32 = 4,
+  MERIT_U16 = 5  /* exact SAD map of 8-bit 8x8 / 16x16 blocks (every SAD <= 65,280): half the bytes of I32 */
 } merit_dtype;
 
 /* Request flags. */

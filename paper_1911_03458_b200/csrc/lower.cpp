@@ -311,7 +311,7 @@ bool lower_sad(const merit_workload_desc& d, const ViewAffine& fa, const ViewAff
   const bool narrow = d.dtype_a == MERIT_F32 && d.dtype_b == MERIT_F32 && d.dtype_out == MERIT_F32 &&
                       !(d.flags & (MERIT_FLAG_ARGMIN | MERIT_FLAG_NO_MAP));
   if (!narrow && (d.dtype_a != MERIT_U8 || d.dtype_b != MERIT_U8)) return false;
-  if (d.dtype_out != MERIT_I32 && d.dtype_out != MERIT_F32) return false;
+  if (d.dtype_out != MERIT_I32 && d.dtype_out != MERIT_F32 && d.dtype_out != MERIT_U16) return false;
   if (!same_shape(d.view_a.p_shape, d.view_a.p_rank, d.view_b.p_shape, d.view_b.p_rank))
     return false;
   if (match_sad_views(d.view_a, fa, d.view_b, fb, sp)) {
@@ -324,6 +324,7 @@ bool lower_sad(const merit_workload_desc& d, const ViewAffine& fa, const ViewAff
   sp.argmin = (d.flags & MERIT_FLAG_ARGMIN) ? 1 : 0;
   sp.write_map = (sp.argmin && (d.flags & MERIT_FLAG_NO_MAP)) ? 0 : 1;
   sp.out_f32 = d.dtype_out == MERIT_F32;
+  sp.out_u16 = d.dtype_out == MERIT_U16;  // exact: 8-bit 8x8 / 16x16 SADs are <= 65,280
   sp.narrow = narrow ? 1 : 0;
   return true;
 }
@@ -524,6 +525,7 @@ int64_t elem_size(int dtype) {
     case MERIT_BF16: return 2;
     case MERIT_U8: return 1;
     case MERIT_I32: return 4;
+    case MERIT_U16: return 2;
     default: return 0;
   }
 }
@@ -654,7 +656,7 @@ merit_status lower(const merit_workload_desc& d, merit_plan& plan) {
     info.aux_elems = sp.argmin ? blocks * 3 : 0;
     info.algorithmic_ops = (double)info.n_outputs * avol;
     info.algorithmic_bytes = (double)info.src_a_bytes + (double)info.src_b_bytes +
-                             (double)info.out_elems * 4 + (double)info.aux_elems * 4;
+                             (double)info.out_elems * elem_size(d.dtype_out) + (double)info.aux_elems * 4;
     std::snprintf(info.description, sizeof(info.description),
                   "sad pairs=%lld frame=%dx%d blocks=%dx%d blk=%dx%d window=%dx%d off=%d,%d %s%s%s",
                   (long long)sp.pairs, sp.Hc, sp.Wc, sp.BY, sp.BX, sp.BH, sp.BW, sp.WY, sp.WX,

@@ -91,6 +91,7 @@ struct SadParams {
   int32_t write_map = 1;
   int32_t argmin = 0;
   int32_t out_f32 = 0;      // SAD map as float (REAL32) instead of int32
+  int32_t out_u16 = 0;      // SAD map as uint16 (exact for 8-bit 8x8 / 16x16 blocks)
   // Block-row band of one launch (pipelined host-buffer runs): block rows
   // [by_begin, by_begin + by_count) of every pair; by_count 0 = all BY rows.
   int32_t by_begin = 0, by_count = 0;

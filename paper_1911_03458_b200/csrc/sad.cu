@@ -256,16 +256,29 @@ __device__ __forceinline__ void issue_tile(const SadLaunch& L, const uint8_t* __
   }
 }
 
+// One SAD-map entry: int32, float (a REAL32 map) or uint16 (exact: every
+// 8-bit 8x8 / 16x16 SAD is <= 65,280), streaming store.
+__device__ __forceinline__ void sad_store1(void* out, const SadParams& p, long long i, uint32_t v) {
+  if (p.out_f32) __stcs(static_cast<float*>(out) + i, static_cast<float>(v));
+  else if (p.out_u16) __stcs(static_cast<unsigned short*>(out) + i, static_cast<unsigned short>(v));
+  else __stcs(static_cast<int32_t*>(out) + i, static_cast<int32_t>(v));
+}
+
 // SAD-map rows d < nd of one (block, dx) thread: out[obase + d * WX]
-// (int32, or float for a REAL32 map), streaming stores.
+// (int32, float for a REAL32 map, or uint16), streaming stores.
 template <int D>
 __device__ __forceinline__ void sad_store_map(void* out, int out_f32, long long obase, int WX, const uint32_t* acc,
-                                              int nd) {
+                                              int nd, int out_u16 = 0) {
   if (out_f32) {
     float* o = static_cast<float*>(out) + obase;
 #pragma unroll
     for (int d = 0; d < D; ++d)
       if (d < nd) __stcs(o + d * WX, static_cast<float>(acc[d]));
+  } else if (out_u16) {
+    unsigned short* o = static_cast<unsigned short*>(out) + obase;
+#pragma unroll
+    for (int d = 0; d < D; ++d)
+      if (d < nd) __stcs(o + d * WX, static_cast<unsigned short>(acc[d]));
   } else {
     int32_t* o = static_cast<int32_t*>(out) + obase;
 #pragma unroll
@@ -437,16 +450,16 @@ __device__ __forceinline__ void sad_tile_work(const SadLaunch& L, void* __restri
       if (nd == D) {
 #pragma unroll
         for (int d = 0; d < D; ++d) bn = min(bn, acc[n][d] * kmul + static_cast<uint32_t>(d * WX));
-        if (store) sad_store_map<D>(out, p.out_f32, obase, WX, acc[n], D);
+        if (store) sad_store_map<D>(out, p.out_f32, obase, WX, acc[n], D, p.out_u16);
       } else if (WXC != 0 && nd == D - 1) {
 #pragma unroll
         for (int d = 0; d < D - 1; ++d) bn = min(bn, acc[n][d] * kmul + static_cast<uint32_t>(d * WX));
-        if (store) sad_store_map<D>(out, p.out_f32, obase, WX, acc[n], D - 1);
+        if (store) sad_store_map<D>(out, p.out_f32, obase, WX, acc[n], D - 1, p.out_u16);
       } else {
 #pragma unroll
         for (int d = 0; d < D; ++d)
           if (d < nd) bn = min(bn, acc[n][d] * kmul + static_cast<uint32_t>(d * WX));
-        if (store) sad_store_map<D>(out, p.out_f32, obase, WX, acc[n], nd);
+        if (store) sad_store_map<D>(out, p.out_f32, obase, WX, acc[n], nd, p.out_u16);
       }
       best[n] = min(best[n], bn + key0);
     }
@@ -599,11 +612,11 @@ __device__ __forceinline__ void sad_tile_work_warp(const SadLaunch& L, void* __r
       if (nd == D) {
 #pragma unroll
         for (int d = 0; d < D; ++d) bn = min(bn, acc[n][d] * kmul + static_cast<uint32_t>(d * WX));
-        if (store) sad_store_map<D>(out, p.out_f32, obase, WX, acc[n], D);
+        if (store) sad_store_map<D>(out, p.out_f32, obase, WX, acc[n], D, p.out_u16);
       } else {
 #pragma unroll
         for (int d = 0; d < D - 1; ++d) bn = min(bn, acc[n][d] * kmul + static_cast<uint32_t>(d * WX));
-        if (store) sad_store_map<D>(out, p.out_f32, obase, WX, acc[n], D - 1);
+        if (store) sad_store_map<D>(out, p.out_f32, obase, WX, acc[n], D - 1, p.out_u16);
       }
       best[n] = min(best[n], bn + static_cast<uint32_t>(ig * D * WX + dxl));
     }
@@ -626,8 +639,7 @@ __device__ __forceinline__ void sad_tile_work_warp(const SadLaunch& L, void* __r
     best[n] = min(best[n], ax * kmul + static_cast<uint32_t>(dxl * WX + (WX - 1)));
     const long long bb = (blk_index + n * (long long)p.BX) * (long long)(WY * WX);
     if (p.write_map && by + n < L.by1) {
-      if (p.out_f32) __stcs(static_cast<float*>(out) + bb + dxl * WX + (WX - 1), static_cast<float>(ax));
-      else __stcs(static_cast<int32_t*>(out) + bb + dxl * WX + (WX - 1), static_cast<int32_t>(ax));
+      sad_store1(out, p, bb + dxl * WX + (WX - 1), ax);
     }
     if (wsub == WPB - 1) {
       // corner (dy = 32k, dx = 32k): BLK x BWW words over the 32 lanes
@@ -643,8 +655,7 @@ __device__ __forceinline__ void sad_tile_work_warp(const SadLaunch& L, void* __r
       const uint32_t axx = __reduce_add_sync(0xffffffffu, v);
       if (lane == 0) best[n] = min(best[n], axx * kmul + static_cast<uint32_t>((WY - 1) * WX + (WX - 1)));
       if (p.write_map && by + n < L.by1 && lane == 0) {
-        if (p.out_f32) __stcs(static_cast<float*>(out) + bb + (WY - 1) * WX + (WX - 1), static_cast<float>(axx));
-        else __stcs(static_cast<int32_t*>(out) + bb + (WY - 1) * WX + (WX - 1), static_cast<int32_t>(axx));
+        sad_store1(out, p, bb + (WY - 1) * WX + (WX - 1), axx);
       }
     }
   }

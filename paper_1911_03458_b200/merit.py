@@ -69,6 +69,7 @@ class Dtype(enum.IntEnum):  # merit_dtype (tensor.hpp:67 + device storage types)
     BF16 = 2
     U8 = 3
     I32 = 4
+    U16 = 5      # exact SAD map of 8-bit 8x8 / 16x16 blocks (half the bytes of I32)
 
 
 class Op(enum.IntEnum):  # rip.hpp:15-31
@@ -329,7 +330,7 @@ def _check(st: int):
 
 
 _NP_OF = {Dtype.Real32: np.float32, Dtype.Fix16: np.int16, Dtype.BF16: np.uint16,
-          Dtype.U8: np.uint8, Dtype.I32: np.int32}
+          Dtype.U8: np.uint8, Dtype.I32: np.int32, Dtype.U16: np.uint16}
 
 
 class Plan:

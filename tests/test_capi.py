@@ -264,3 +264,17 @@ def test_multi_plan_unfusable_runs_members():
     with pytest.raises(Error) as ei:
         PlanGroup([c, m])
     assert ei.value.code == ErrorCode.BadParams
+
+
+def test_u16_sad_map_lowering():
+    # an exact uint16 SAD map (8-bit 16x16 blocks: every SAD <= 65,280) halves
+    # the map's bytes; other kernels do not take it
+    w = W.me_view(64, 96, 16, 16)
+    w.dtype_out = W.Dtype.U16
+    plan = Plan(w, FLAG_ARGMIN)
+    assert plan.kernel == Kernel.SAD
+    assert plan.info.out_bytes == 2 * plan.info.out_elems
+    c = W.conv_nchw_view(1, 8, 10, 10, 4)
+    c.dtype_out = W.Dtype.U16
+    with pytest.raises(Error):
+        Plan(c)

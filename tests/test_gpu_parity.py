@@ -490,3 +490,15 @@ def test_sad_real32_frames_narrowed_bit_exact(cuda, integer, blk, r):
     assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
     if integer:
         assert np.array_equal(got, O.me_sad(cur, ref, blk, r).astype(np.float32))
+
+
+@pytest.mark.parametrize("h,wd,blk,r", [(1080, 1920, 16, 16), (72, 80, 8, 32), (64, 96, 16, 32)])
+def test_sad_u16_map_bit_exact(cuda, h, wd, blk, r):
+    cur, ref = W.gen_me_pair(h, wd, 61, blk, min(r, 16), 4)
+    w = W.me_view(h, wd, blk, r)
+    w.src_a, w.src_b = cur, ref
+    w.dtype_out = W.Dtype.U16
+    sad, mv = run_full_argmin(w)
+    want = O.me_sad(cur, ref, blk, r)
+    assert sad.dtype == np.uint16 and np.array_equal(sad.astype(np.int32), want)
+    assert np.array_equal(mv, O.me_argmin(want, r))
