@@ -278,3 +278,13 @@ def test_u16_sad_map_lowering():
     c.dtype_out = W.Dtype.U16
     with pytest.raises(Error):
         Plan(c)
+
+
+def test_plan_member_of_single_plan_is_itself():
+    w = W.maxpool_nchw_view(1, 2, 8, 8)
+    plan = Plan(w)
+    info = _capi.PlanInfoC()
+    oo, ao = C.c_int64(-1), C.c_int64(-1)
+    assert plan.lib.merit_dev_plan_member(plan.handle, 0, C.byref(info), C.byref(oo), C.byref(ao)) == 0
+    assert info.n_outputs == plan.info.n_outputs and oo.value == 0 and ao.value == 0
+    assert plan.lib.merit_dev_plan_member(plan.handle, 1, C.byref(info), None, None) != 0

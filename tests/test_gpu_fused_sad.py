@@ -107,3 +107,63 @@ def test_fused_c5_all_64_pairs_as_benched(cuda):
         for p0 in range(0, 64, 8):
             want = me_argmin_checker(cur[p0:p0 + 8], ref[p0:p0 + 8], blk, 32)
             assert np.array_equal(recs[p0 * nb:(p0 + 8) * nb], want), (blk, p0)
+
+
+def test_multi_plan_of_convolutions_runs_members(cuda):
+    # two Workloads over the same input and weights (plain and relu-fused
+    # conv): one MULTI plan, outputs back to back, each equal to its own run
+    from paper_1911_03458_b200 import run_full
+    ws = [W.conv_nchw_view(2, 16, 12, 10, 8, 3, 1, 1, 1, relu) for relu in (False, True)]
+    x = W.gen_uniform([2, 16, 12, 10], 500)
+    wt = W.gen_normal([8, 16, 3, 3], 501, 0.1)
+    for w in ws:
+        w.src_a, w.src_b = x, wt
+    g = PlanGroup(ws)
+    assert g.kernel == Kernel.MULTI and g.info.launches_per_run >= 2
+    res = g.run_host(x, wt)
+    for (out, aux), w in zip(res, ws):
+        assert aux is None
+        assert np.array_equal(out.view(np.uint32), run_full(w).view(np.uint32))
+
+
+def test_multi_plan_error_from_a_member(cuda):
+    # a REJECT gather out of range in the second member raises OutOfRange,
+    # as the reference's run_full of that Workload would
+    from paper_1911_03458_b200 import Error, ErrorCode
+    w1 = W.build_template("maxpool", {"h": 9, "w": 9, "k": 3})
+    W.fill_random(w1, 1, 2)
+    w2 = W.build_template("maxpool", {"h": 9, "w": 9, "k": 3})
+    w2.src_a, w2.src_b = w1.src_a, w1.src_b
+    w2.view_a.p_shape = [5, 4]
+    w2.view_b.p_shape = [5, 4]
+    g = PlanGroup([w1, w2])
+    with pytest.raises(Error) as ei:
+        g.run_host(w1.src_a, w1.src_b)
+    assert ei.value.code == ErrorCode.OutOfRange
+
+
+def test_u16_maps_in_a_multi_plan(cuda):
+    cur, ref = _frames(64, 128, 2, 330)
+    ws = []
+    for blk in (16, 8):
+        w = W.me_view(64, 128, blk, 32, pairs=2)
+        w.dtype_out = W.Dtype.U16
+        ws.append(w)
+    g = PlanGroup(ws, FLAG_ARGMIN)          # maps requested: members run one by one
+    assert g.kernel == Kernel.MULTI
+    for (sad, mv), blk in zip(g.run_host(cur, ref), (16, 8)):
+        want = O.me_sad(cur, ref, blk, 32)
+        assert sad.dtype == np.uint16 and np.array_equal(sad.astype(np.int32), want)
+        assert np.array_equal(mv, O.me_argmin(want, 32))
+
+
+def test_narrowed_real32_frames_with_pairs_axis_and_clamp(cuda):
+    from paper_1911_03458_b200 import run_full
+    cur, ref = _frames(48, 64, 3, 340)
+    w = W.me_view(48, 64, 16, 8, pairs=3)
+    w.view_b.boundary = W.Boundary.Clamp
+    w.src_a, w.src_b = cur.astype(np.float32), ref.astype(np.float32)
+    w.dtype_a = w.dtype_b = w.dtype_out = W.Dtype.Real32
+    assert Plan(w).kernel == Kernel.SAD
+    got = run_full(w)
+    assert np.array_equal(got, O.me_sad(cur, ref, 16, 8, clamp=True).astype(np.float32))
