@@ -88,6 +88,9 @@ struct SadLaunch {
   uint32_t key_mul;           // 65536 as a launch parameter: argmin keys acc * key_mul + d * WX
                               // stay IMADs (FMA pipe) instead of folding into ALU shift-adds
   uint32_t one;               // 1 as a launch parameter: sums written as IMADs (FMA pipe)
+  int fast_build;             // fused kernel: the staged geometry is the compile-time one
+                              // (sad_build_copies_fused) and the window starts word-aligned
+  int dref_w;                 // fused kernel: words of the staged rows before the window
 };
 
 // n / d for n < 2^31 by multiply-high (Granlund-Montgomery): s = ceil(log2 d),
@@ -215,7 +218,11 @@ __device__ __forceinline__ void sad_mbar_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
       "LAB_WAIT:\n\t"
+#ifdef MERIT_SAD_SUSPEND
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, " MERIT_SAD_SUSPEND ";\n\t"
+#else
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+#endif
       "@P1 bra DONE;\n\t"
       "bra LAB_WAIT;\n\t"
       "DONE:\n\t}" ::"r"(bar),
@@ -336,6 +343,35 @@ __device__ __forceinline__ void sad_build_copies(const SadLaunch& L, int tile, c
     if (w >= L.Ww) {
       w -= L.Ww;
       ++r;
+    }
+  }
+}
+
+// The fused kernel's copy builder: the staged geometry is fixed (8x8 blocks,
+// 8-block tiles, two block rows, a 65x65 window: R = 81 rows of Ww = 33 words,
+// raw rows of 40 words, CS = 2696) and the window starts on a word, so item
+// it = (r, w) of the flattened R x Ww walk reads raw word it + 7 r and writes
+// copy word it of each of the four byte shifts: no per-item row/column
+// bookkeeping (the generic builder spends ~45 instructions per item on it).
+constexpr int kFusedWW = 33, kFusedR = 81, kFusedRW = 40, kFusedCS = 2696, kFusedCPW = 20;
+template <int NT>
+__device__ __forceinline__ void sad_build_copies_fused(const uint32_t* raw, uint32_t* copies) {
+  constexpr int N = kFusedR * kFusedWW;
+  const uint32_t raw_s = smem_u32(raw), cop_s = smem_u32(copies);
+#pragma unroll
+  for (int k = 0; k < (N + NT - 1) / NT; ++k) {
+    const int it = static_cast<int>(threadIdx.x) + k * NT;
+    if ((k + 1) * NT <= N || it < N) {
+      const int r = it / kFusedWW;
+      const uint32_t ra = raw_s + static_cast<uint32_t>(it + (kFusedRW - kFusedWW) * r) * 4u;
+      const uint32_t ca = cop_s + static_cast<uint32_t>(it) * 4u;
+      uint32_t a0, a1;
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(a0) : "r"(ra));
+      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(a1) : "r"(ra + 4));
+      asm volatile("st.shared.u32 [%0], %1;" ::"r"(ca), "r"(a0) : "memory");
+      asm volatile("st.shared.u32 [%0], %1;" ::"r"(ca + 4 * kFusedCS), "r"(__byte_perm(a0, a1, 0x4321)) : "memory");
+      asm volatile("st.shared.u32 [%0], %1;" ::"r"(ca + 8 * kFusedCS), "r"(__byte_perm(a0, a1, 0x5432)) : "memory");
+      asm volatile("st.shared.u32 [%0], %1;" ::"r"(ca + 12 * kFusedCS), "r"(__byte_perm(a0, a1, 0x6543)) : "memory");
     }
   }
 }
@@ -712,8 +748,9 @@ __device__ __forceinline__ void sad_tile_work_fused(const SadLaunch& L, int32_t*
                                                     const uint32_t* curw, const uint32_t* copies, uint32_t* keys,
                                                     uint32_t* cnt, AfterCw after_cw) {
   constexpr int BLK = 8, NBY = 2, D = 33, WX = 65, WY = 65, BWW = 2, G = 2;
+  constexpr int WW = kFusedWW;  // staged row pitch in words (fixed geometry: the launcher checks L.Ww)
   const SadParams& p = L.p;
-  const int cpw = L.cur_pitch / 4;
+  constexpr int cpw = kFusedCPW;  // words per staged current row (fixed geometry)
   const int warp = static_cast<int>(threadIdx.x) >> 5;
   const int q = warp >> 2, h = warp & 3;
   const int lane = static_cast<int>(threadIdx.x) & 31;
@@ -755,15 +792,12 @@ __device__ __forceinline__ void sad_tile_work_fused(const SadLaunch& L, int32_t*
   for (int n = 0; n < NBY; ++n) best[n] = 0xffffffffu;
   const int col = ib * BLK + dxl;
   const uint32_t one = L.one;
-#ifdef MERIT_SAD_FUSED_UNROLL  // experiment: both dy groups unrolled (compile-time nd)
-#pragma unroll
-#else
+  // dy groups [0, 33) and [32, 65): both 33 rows, the shared dy = 32 gives
+  // the same key in both (min is idempotent), so the fold below is branch-free
+  constexpr int DY1 = WY - D;
 #pragma unroll 1
-#endif
   for (int ig = 0; ig < G; ++ig) {
-    const uint32_t* cp = copies + (col & 3) * L.CS + (col >> 2) + ig * D * L.Ww;
-    // the last group of the 65-row window has 32 rows (65 = 33 + 32)
-    const int nd = ig == 0 ? D : D - 1;
+    const uint32_t* cp = copies + (col & 3) * L.CS + (col >> 2) + ig * DY1 * WW;
     uint32_t acc[NBY][D];
 #pragma unroll
     for (int n = 0; n < NBY; ++n)
@@ -775,7 +809,7 @@ __device__ __forceinline__ void sad_tile_work_fused(const SadLaunch& L, int32_t*
       uint32_t rwv[BWW];
 #pragma unroll
       for (int j = 0; j < BWW; ++j) rwv[j] = cp[j];
-      cp += L.Ww;
+      cp += WW;
 #pragma unroll
       for (int n = 0; n < NBY; ++n)
 #pragma unroll
@@ -789,34 +823,29 @@ __device__ __forceinline__ void sad_tile_work_fused(const SadLaunch& L, int32_t*
       // displacement d is complete once its bottom block's last row
       // (r = d + 2 BLK - 1) is in: fold its keys here, so the key IMADs,
       // the shuffle and the mins interleave with the VABSDIFF4 stream and the
-      // two accumulators die early
-      // (two displacements per fold: 3-way mins)
+      // two accumulators die early (two displacements per fold: 3-way mins).
+      // Keys: 8x8 acc * 2^16 + dy * WX; 16x16 (sum of the four 8x8 SADs)
+      // * 2^16 + 4 dy * WX, built from the two 8x8 keys (t = k0 + k1 = (top +
+      // bottom) * 2^16 + 2c, plus the other half's t from lane ^ 16): three
+      // IMADs and a shuffle per displacement; the 4x index scaling keeps the
+      // raster order (4 * 65 * 65 < 2^16) and is undone when the record is written
       const int d = r - (NBY * BLK - 1);
       auto keys = [&](int dd, uint32_t& k0v, uint32_t& k1v, uint32_t& k2v) {
         const uint32_t c = static_cast<uint32_t>(dd * WX);
         k0v = acc[0][dd] * kmul + c;
         k1v = acc[1][dd] * kmul + c;
-        // 16x16: this half's top + bottom (an IMAD: FMA pipe), plus the other half's (lane ^ 16)
-        const uint32_t sv = acc[0][dd] * one + acc[1][dd];
-        const uint32_t so = __shfl_xor_sync(0xffffffffu, sv, 16);
-        k2v = sv * kmul + (so * kmul + c);
+        const uint32_t t = k0v * one + k1v;
+        const uint32_t to = __shfl_xor_sync(0xffffffffu, t, 16);
+        k2v = t * one + to;
       };
-      if (d >= 1 && d < D && (d & 1)) {
-        if (d < nd) {
-          uint32_t a0, a1, a2, b0, b1, b2;
-          keys(d - 1, a0, a1, a2);
-          keys(d, b0, b1, b2);
-          bn0 = __vimin3_u32(bn0, a0, b0);
-          bn1 = __vimin3_u32(bn1, a1, b1);
-          bn2 = __vimin3_u32(bn2, a2, b2);
-        } else if (d - 1 < nd) {
-          uint32_t a0, a1, a2;
-          keys(d - 1, a0, a1, a2);
-          bn0 = min(bn0, a0);
-          bn1 = min(bn1, a1);
-          bn2 = min(bn2, a2);
-        }
-      } else if (d == D - 1 && (d & 1) == 0 && d < nd) {  // odd D: the last one alone
+      if (d >= 1 && (d & 1)) {
+        uint32_t a0, a1, a2, b0, b1, b2;
+        keys(d - 1, a0, a1, a2);
+        keys(d, b0, b1, b2);
+        bn0 = __vimin3_u32(bn0, a0, b0);
+        bn1 = __vimin3_u32(bn1, a1, b1);
+        bn2 = __vimin3_u32(bn2, a2, b2);
+      } else if (d == D - 1 && (d & 1) == 0) {  // odd D: the last one alone
         uint32_t a0, a1, a2;
         keys(d, a0, a1, a2);
         bn0 = min(bn0, a0);
@@ -824,10 +853,10 @@ __device__ __forceinline__ void sad_tile_work_fused(const SadLaunch& L, int32_t*
         bn2 = min(bn2, a2);
       }
     }
-    const uint32_t k0 = static_cast<uint32_t>(ig * D * WX + dxl);
+    const uint32_t k0 = static_cast<uint32_t>(ig * DY1 * WX + dxl);
     best[0] = min(best[0], bn0 + k0);
     best[1] = min(best[1], bn1 + k0);
-    best2 = min(best2, bn2 + k0);
+    best2 = min(best2, bn2 + 4 * k0);
   }
   // the last column dx = 64 (byte column ib*8 + 64: shifted copy 0): this
   // lane takes dy = 16 h + (lane & 15); block row n reads staged rows dy + 8 n ..
@@ -838,12 +867,12 @@ __device__ __forceinline__ void sad_tile_work_fused(const SadLaunch& L, int32_t*
 #pragma unroll
     for (int n = 0; n < NBY; ++n) {
       ax[n] = 0;
-      const uint32_t* cx = cx0 + (dxl + n * BLK) * L.Ww;
+      const uint32_t* cx = cx0 + (dxl + n * BLK) * WW;
 #pragma unroll
       for (int i = 0; i < BLK; ++i) {
 #pragma unroll
         for (int j = 0; j < BWW; ++j) ax[n] = vabsdiff4_acc(cw[n][i][j], cx[j], ax[n]);
-        cx += L.Ww;
+        cx += WW;
       }
     }
     const uint32_t c = static_cast<uint32_t>(dxl * WX + (WX - 1));
@@ -851,14 +880,14 @@ __device__ __forceinline__ void sad_tile_work_fused(const SadLaunch& L, int32_t*
     best[1] = min(best[1], ax[1] * kmul + c);
     const uint32_t sv = ax[0] + ax[1];
     const uint32_t so = __shfl_xor_sync(0xffffffffu, sv, 16);
-    best2 = min(best2, (sv + so) * kmul + c);
+    best2 = min(best2, (sv + so) * kmul + 4 * c);
   }
   if (h == 3) {
     // corner (64, 64): each half's 8x8 block from its 16 lanes, the 16x16 block from all 32
     uint32_t v[NBY];
 #pragma unroll
     for (int n = 0; n < NBY; ++n)
-      v[n] = vabsdiff4_acc(ccw[n], cx0[(WY - 1 + n * BLK + (l16 >> 1)) * L.Ww + (l16 & 1)], 0u);
+      v[n] = vabsdiff4_acc(ccw[n], cx0[(WY - 1 + n * BLK + (l16 >> 1)) * WW + (l16 & 1)], 0u);
     const uint32_t c = static_cast<uint32_t>((WY - 1) * WX + (WX - 1));
     const uint32_t s0 = __reduce_add_sync(hmask, v[0]);
     const uint32_t s1 = __reduce_add_sync(hmask, v[1]);
@@ -867,18 +896,18 @@ __device__ __forceinline__ void sad_tile_work_fused(const SadLaunch& L, int32_t*
       best[0] = min(best[0], s0 * kmul + c);
       best[1] = min(best[1], s1 * kmul + c);
     }
-    if (lane == 0) best2 = min(best2, s2 * kmul + c);
+    if (lane == 0) best2 = min(best2, s2 * kmul + 4 * c);
   }
   if (by >= L.by1) return;
   // 8x8 records: 4 warps (h) x 16 lanes per block
-  auto fold = [&](uint32_t key, int slot, int32_t* a) {
+  auto fold = [&](uint32_t key, int slot, int32_t* a, int ishift) {
     atomicMin(&keys[slot], key);
     __threadfence_block();
     if (atomicAdd(&cnt[slot], 1u) == 3u) {
       __threadfence_block();
       const uint32_t fin = atomicExch(&keys[slot], 0xffffffffu);
       cnt[slot] = 0u;
-      const int k = static_cast<int>(fin & 0xffffu);
+      const int k = static_cast<int>(fin & 0xffffu) >> ishift;
       const int dy = k / WX, dx = k - (k / WX) * WX;
       a[0] = dy + p.oy - p.cy;
       a[1] = dx + p.ox - p.cx;
@@ -888,13 +917,13 @@ __device__ __forceinline__ void sad_tile_work_fused(const SadLaunch& L, int32_t*
 #pragma unroll
   for (int n = 0; n < NBY; ++n) {
     const uint32_t key = __reduce_min_sync(hmask, best[n]);
-    if (l16 == 0) fold(key, n * L.TBX + ib, aux + (blk_index + n * (long long)p.BX) * 3);
+    if (l16 == 0) fold(key, n * L.TBX + ib, aux + (blk_index + n * (long long)p.BX) * 3, 0);
   }
   // 16x16 record of block (by / 2, (bx0 + 2 q) / 2)
   const uint32_t key2 = __reduce_min_sync(0xffffffffu, best2);
   if (lane == 0) {
     const long long b2 = (pair * p.BY2 + by / 2) * (long long)p.BX2 + (bx0 >> 1) + q;
-    fold(key2, NBY * L.TBX + q, aux + p.aux2_delta + b2 * 3);
+    fold(key2, NBY * L.TBX + q, aux + p.aux2_delta + b2 * 3, 2);
   }
 }
 
@@ -1033,7 +1062,10 @@ sad_async_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ re
     const int b = k & 1, c = k % 3;
     if (k >= 3) sad_mbar_wait(bar_done + 8u * c, static_cast<uint32_t>((k - 3) / 3) & 1u);  // copies[c] free
     sad_mbar_wait(bar_tma + 8u * b, static_cast<uint32_t>(k >> 1) & 1u);
-    sad_build_copies<BLK>(L, tile_of(k), raw0, copies0 + c * 4 * L.CS, cp_r0, cp_w0);
+    if (MODE == 2 && L.fast_build)
+      sad_build_copies_fused<NT>(raw0 + L.dref_w, copies0 + c * 4 * L.CS);
+    else
+      sad_build_copies<BLK>(L, tile_of(k), raw0, copies0 + c * 4 * L.CS, cp_r0, cp_w0);
     arrive(bar_full + 8u * c);
   };
   if (threadIdx.x == 0 && nk > 0) issue(0);
@@ -1265,6 +1297,9 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
         if (kern == sad_kernel<8, 33, 2, 512, 65, true>) kern = sad_async_kernel<8, 33, 2, 512, 65, true>;
         if (kern == sad_kernel<8, 33, 1, 512, 65, true>) kern = sad_async_kernel<8, 33, 1, 512, 65, true>;
         if (p.fuse2) kern = sad_async_kernel<8, 33, 2, 512, 65, 2>;
+        if (p.fuse2 && (L.Ww != kFusedWW || L.R != kFusedR || L.rw != kFusedRW || L.CS != kFusedCS ||
+                        L.cur_pitch != 4 * kFusedCPW))
+          return fail(MERIT_E_UNSUPPORTED_VIEW, "fused SAD staging geometry");
       }
     }
   }
@@ -1275,6 +1310,13 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
   const int threads = (L.items + 31) / 32 * 32;
   L.key_mul = 65536u;
   L.one = 1u;
+  // fused kernel: compile-time staged geometry when it matches (always, for
+  // the +/-32 8x8 + 16x16 search; the window starts on a word when ox % 4 == 0)
+  L.dref_w = ((p.ox % 16) + 16) % 16 / 4;
+  L.fast_build = (p.fuse2 && threads == 512 && p.ox % 4 == 0) ? 1 : 0;
+#ifdef MERIT_NO_FAST_BUILD
+  L.fast_build = 0;
+#endif
   L.cp_sr = threads / L.Ww;
   L.cp_sw = threads - L.cp_sr * L.Ww;
   L.n_full_x = p.BX / L.TBX;
