@@ -347,31 +347,49 @@ __device__ __forceinline__ void sad_build_copies(const SadLaunch& L, int tile, c
   }
 }
 
-// The fused kernel's copy builder: the staged geometry is fixed (8x8 blocks,
-// 8-block tiles, two block rows, a 65x65 window: R = 81 rows of Ww = 33 words,
-// raw rows of 40 words, CS = 2696) and the window starts on a word, so item
-// it = (r, w) of the flattened R x Ww walk reads raw word it + 7 r and writes
-// copy word it of each of the four byte shifts: no per-item row/column
-// bookkeeping (the generic builder spends ~45 instructions per item on it).
-constexpr int kFusedWW = 33, kFusedR = 81, kFusedRW = 40, kFusedCS = 2696, kFusedCPW = 20;
-template <int NT>
-__device__ __forceinline__ void sad_build_copies_fused(const uint32_t* raw, uint32_t* copies) {
-  constexpr int N = kFusedR * kFusedWW;
+// Compile-time staging geometry of the warp-per-block kernels (8-block tiles,
+// TMA staging), the values the launcher derives at run time:
+// span = 8 BLK + WX - 1 bytes, Ww = ceil(span / 4) made odd, R = G D + NBY BLK
+// - 1 rows, raw rows of rw = 4 ceil((Ww + 5) / 4) words, CS = R Ww padded to 8
+// mod 32.  C2 (16x16, +/-16): Ww 41, R 48, rw 48,
+// CS 1992; C5 8x8 / fused (+/-32, two block rows): Ww 33, R 81, rw 40, CS 2696.
+template <int BLK, int WX, int NBY>
+struct WarpGeo {
+  static constexpr int D = 33, G = (WX + D - 1) / D;
+  static constexpr int span = 8 * BLK + WX - 1;
+  static constexpr int WW = ((span + 3) / 4) | 1;
+  static constexpr int R = G * D + NBY * BLK - 1;
+  static constexpr int RW = (WW + 5 + 3) / 4 * 4;
+  static constexpr int CS = R * WW + ((8 - (R * WW) % 32) + 32) % 32;
+};
+using FusedGeo = WarpGeo<8, 65, 2>;
+constexpr int kFusedCPW = (8 * 8 + 12 + 15) / 16 * 16 / 4;  // fused kernel: words per staged current row
+static_assert(FusedGeo::WW == 33 && FusedGeo::R == 81 && FusedGeo::RW == 40 && FusedGeo::CS == 2696, "fused geometry");
+static_assert(WarpGeo<16, 33, 1>::WW == 41 && WarpGeo<16, 33, 1>::CS == 1992, "C2 geometry");
+
+// The warp kernels' copy builder on that fixed geometry, for windows that
+// start on a word: item it = (r, w) of the flattened R x Ww walk reads raw
+// word it + (rw - Ww) r and writes copy word it of each of the four byte
+// shifts: no per-item row/column bookkeeping (the generic builder spends ~45
+// instructions per item on it).
+template <class GEO, int NT>
+__device__ __forceinline__ void sad_build_copies_geo(const uint32_t* raw, uint32_t* copies) {
+  constexpr int N = GEO::R * GEO::WW;
   const uint32_t raw_s = smem_u32(raw), cop_s = smem_u32(copies);
 #pragma unroll
   for (int k = 0; k < (N + NT - 1) / NT; ++k) {
     const int it = static_cast<int>(threadIdx.x) + k * NT;
     if ((k + 1) * NT <= N || it < N) {
-      const int r = it / kFusedWW;
-      const uint32_t ra = raw_s + static_cast<uint32_t>(it + (kFusedRW - kFusedWW) * r) * 4u;
+      const int r = it / GEO::WW;
+      const uint32_t ra = raw_s + static_cast<uint32_t>(it + (GEO::RW - GEO::WW) * r) * 4u;
       const uint32_t ca = cop_s + static_cast<uint32_t>(it) * 4u;
       uint32_t a0, a1;
       asm volatile("ld.shared.u32 %0, [%1];" : "=r"(a0) : "r"(ra));
       asm volatile("ld.shared.u32 %0, [%1];" : "=r"(a1) : "r"(ra + 4));
       asm volatile("st.shared.u32 [%0], %1;" ::"r"(ca), "r"(a0) : "memory");
-      asm volatile("st.shared.u32 [%0], %1;" ::"r"(ca + 4 * kFusedCS), "r"(__byte_perm(a0, a1, 0x4321)) : "memory");
-      asm volatile("st.shared.u32 [%0], %1;" ::"r"(ca + 8 * kFusedCS), "r"(__byte_perm(a0, a1, 0x5432)) : "memory");
-      asm volatile("st.shared.u32 [%0], %1;" ::"r"(ca + 12 * kFusedCS), "r"(__byte_perm(a0, a1, 0x6543)) : "memory");
+      asm volatile("st.shared.u32 [%0], %1;" ::"r"(ca + 4 * GEO::CS), "r"(__byte_perm(a0, a1, 0x4321)) : "memory");
+      asm volatile("st.shared.u32 [%0], %1;" ::"r"(ca + 8 * GEO::CS), "r"(__byte_perm(a0, a1, 0x5432)) : "memory");
+      asm volatile("st.shared.u32 [%0], %1;" ::"r"(ca + 12 * GEO::CS), "r"(__byte_perm(a0, a1, 0x6543)) : "memory");
     }
   }
 }
@@ -552,6 +570,7 @@ __device__ __forceinline__ void sad_tile_work_warp(const SadLaunch& L, void* __r
                                                    AfterCw after_cw) {
   constexpr int D = 33, WX = WXC, WY = WXC, BWW = BLK / 4;
   constexpr int WPB = (WX - 1) / 32;  // warps per block column
+  constexpr int WW = WarpGeo<BLK, WX, NBY>::WW;  // staged row pitch in words (the launcher checks L.Ww)
   constexpr int G = (WY + D - 1) / D;
   const SadParams& p = L.p;
   const int cpw = L.cur_pitch / 4;
@@ -615,7 +634,7 @@ __device__ __forceinline__ void sad_tile_work_warp(const SadLaunch& L, void* __r
   const int col = ib * BLK + dxl;  // byte column of this lane's dx in the staged window
 #pragma unroll 1
   for (int ig = 0; ig < G; ++ig) {
-    const uint32_t* cp = copies + (col & 3) * L.CS + (col >> 2) + ig * D * L.Ww;
+    const uint32_t* cp = copies + (col & 3) * L.CS + (col >> 2) + ig * D * WW;
     uint32_t acc[NBY][D];
 #pragma unroll
     for (int n = 0; n < NBY; ++n)
@@ -626,7 +645,7 @@ __device__ __forceinline__ void sad_tile_work_warp(const SadLaunch& L, void* __r
       uint32_t rwv[BWW];
 #pragma unroll
       for (int j = 0; j < BWW; ++j) rwv[j] = cp[j];
-      cp += L.Ww;
+      cp += WW;
 #pragma unroll
       for (int n = 0; n < NBY; ++n)
 #pragma unroll
@@ -665,12 +684,12 @@ __device__ __forceinline__ void sad_tile_work_warp(const SadLaunch& L, void* __r
 #pragma unroll
   for (int n = 0; n < NBY; ++n) {
     uint32_t ax = 0;
-    const uint32_t* cx = cx0 + (dxl + n * BLK) * L.Ww;
+    const uint32_t* cx = cx0 + (dxl + n * BLK) * WW;
 #pragma unroll
     for (int i = 0; i < BLK; ++i) {
 #pragma unroll
       for (int j = 0; j < BWW; ++j) ax = vabsdiff4_acc(cw[n][i][j], cx[j], ax);
-      cx += L.Ww;
+      cx += WW;
     }
     best[n] = min(best[n], ax * kmul + static_cast<uint32_t>(dxl * WX + (WX - 1)));
     const long long bb = (blk_index + n * (long long)p.BX) * (long long)(WY * WX);
@@ -683,10 +702,10 @@ __device__ __forceinline__ void sad_tile_work_warp(const SadLaunch& L, void* __r
       if constexpr (PER >= 1) {
         const int i = lane / (BWW / PER), j0 = PER * (lane % (BWW / PER));
 #pragma unroll
-        for (int q = 0; q < PER; ++q) v = vabsdiff4_acc(ccw[n][q], cx0[(WY - 1 + n * BLK + i) * L.Ww + j0 + q], v);
+        for (int q = 0; q < PER; ++q) v = vabsdiff4_acc(ccw[n][q], cx0[(WY - 1 + n * BLK + i) * WW + j0 + q], v);
       } else if (lane < BLK * BWW) {
         const int i = lane / BWW, j = lane % BWW;
-        v = vabsdiff4_acc(ccw[n][0], cx0[(WY - 1 + n * BLK + i) * L.Ww + j], 0u);
+        v = vabsdiff4_acc(ccw[n][0], cx0[(WY - 1 + n * BLK + i) * WW + j], 0u);
       }
       const uint32_t axx = __reduce_add_sync(0xffffffffu, v);
       if (lane == 0) best[n] = min(best[n], axx * kmul + static_cast<uint32_t>((WY - 1) * WX + (WX - 1)));
@@ -748,7 +767,7 @@ __device__ __forceinline__ void sad_tile_work_fused(const SadLaunch& L, int32_t*
                                                     const uint32_t* curw, const uint32_t* copies, uint32_t* keys,
                                                     uint32_t* cnt, AfterCw after_cw) {
   constexpr int BLK = 8, NBY = 2, D = 33, WX = 65, WY = 65, BWW = 2, G = 2;
-  constexpr int WW = kFusedWW;  // staged row pitch in words (fixed geometry: the launcher checks L.Ww)
+  constexpr int WW = FusedGeo::WW;  // staged row pitch in words (fixed geometry: the launcher checks L.Ww)
   const SadParams& p = L.p;
   constexpr int cpw = kFusedCPW;  // words per staged current row (fixed geometry)
   const int warp = static_cast<int>(threadIdx.x) >> 5;
@@ -1062,10 +1081,19 @@ sad_async_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ re
     const int b = k & 1, c = k % 3;
     if (k >= 3) sad_mbar_wait(bar_done + 8u * c, static_cast<uint32_t>((k - 3) / 3) & 1u);  // copies[c] free
     sad_mbar_wait(bar_tma + 8u * b, static_cast<uint32_t>(k >> 1) & 1u);
-    if (MODE == 2 && L.fast_build)
-      sad_build_copies_fused<NT>(raw0 + L.dref_w, copies0 + c * 4 * L.CS);
-    else
-      sad_build_copies<BLK>(L, tile_of(k), raw0, copies0 + c * 4 * L.CS, cp_r0, cp_w0);
+    bool built = false;
+    if constexpr (MODE == 2) {
+      if (L.fast_build) {
+        sad_build_copies_geo<FusedGeo, NT>(raw0 + L.dref_w, copies0 + c * 4 * L.CS);
+        built = true;
+      }
+    } else if constexpr (MODE == 1 && WXC > 0) {
+      if (L.fast_build) {
+        sad_build_copies_geo<WarpGeo<BLK, WXC, NBY>, NT>(raw0 + L.dref_w, copies0 + c * 4 * L.CS);
+        built = true;
+      }
+    }
+    if (!built) sad_build_copies<BLK>(L, tile_of(k), raw0, copies0 + c * 4 * L.CS, cp_r0, cp_w0);
     arrive(bar_full + 8u * c);
   };
   if (threadIdx.x == 0 && nk > 0) issue(0);
@@ -1261,6 +1289,11 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
       if (warp_mode) kern = L.nby == 2 ? sad_kernel<8, 33, 2, 512, 65, true> : sad_kernel<8, 33, 1, 512, 65, true>;
     }
   }
+  if (warp_mode) {
+    const int ww = BLK == 16 ? (p.WX == 33 ? WarpGeo<16, 33, 1>::WW : WarpGeo<16, 65, 1>::WW)
+                             : WarpGeo<8, 65, 1>::WW;
+    if (L.Ww != ww) return fail(MERIT_E_UNSUPPORTED_VIEW, "warp-per-block SAD row pitch");
+  }
   if (const char* we = getenv("MERIT_SAD_WXC"); we && we[0] == '0' && !warp_mode) {  // A/B: runtime width
     kern = nt == 512 ? sad_kernel<BLK, D, 1, 512, 0> : sad_kernel<BLK, D, 1, 256, 0>;
     if constexpr (BLK == 8) {
@@ -1297,8 +1330,8 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
         if (kern == sad_kernel<8, 33, 2, 512, 65, true>) kern = sad_async_kernel<8, 33, 2, 512, 65, true>;
         if (kern == sad_kernel<8, 33, 1, 512, 65, true>) kern = sad_async_kernel<8, 33, 1, 512, 65, true>;
         if (p.fuse2) kern = sad_async_kernel<8, 33, 2, 512, 65, 2>;
-        if (p.fuse2 && (L.Ww != kFusedWW || L.R != kFusedR || L.rw != kFusedRW || L.CS != kFusedCS ||
-                        L.cur_pitch != 4 * kFusedCPW))
+        if (p.fuse2 && (L.Ww != FusedGeo::WW || L.R != FusedGeo::R || L.rw != FusedGeo::RW ||
+                        L.CS != FusedGeo::CS || L.cur_pitch != 4 * kFusedCPW))
           return fail(MERIT_E_UNSUPPORTED_VIEW, "fused SAD staging geometry");
       }
     }
@@ -1310,10 +1343,24 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
   const int threads = (L.items + 31) / 32 * 32;
   L.key_mul = 65536u;
   L.one = 1u;
-  // fused kernel: compile-time staged geometry when it matches (always, for
-  // the +/-32 8x8 + 16x16 search; the window starts on a word when ox % 4 == 0)
+  // warp-per-block / fused kernels: the copy builder on the compile-time
+  // staging geometry when it matches (TMA staging, 8-block tiles) and the
+  // window starts on a word (ox % 4 == 0)
   L.dref_w = ((p.ox % 16) + 16) % 16 / 4;
-  L.fast_build = (p.fuse2 && threads == 512 && p.ox % 4 == 0) ? 1 : 0;
+  auto geo_is = [&](auto geo) {
+    using GEO = decltype(geo);
+    return L.Ww == GEO::WW && L.R == GEO::R && L.rw == GEO::RW && L.CS == GEO::CS;
+  };
+  bool geo_ok = false;
+  if constexpr (D == 33) {
+    if (p.fuse2)
+      geo_ok = geo_is(FusedGeo{}) && threads == 512;
+    else if (warp_mode && BLK == 16)
+      geo_ok = p.WX == 33 ? geo_is(WarpGeo<16, 33, 1>{}) && threads == 256 : geo_is(WarpGeo<16, 65, 1>{}) && threads == 512;
+    else if (warp_mode && BLK == 8)
+      geo_ok = L.nby == 2 ? geo_is(WarpGeo<8, 65, 2>{}) : geo_is(WarpGeo<8, 65, 1>{});
+  }
+  L.fast_build = (use_async && L.tma && geo_ok && p.ox % 4 == 0) ? 1 : 0;
 #ifdef MERIT_NO_FAST_BUILD
   L.fast_build = 0;
 #endif
