@@ -328,6 +328,95 @@ def _dist_init(backend, device=None):
     return dist
 
 
+def time_device(case, steps, warmup, soak, stream, lib, barrier, local, graph=True):
+    """W untimed warm-up steps, a clock soak of the same step, then exactly K
+    steps between barrier + synchronize on both sides, CUDA events on the
+    launching stream.  The K steps are captured once into a CUDA graph that is
+    replayed inside the timed region (microsecond-scale kernels are otherwise
+    bound by the host launch path).  Returns (ms, launches, last kernel, clocks)."""
+    import torch
+    sp = stream.cuda_stream
+    with torch.cuda.stream(stream):
+        for i in range(warmup):
+            case.step(i, sp)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    t_soak = time.perf_counter()
+    i = 0
+    with torch.cuda.stream(stream):
+        while time.perf_counter() - t_soak < soak:
+            for _ in range(4):
+                case.step(i, sp)
+                i += 1
+            stream.synchronize()
+    l0 = lib.merit_dev_launch_count()
+    g = None
+    if graph:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            for i in range(steps):
+                case.step(i, sp)
+        torch.cuda.synchronize()
+        # one untimed replay: the first launch of an instantiated graph also
+        # uploads it (~1 us per captured node), which is not a step's cost
+        with torch.cuda.stream(stream):
+            g.replay()
+        torch.cuda.synchronize()
+    launches = lib.merit_dev_launch_count() - l0
+    kern_name = (lib.merit_dev_last_kernel() or b"").decode()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    with torch.cuda.stream(stream):
+        if g is not None:
+            g.replay()
+        else:
+            for i in range(steps):
+                case.step(i, sp)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks.stop()
+    if g is None:
+        launches = lib.merit_dev_launch_count() - l0
+        kern_name = (lib.merit_dev_last_kernel() or b"").decode()
+    return e0.elapsed_time(e1), launches, kern_name, clocks
+
+
+# steps for the other configurations' per_config entries (microsecond-scale steps)
+PER_CONFIG_STEPS = {"C1": 200, "C2": 200, "C3": 200, "C4": 100}
+
+
+def per_config_entries(args, device, stream, lib, local, peaks, peaks_kind):
+    """The other configurations on the same GPU (N = 1 only), device-resident
+    inputs, the same timing protocol as the headline (own K, W = 5, clock
+    soak, CUDA-graph replay, rotating sets > L2): value, ms/step, the dominant
+    kernel's roofline fraction and the clocks seen."""
+    import torch
+    out = {}
+    for c in ("C1", "C2", "C3", "C4"):
+        if c == args.config:
+            continue
+        case = Case(c, 0, 1, device)
+        k = PER_CONFIG_STEPS[c]
+        ms, launches, kern, clk = time_device(case, k, 5, 0.3, stream, lib, lambda: None, local)
+        step_ms = ms / k
+        rf, _ = roofline(case, step_ms, peaks, peaks_kind, kern, None)
+        out[c] = {"workload": WORKLOAD[c], "value": round(case.outputs_per_step / (step_ms * 1e-3) / 1e9, 4),
+                  "unit": UNIT, "ms_per_step": round(step_ms, 6), "steps": k, "warmup": 5,
+                  "dtype": case.dtype, "gpu_launches": int(launches), "l2": case.rotation,
+                  "roofline": {kk: rf[kk] for kk in ("bound", "achieved", "peak", "unit", "frac", "kernel")
+                               if kk in rf},
+                  "clocks": clk.summary("timed region + 0.3 s soak")}
+        del case
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args):
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -348,59 +437,8 @@ def run_ours(args):
         if dist is not None:
             dist.barrier()
 
-    # warm-up (untimed)
-    with torch.cuda.stream(stream):
-        for i in range(args.warmup):
-            case.step(i, sp)
-    torch.cuda.synchronize()
-    # clock soak: the same step, untimed, so the sampler sees the loaded clock
-    clocks = ClockSampler(local)
-    clocks.start()
-    t_soak = time.perf_counter()
-    i = 0
-    with torch.cuda.stream(stream):
-        while time.perf_counter() - t_soak < args.soak:
-            for _ in range(4):
-                case.step(i, sp)
-                i += 1
-            stream.synchronize()
-    # timed region: exactly K steps.  The K steps are captured once into a
-    # CUDA graph and the graph is replayed inside the timed region
-    # (microsecond-scale kernels are otherwise bound by the host launch path).
-    l0 = lib.merit_dev_launch_count()
-    graph = None
-    if not args.no_graph:
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph, stream=stream):
-            for i in range(args.steps):
-                case.step(i, sp)
-        torch.cuda.synchronize()
-        # one untimed replay: the first launch of an instantiated graph also
-        # uploads it (~1 us per captured node), which is not a step's cost
-        with torch.cuda.stream(stream):
-            graph.replay()
-        torch.cuda.synchronize()
-    launches = lib.merit_dev_launch_count() - l0
-    kern_name = (lib.merit_dev_last_kernel() or b"").decode()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    barrier()
-    torch.cuda.synchronize()
-    e0.record(stream)
-    with torch.cuda.stream(stream):
-        if graph is not None:
-            graph.replay()
-        else:
-            for i in range(args.steps):
-                case.step(i, sp)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    barrier()
-    clocks.stop()
-    if graph is None:
-        launches = lib.merit_dev_launch_count() - l0
-        kern_name = (lib.merit_dev_last_kernel() or b"").decode()
-    ms = e0.elapsed_time(e1)
+    ms, launches, kern_name, clocks = time_device(case, args.steps, args.warmup, args.soak, stream, lib, barrier,
+                                                  local, graph=not args.no_graph)
     t = torch.tensor([ms], dtype=torch.float64, device=device)
     if dist is not None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -452,6 +490,8 @@ def run_ours(args):
     }
     if rf2 is not None:
         line["roofline_hbm"] = rf2
+    if world == 1 and not args.no_per_config:
+        line["per_config"] = per_config_entries(args, device, stream, lib, local, peaks, peaks_kind)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.config, budget_s=args.cpu_budget)
         line["cpu_baseline_oracle_loop"] = cpu_baseline(args.config, budget_s=args.cpu_budget / 3,
@@ -576,6 +616,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA graph")
     ap.add_argument("--dry-run", action="store_true", help="CPU check of the multi-rank shard logic (gloo)")
+    ap.add_argument("--no-per-config", action="store_true",
+                    help="N=1: skip the per_config entries (the other configurations, device-resident)")
     ap.add_argument("--no-fuse", action="store_true", help="C5: run the two Workloads as separate plans")
     ap.add_argument("--sad-map", default="i32", choices=["i32", "u16"],
                     help="C2: SAD map element type (u16 is exact and halves the map's bytes)")
