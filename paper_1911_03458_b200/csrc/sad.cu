@@ -814,8 +814,12 @@ __device__ __forceinline__ void sad_tile_work_fused(const SadLaunch& L, int32_t*
   // dy groups [0, 33) and [32, 65): both 33 rows, the shared dy = 32 gives
   // the same key in both (min is idempotent), so the fold below is branch-free
   constexpr int DY1 = WY - D;
+#ifndef MERIT_FUSED_HOTX  // timing experiment: run the dy groups MERIT_FUSED_HOTX times (same result)
+#define MERIT_FUSED_HOTX 1
+#endif
 #pragma unroll 1
-  for (int ig = 0; ig < G; ++ig) {
+  for (int igx = 0; igx < G * MERIT_FUSED_HOTX; ++igx) {
+    const int ig = igx % G;
     const uint32_t* cp = copies + (col & 3) * L.CS + (col >> 2) + ig * DY1 * WW;
     uint32_t acc[NBY][D];
 #pragma unroll
