@@ -490,7 +490,7 @@ def run_ours(args):
     }
     if rf2 is not None:
         line["roofline_hbm"] = rf2
-    if world == 1 and not args.no_per_config:
+    if world == 1 and args.config == "C5" and not args.no_per_config:
         line["per_config"] = per_config_entries(args, device, stream, lib, local, peaks, peaks_kind)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.config, budget_s=args.cpu_budget)
@@ -617,7 +617,7 @@ def main():
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA graph")
     ap.add_argument("--dry-run", action="store_true", help="CPU check of the multi-rank shard logic (gloo)")
     ap.add_argument("--no-per-config", action="store_true",
-                    help="N=1: skip the per_config entries (the other configurations, device-resident)")
+                    help="C5 at N=1: skip the per_config entries (C1-C4 on the same GPU, device-resident)")
     ap.add_argument("--no-fuse", action="store_true", help="C5: run the two Workloads as separate plans")
     ap.add_argument("--sad-map", default="i32", choices=["i32", "u16"],
                     help="C2: SAD map element type (u16 is exact and halves the map's bytes)")
