@@ -54,7 +54,9 @@ struct S1Args {
   int tiles_per_img;   // ceil(Ho / rows)
   int n_tiles;
   int n_full;          // units below n_full are whole tiles; the last (n_tiles - n_full)
-  int n_units;         // tiles run as two half-N units each (the final, partial wave)
+  int n_units;         // tiles from n_full on run as `parts` N-part units each (the final, partial wave)
+  int parts;           // 2 or 4: output-channel parts of a tail tile (N = 3 BN / parts)
+  int parts_log2;      // log2(parts)
   int n_groups;        // KH * CB
   uint32_t raw_bytes;  // 128 slots * 32 ch * 4 = 16 KB (half a 64-channel k-block)
   uint32_t a_slot;     // nsplit planes x 16 KB
@@ -153,15 +155,16 @@ conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
   pdl_wait();  // prologue done: from here on global memory is touched
   const int BN = p.BN;
   const int W = p.W;
-  // scheduling unit -> (tile, half): half = -1 for a whole tile, 0 / 1 for the
-  // lower / upper half of the output channels of a tail tile
+  // scheduling unit -> (tile, half): half = -1 for a whole tile, else the
+  // part 0 .. parts - 1 of the output channels of a tail tile (BN / parts
+  // channels each; the name `half` is kept for parts = 2)
   auto unit_of = [&](int u, int& tile, int& half) {
     if (u < A.n_full) {
       tile = u;
       half = -1;
     } else {
-      tile = A.n_full + ((u - A.n_full) >> 1);
-      half = (u - A.n_full) & 1;
+      tile = A.n_full + ((u - A.n_full) >> A.parts_log2);
+      half = (u - A.n_full) & (A.parts - 1);
     }
   };
   const int slots_mask = (1 << A.slots_log2) - 1;
@@ -309,9 +312,9 @@ conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
         unit_of(u, tile, half);
         for (int g = 0; g < A.n_groups; ++g) {
           twait_s1(b_empty(st), ph ^ 1, w1, pon);
-          // a half unit stacks the taps' rows of its 32-channel half: N = 3 BN / 2
-          const uint32_t rows = half < 0 ? A.b_plane : A.b_plane / 2;
-          const uint32_t src_off = half < 0 ? 0u : static_cast<uint32_t>(half) * (A.b_plane / 2);
+          // a part unit stacks the taps' rows of its channel part: N = 3 BN / parts
+          const uint32_t rows = half < 0 ? A.b_plane : A.b_plane >> A.parts_log2;
+          const uint32_t src_off = half < 0 ? 0u : static_cast<uint32_t>(half) * rows;
           mbar_expect_tx(b_full(st), 3u * nsp * rows);
           for (int kx = 0; kx < 3; ++kx)
             for (int sp = 0; sp < nsp; ++sp)
@@ -327,14 +330,14 @@ conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
     // operands in uniform registers), one elected lane issues each MMA ======
     const bool pon_w = (A.debug & 64) != 0;
     const uint32_t idesc_full = make_idesc(3 * BN);
-    const uint32_t idesc_half = make_idesc(3 * (BN / 2));
+    const uint32_t idesc_half = make_idesc(3 * (BN >> A.parts_log2));
     int as = 0, bs = 0, acc = 0;
     uint32_t aph = 0, bph = 0, acc_phase = 0;
     for (int u = blockIdx.x; u < A.n_units; u += gridDim.x) {
       int tile, half;
       unit_of(u, tile, half);
       const uint32_t idesc = half < 0 ? idesc_full : idesc_half;
-      const uint32_t b_lo16 = (3 * (half < 0 ? A.b_plane : A.b_plane / 2)) >> 4;  // lo planes, descriptor units
+      const uint32_t b_lo16 = (3 * (half < 0 ? A.b_plane : A.b_plane >> A.parts_log2)) >> 4;  // lo planes, descriptor units
       twait_s1(tempty(acc), acc_phase ^ 1, w3, pon_w);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * acc_cols;
@@ -347,15 +350,15 @@ conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
         tc_fence_after();
         const uint64_t bd = sw128_desc(bring + bs * A.b_slot);
         if (A.resident && half >= 0) {
-          // half unit on the resident full image: one N = BN / 2 MMA per tap
-          // (rows kx * BN + half * BN / 2 of each split plane) into columns kx * BN / 2
-          const uint32_t hb = static_cast<uint32_t>(p.BN / 2);
+          // part unit on the resident full image: one N = BN / parts MMA per tap
+          // (rows kx * BN + part * BN / parts of each split plane) into columns kx * BN / parts
+          const uint32_t hb = static_cast<uint32_t>(p.BN >> A.parts_log2);
           const uint32_t lo16 = (3u * A.b_plane) >> 4;
 #pragma unroll
           for (int kx = 0; kx < 3; ++kx) {
-            const uint64_t bk = bd + ((static_cast<uint32_t>(kx * p.BN + half * (p.BN / 2)) * 128u) >> 4);
+            const uint64_t bk = bd + ((static_cast<uint32_t>(kx * p.BN + half * (p.BN >> A.parts_log2)) * 128u) >> 4);
             const uint32_t dk = d_tmem + static_cast<uint32_t>(kx) * hb;
-            const uint32_t idk = make_idesc(p.BN / 2);
+            const uint32_t idk = make_idesc(p.BN >> A.parts_log2);
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
               if constexpr (TMEMA) {
@@ -432,8 +435,8 @@ conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
       const int n = tile / A.tiles_per_img;
       const int y = (tile - n * A.tiles_per_img) * A.rows + r;
       const bool store = x >= 0 && x < W && y < p.Ho && !(A.debug & 128);
-      // a half unit holds 32 channels: P_kx at columns kx * bn
-      const int bn = half < 0 ? BN : BN / 2;
+      // a part unit holds BN / parts channels: P_kx at columns kx * bn
+      const int bn = half < 0 ? BN : BN >> A.parts_log2;
       const int co_off = half < 0 ? 0 : half * bn;
       const int n_chunks = bn / kEC;
       const int my_last = ((n_chunks - 1 - set) / 2) * 2 + set;  // this set's last chunk
@@ -609,15 +612,24 @@ merit_status launch_conv_s1(const merit_plan& plan, const void* a, const void* p
   int grid = num_sms();
   if (grid > A.n_tiles) grid = A.n_tiles;
   grid = grid_cap(grid);
-  // Tail split: the final partial wave of r = n_tiles % grid tiles runs as 2r
-  // half-N units, so it costs half a tile instead of a whole one (C3: 896
-  // tiles on 148 SMs).  Needs N / 2 = 3 BN / 2 to stay a multiple of 16.
+  // Tail split: the final partial wave of r = n_tiles % grid tiles runs as
+  // `parts` r units of BN / parts output channels each, so it costs 1 / parts
+  // of a tile instead of a whole one (C3: 896 tiles on 148 SMs, r = 8: four
+  // parts of 16 channels, the busiest SM runs 6.25 tiles against 6.05 on
+  // average; halves: 6.5).  A part keeps BN / parts a multiple of 16 (N =
+  // 3 BN / parts a multiple of 16, whole 8-row B atoms, two epilogue chunks).
+  // MERIT_S1_SPLIT=0 / 2 / 4: no split / halves / quarters (A/B).
   {
     const int r = A.n_tiles % grid;
     const char* se = getenv("MERIT_S1_SPLIT");
-    const bool split = !(se && se[0] == '0') && r > 0 && 2 * r <= grid && p.BN % 32 == 0;
-    A.n_full = split ? A.n_tiles - r : A.n_tiles;
-    A.n_units = A.n_full + 2 * (A.n_tiles - A.n_full);
+    const int want = se ? atoi(se) : 4;
+    A.parts = 1;
+    for (int parts : {4, 2})
+      if (A.parts == 1 && parts <= want && r > 0 && parts * r <= grid && p.BN % (16 * parts) == 0) A.parts = parts;
+    A.n_full = A.parts > 1 ? A.n_tiles - r : A.n_tiles;
+    A.n_units = A.n_full + A.parts * (A.n_tiles - A.n_full);
+    if (A.parts == 1) A.parts = 2;  // unused (no part units)
+    A.parts_log2 = A.parts == 4 ? 2 : 1;
   }
   {
     const char* dbg = debug_env("MERIT_CONV_DEBUG");
