@@ -50,6 +50,8 @@ struct S1Args {
   const uint8_t* wpk;
   float* out;
   int slots_log2;      // slots per output row = 1 << slots_log2
+  int segs_log2;       // 32-lane segments per output row (slots / 32)
+  int seg_w;           // output columns per segment (<= 30: the segment's lanes 1 .. seg_w)
   int rows;            // output rows per tile = 128 / slots
   int tiles_per_img;   // ceil(Ho / rows)
   int n_tiles;
@@ -168,6 +170,19 @@ conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
     }
   };
   const int slots_mask = (1 << A.slots_log2) - 1;
+  // Segmented slot layout: TMEM lane quadrant q (A rows 32q .. 32q + 31) is
+  // segment sg = q % S of output row r = q / S (S = slots / 32): lane l holds
+  // input column x = sg * seg_w - 1 + l, so lanes 1 .. seg_w produce outputs
+  // sg * seg_w .. + seg_w - 1 and both neighbours of every output column
+  // (x - 1, x + 1) are in the same warp: the epilogue's tap shifts are plain
+  // lane shuffles.  Raw row r holds column x at word r * slots + x (x = -1:
+  // the previous row's zero-filled tail, or the pad before the ring; x >= W:
+  // the box's zero fill).
+  auto seg_word = [&](int q, int l) {
+    const int r = q >> A.segs_log2, sg = q & ((1 << A.segs_log2) - 1);
+    return (r << A.slots_log2) + sg * A.seg_w - 1 + l;
+  };
+  (void)slots_mask;
   const bool pon = (A.debug & 64) && lane == 0 && warp < 16;
   unsigned long long w1 = 0, w2 = 0, w3 = 0;
   const unsigned long long t_start = clock64();
@@ -210,7 +225,8 @@ conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
     // raw [c][128 slots]: A row m is slot m, i.e. raw word m - 1 (the
     // zero-filled column x = slots - 1 of the previous row, or the pad, for
     // x = -1); channel stride 512 B, an immediate
-    const uint32_t lane_off = static_cast<uint32_t>(m - 1) * 4u;
+    const uint32_t lane_off = static_cast<uint32_t>(seg_word(q, lane)) * 4u;
+    (void)m;
     const uint32_t t_lane = tmem_base + (static_cast<uint32_t>(32 * q) << 16) + kTmemA + 16u * h;
     int rs = h, as = 0;
     uint32_t rph = 0, aph = 0;
@@ -259,7 +275,7 @@ conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
         const uint32_t src = rring + rs * A.raw_bytes + cbase;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const uint32_t a0 = src + static_cast<uint32_t>(32 * j + lane - 1) * 4u;
+          const uint32_t a0 = src + static_cast<uint32_t>(seg_word(j, lane)) * 4u;
           const float* sp = reinterpret_cast<const float*>(smem_raw + (a0 - smem_u32(smem_raw)));
 #pragma unroll
           for (int c = 0; c < 8; ++c) v[j][c] = sp[c * 128];
@@ -412,29 +428,24 @@ conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
     __syncwarp();
   } else if ((warp >= kWarpEpi0 && warp < kWarpEpi0 + 4) || warp >= kWarpEpi1) {
     // ============ epilogue: out[x] = P0[x-1] + P1[x] + P2[x+1] =============
-    // Warp quadrant q holds A rows 32q..32q+31; set k (0: warps 10-13,
-    // 1: warps 15-18) takes chunks of kEC channels c0 = kEC * (2i + k).  The
-    // x-1 / x+1 neighbours are lane shuffles; across a warp boundary the
-    // edge values go through a small shared exchange (double-buffered by
-    // chunk, one named barrier per set and chunk).
+    // Warp quadrant q holds A rows 32q..32q+31 (one row segment with its two
+    // halo columns); set k (0: warps 10-13, 1: warps 15-18) takes chunks of
+    // kEC channels c0 = kEC * (2i + k).  The x - 1 / x + 1 neighbours are lane
+    // shuffles inside the segment: no cross-warp exchange, no barrier.
     const int q = warp & 3;
     const int set = warp >= kWarpEpi1 ? 1 : 0;
-    const int arow = 32 * q + lane;
-    const int r = arow >> A.slots_log2;
-    const int x = (arow & slots_mask) - 1;
+    const int r = q >> A.segs_log2;
+    const int x = (q & ((1 << A.segs_log2) - 1)) * A.seg_w + lane - 1;
+    const bool in_seg = lane >= 1 && lane <= A.seg_w;
     const bool relu = p.post == POST_RELU;
-    const bool first = lane == 0, last = lane == 31;
-    const bool has_prev = q > 0, has_next = q < 3;
-    const uint32_t xset = xring + static_cast<uint32_t>(set) * (2 * 4 * 16 * 4);
     int acc = 0;
     uint32_t acc_phase = 0;
-    int par = 0;
     for (int u = blockIdx.x; u < A.n_units; u += gridDim.x) {
         int tile, half;
         unit_of(u, tile, half);
       const int n = tile / A.tiles_per_img;
       const int y = (tile - n * A.tiles_per_img) * A.rows + r;
-      const bool store = x >= 0 && x < W && y < p.Ho && !(A.debug & 128);
+      const bool store = in_seg && x < W && y < p.Ho && !(A.debug & 128);
       // a part unit holds BN / parts channels: P_kx at columns kx * bn
       const int bn = half < 0 ? BN : BN >> A.parts_log2;
       const int co_off = half < 0 ? 0 : half * bn;
@@ -463,45 +474,17 @@ conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
           __syncwarp();
           if (lane == 0) mbar_arrive(tempty(acc));
         }
-        // edge values for the neighbouring warps: lane 31's P0, lane 0's P2
-        const uint32_t xb = xset + static_cast<uint32_t>((par * 4 + q) * 16) * 4u;
-        if (last) {
-          st_shared_v4(xb, p0[0], p0[1], p0[2], p0[3]);
-          st_shared_v4(xb + 16u, p0[4], p0[5], p0[6], p0[7]);
-        }
-        if (first) {
-          st_shared_v4(xb + 32u, p2[0], p2[1], p2[2], p2[3]);
-          st_shared_v4(xb + 48u, p2[4], p2[5], p2[6], p2[7]);
-        }
-        asm volatile("bar.sync %0, 128;" ::"r"(1 + set) : "memory");
-        // every lane loads the (warp-uniform, broadcast) neighbour edges and
-        // selects them on lane 0 / 31: no divergent branches in the loop
-        uint32_t xp[kEC], xn[kEC];
-        const uint32_t xpa = xset + static_cast<uint32_t>((par * 4 + ((q + 3) & 3)) * 16) * 4u;
-        const uint32_t xna = xset + static_cast<uint32_t>((par * 4 + ((q + 1) & 3)) * 16 + 8) * 4u;
-#pragma unroll
-        for (int e = 0; e < kEC; e += 4) {
-          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                       : "=r"(xp[e]), "=r"(xp[e + 1]), "=r"(xp[e + 2]), "=r"(xp[e + 3])
-                       : "r"(xpa + 4u * e));
-          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
-                       : "=r"(xn[e]), "=r"(xn[e + 1]), "=r"(xn[e + 2]), "=r"(xn[e + 3])
-                       : "r"(xna + 4u * e));
-        }
         const int cmax = p.Cout - co_off - c0;  // channels of this chunk that exist
         float* ptr = dst + (long long)c0 * co_stride;
 #pragma unroll
         for (int e = 0; e < kEC; ++e) {
-          float left = __shfl_up_sync(0xffffffffu, __uint_as_float(p0[e]), 1);
-          float right = __shfl_down_sync(0xffffffffu, __uint_as_float(p2[e]), 1);
-          left = first ? (has_prev ? __uint_as_float(xp[e]) : 0.f) : left;
-          right = last ? (has_next ? __uint_as_float(xn[e]) : 0.f) : right;
+          const float left = __shfl_up_sync(0xffffffffu, __uint_as_float(p0[e]), 1);
+          const float right = __shfl_down_sync(0xffffffffu, __uint_as_float(p2[e]), 1);
           float v = __fadd_rn(__fadd_rn(left, __uint_as_float(p1[e])), right);
           v = relu ? fmaxf(v, 0.f) : __fadd_rn(v, 0.f);
           if (store && e < cmax) *ptr = v;
           ptr += co_stride;
         }
-        par ^= 1;
       }
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
@@ -534,6 +517,8 @@ bool conv_s1_eligible(const ConvParams& p, const void* a) {
   if (e && e[0] == '0') return false;
   return p.KW == 3 && p.dx == 1 && p.ox == -1 && p.sx == 1 && p.sy == 1 && p.Wo == p.W && !p.in_bf16 &&
          p.n_tiles_n == 1 && 3 * p.BN <= 240 && p.BN % 16 == 0 && slots_log2_for(p.W) > 0 && p.W % 4 == 0 &&
+         // row segments of at most 30 output columns (32 lanes with both halo columns)
+         (p.W + (1 << (slots_log2_for(p.W) - 5)) - 1) >> (slots_log2_for(p.W) - 5) <= 30 &&
          (reinterpret_cast<uintptr_t>(a) % 16) == 0 && tensor_map_encoder() != nullptr;
 }
 
@@ -545,6 +530,8 @@ merit_status launch_conv_s1(const merit_plan& plan, const void* a, const void* p
   A.wpk = static_cast<const uint8_t*>(packed_b);
   A.out = static_cast<float*>(out);
   A.slots_log2 = slots_log2_for(p.W);
+  A.segs_log2 = A.slots_log2 - 5;
+  A.seg_w = (p.W + (1 << A.segs_log2) - 1) >> A.segs_log2;
   A.rows = 128 >> A.slots_log2;
   A.tiles_per_img = (p.Ho + A.rows - 1) / A.rows;
   A.n_tiles = p.N * A.tiles_per_img;
