@@ -384,6 +384,15 @@ conv_tma_kernel(const __grid_constant__ CUtensorMap in_map, const __grid_constan
       const int y0 = (mt - n * A.tiles_per_img) * 4;
       twait(tfull(acc), acc_phase, w1, pon);
       tc_fence_after();
+#ifdef MERIT_DEV_DEBUG
+      if (A.debug & 1024) {  // timing experiment: release the accumulator unread (no output)
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) to_leader(tempty(acc));
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        continue;
+      }
+#endif
       const uint32_t t_row = tmem_base + acc * BN + (static_cast<uint32_t>(qd * 32) << 16);
       for (int c0 = 0; c0 < BN; c0 += 32) {
         uint32_t rr[32];
