@@ -194,6 +194,9 @@ conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
       int st = 0;
       uint32_t ph = 0;
       for (int u = blockIdx.x; u < A.n_units; u += gridDim.x) {
+#ifdef MERIT_DEV_DEBUG
+        if (A.debug & 8192) break;  // no raw rows in the A-release experiment
+#endif
         int tile, half;
         unit_of(u, tile, half);
         const int n = tile / A.tiles_per_img;
@@ -232,6 +235,15 @@ conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
     uint32_t rph = 0, aph = 0;
     for (int u = blockIdx.x; u < A.n_units; u += gridDim.x) {
       for (int g = 0; g < A.n_groups; ++g) {
+#ifdef MERIT_DEV_DEBUG
+        if (A.debug & 8192) {  // timing experiment: A slots released without raw rows or repack (wrong values)
+          twait_s1(a_empty(as), aph ^ 1, w2, pon);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(a_full(as));
+          if (++as == A.na) { as = 0; aph ^= 1; }
+          continue;
+        }
+#endif
         twait_s1(r_full(rs), rph, w1, pon);
         float v[32];
         const uint32_t src = rring + rs * A.raw_bytes + lane_off;
