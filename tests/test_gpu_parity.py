@@ -276,7 +276,9 @@ def test_conv_variants_fp32(cuda, n, cin, h, wd, cout, k, s, pad, dil, relu):
     (2, 64, 28, 28, 80, True),     # Cout = 80 -> N = 240, relu
     (1, 128, 13, 12, 48, False),   # two channel blocks, 32 slots (4 rows / tile), Ho % 4 != 0
     (3, 32, 30, 28, 32, False),    # 32 slots
-    (1, 16, 9, 124, 16, False),    # 128 slots, 1 row / tile
+    (1, 16, 9, 124, 16, False),    # 128 slots: segments of 31 > 30 columns -> general kernel
+    (1, 16, 9, 120, 16, False),    # 128 slots, 1 row / tile: four segments of 30 columns
+    (1, 32, 6, 60, 32, False),     # 64 slots: two segments of 30 columns
 ])
 def test_conv_fp32_stride1_tap_stacked(cuda, monkeypatch, variant, n, cin, h, wd, cout, relu):
     if variant == "no_s1":
@@ -285,6 +287,9 @@ def test_conv_fp32_stride1_tap_stacked(cuda, monkeypatch, variant, n, cin, h, wd
     w.src_a = W.gen_uniform([n, cin, h, wd], 41)
     w.src_b = W.gen_normal([cout, cin, 3, 3], 42, (2.0 / (cin * 9)) ** 0.5)
     got = run_full(w)
+    kern = (_capi.load().merit_dev_last_kernel() or b"").decode()
+    if variant == "s1":  # K3d takes every shape whose row segments fit 30 columns
+        assert ("conv_s1" in kern) == (wd != 124), kern
     assert rel_err(got, O.conv2d(w.src_a, w.src_b, 1, 1, 1, relu)) <= TOL_F32
 
 
