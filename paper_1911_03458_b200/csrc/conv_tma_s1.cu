@@ -106,8 +106,7 @@ conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
   const uint32_t aring = base;                          // na x a_slot
   const uint32_t bring = aring + A.na * A.a_slot;       // nb x b_slot
   const uint32_t rring = bring + A.nb * A.b_slot + 128;  // nr x raw_bytes after a 128-B zero pad
-  const uint32_t xring = rring + A.nr * A.raw_bytes;    // epilogue edge exchange
-  const uint32_t bars = xring + 2 * 2 * 4 * 16 * 4;  // [set][parity][warp][8 P0 | 8 P2]
+  const uint32_t bars = rring + A.nr * A.raw_bytes;
   auto r_full = [&](int s) { return bars + 8u * s; };
   auto r_empty = [&](int s) { return bars + 8u * (kMaxRing + s); };
   auto a_full = [&](int s) { return bars + 8u * (2 * kMaxRing + s); };
@@ -169,7 +168,6 @@ conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
       half = (u - A.n_full) & (A.parts - 1);
     }
   };
-  const int slots_mask = (1 << A.slots_log2) - 1;
   // Segmented slot layout: TMEM lane quadrant q (A rows 32q .. 32q + 31) is
   // segment sg = q % S of output row r = q / S (S = slots / 32): lane l holds
   // input column x = sg * seg_w - 1 + l, so lanes 1 .. seg_w produce outputs
@@ -182,7 +180,6 @@ conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
     const int r = q >> A.segs_log2, sg = q & ((1 << A.segs_log2) - 1);
     return (r << A.slots_log2) + sg * A.seg_w - 1 + l;
   };
-  (void)slots_mask;
   const bool pon = (A.debug & 64) && lane == 0 && warp < 16;
   unsigned long long w1 = 0, w2 = 0, w3 = 0;
   const unsigned long long t_start = clock64();
@@ -224,12 +221,9 @@ conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
     // 16 lo columns.
     const int w = warp;
     const int q = w & 3, h = w >> 2;
-    const int m = 32 * q + lane;
-    // raw [c][128 slots]: A row m is slot m, i.e. raw word m - 1 (the
-    // zero-filled column x = slots - 1 of the previous row, or the pad, for
-    // x = -1); channel stride 512 B, an immediate
+    // raw [c][128 slots]: A row 32q + lane reads the raw word of its segment
+    // column (seg_word); channel stride 512 B, an immediate
     const uint32_t lane_off = static_cast<uint32_t>(seg_word(q, lane)) * 4u;
-    (void)m;
     const uint32_t t_lane = tmem_base + (static_cast<uint32_t>(32 * q) << 16) + kTmemA + 16u * h;
     int rs = h, as = 0;
     uint32_t rph = 0, aph = 0;
@@ -556,7 +550,7 @@ merit_status launch_conv_s1(const merit_plan& plan, const void* a, const void* p
   A.a_slot = tmema ? 0u : nsp * kAPlane;  // TMEM-resident A: no shared-memory ring
   A.b_plane = static_cast<uint32_t>(p.BN) * 128u;
   A.b_slot = 3u * nsp * A.b_plane;
-  const size_t fixed = 1024 + 128 + 2 * 2 * 4 * 16 * 4 + 8 * (6 * kMaxRing + 4) + 16;
+  const size_t fixed = 1024 + 128 + 8 * (6 * kMaxRing + 4) + 16;
   const size_t budget = 227 * 1024 - fixed;
   A.na = 2;
   A.nb = 2;
