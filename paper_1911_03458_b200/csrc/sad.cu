@@ -922,32 +922,59 @@ __device__ __forceinline__ void sad_tile_work_fused(const SadLaunch& L, int32_t*
     if (lane == 0) best2 = min(best2, s2 * kmul + 4 * c);
   }
   if (by >= L.by1) return;
-  // 8x8 records: 4 warps (h) x 16 lanes per block
-  auto fold = [&](uint32_t key, int slot, int32_t* a, int ishift) {
-    atomicMin(&keys[slot], key);
-    __threadfence_block();
-    if (atomicAdd(&cnt[slot], 1u) == 3u) {
-      __threadfence_block();
-      const uint32_t fin = atomicExch(&keys[slot], 0xffffffffu);
-      cnt[slot] = 0u;
-      const int k = static_cast<int>(fin & 0xffffu) >> ishift;
-      const int dy = k / WX, dx = k - (k / WX) * WX;
-      a[0] = dy + p.oy - p.cy;
-      a[1] = dx + p.ox - p.cx;
-      a[2] = static_cast<int32_t>(fin >> 16);
-    }
-  };
+  // this warp's partial argmin keys (its dx quarter h) for the tile's 8x8
+  // blocks (half-warp REDUX) and 16x16 block (warp REDUX): plain shared
+  // stores into part[slot][h]; one warp of the CTA combines the four
+  // quarters and writes the records once every warp has finished the tile
+  // (sad_fused_finalize: no shared atomics or fences on this path)
 #pragma unroll
   for (int n = 0; n < NBY; ++n) {
     const uint32_t key = __reduce_min_sync(hmask, best[n]);
-    if (l16 == 0) fold(key, n * L.TBX + ib, aux + (blk_index + n * (long long)p.BX) * 3, 0);
+    if (l16 == 0) keys[(n * L.TBX + ib) * 4 + h] = key;
   }
-  // 16x16 record of block (by / 2, (bx0 + 2 q) / 2)
   const uint32_t key2 = __reduce_min_sync(0xffffffffu, best2);
-  if (lane == 0) {
-    const long long b2 = (pair * p.BY2 + by / 2) * (long long)p.BX2 + (bx0 >> 1) + q;
-    fold(key2, NBY * L.TBX + q, aux + p.aux2_delta + b2 * 3, 2);
+  if (lane == 0) keys[(NBY * L.TBX + q) * 4 + h] = key2;
+  (void)aux;
+  (void)cnt;
+}
+
+// The argmin records of fused tile `tile` from its four dx-quarter partial
+// keys (part[slot][h]), by one warp: lane s takes slot s (8x8 blocks n * TBX
+// + ib, then the 16x16 blocks).  Keys: sad << 16 | index, the 16x16 index
+// scaled by 4 (sad_tile_work_fused).
+__device__ __forceinline__ void sad_fused_finalize(const SadLaunch& L, int32_t* __restrict__ aux, int tile,
+                                                   const uint32_t* part) {
+  constexpr int NBY = 2, WX = 65;
+  const SadParams& p = L.p;
+  const int lane = static_cast<int>(threadIdx.x) & 31;
+  int t2, tx;
+  sad_tile_coords(tile, L.n_full_tiles, L.n_full_x, L.ntx_m, L.ntx_s, t2, tx);
+  const int pair_i = static_cast<int>(fast_div(t2, L.byt_m, L.byt_s));
+  const int by = L.by0 + (t2 - pair_i * L.BYT) * NBY;
+  if (by >= L.by1) return;
+  const long long pair = pair_i;
+  const int bx0 = tx * L.TBX;
+  const int nb = min(L.TBX, p.BX - bx0);
+  const int n8 = NBY * L.TBX;
+  if (lane >= n8 + L.TBX / 2) return;
+  const bool is16 = lane >= n8;
+  const int n = is16 ? 0 : lane / L.TBX;
+  const int ib = is16 ? 2 * (lane - n8) : lane - n * L.TBX;  // 16x16: its left 8x8 column
+  if (ib >= nb) return;
+  const uint32_t* pk = part + lane * 4;
+  const uint32_t fin = min(__vimin3_u32(pk[0], pk[1], pk[2]), pk[3]);
+  const int k = static_cast<int>(fin & 0xffffu) >> (is16 ? 2 : 0);
+  const int dy = k / WX, dx = k - (k / WX) * WX;
+  int32_t* a;
+  if (is16) {
+    const long long b2 = (pair * p.BY2 + by / 2) * (long long)p.BX2 + (bx0 >> 1) + (lane - n8);
+    a = aux + p.aux2_delta + b2 * 3;
+  } else {
+    a = aux + ((pair * p.BY + by + n) * (long long)p.BX + bx0 + ib) * 3;
   }
+  a[0] = dy + p.oy - p.cy;
+  a[1] = dx + p.ox - p.cx;
+  a[2] = static_cast<int32_t>(fin >> 16);
 }
 
 template <int BLK, int D, int NBY, int NT, int WXC, int MODE = 0>
@@ -1046,8 +1073,10 @@ sad_async_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ re
   uint32_t* cur0 = raw0 + raw_words;
   uint32_t* copies0 = cur0 + 2 * cur_words;
   const int nslot = NBY * L.TBX + (MODE == 2 ? L.TBX / 2 : 0);  // fused: + the 16x16 slots
+  // MODE 2: three tiles' partial keys [slot][dx quarter] (tile k at k % 3);
+  // else two tiles' running keys + arrival counters
   uint32_t* keys0 = copies0 + 12 * L.CS;
-  uint32_t* cnt0 = keys0 + 2 * nslot;
+  uint32_t* cnt0 = keys0 + (MODE == 2 ? 12 : 2) * nslot;
   uint32_t* ctr = cnt0 + 2 * nslot;
   const uint32_t bar_tma = (smem_u32(ctr + 2) + 7u) & ~7u;
   const uint32_t bar_full = bar_tma + 16u;
@@ -1084,6 +1113,12 @@ sad_async_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ re
   auto build = [&](int k) {  // this thread's share of tile k's copies
     const int b = k & 1, c = k % 3;
     if (k >= 3) sad_mbar_wait(bar_done + 8u * c, static_cast<uint32_t>((k - 3) / 3) & 1u);  // copies[c] free
+    if constexpr (MODE == 2) {
+      // every warp finished tile k - 3: one warp writes its argmin records
+      // (before building tile k, whose partial keys reuse that buffer)
+      if (k >= 3 && ((k - 3) % nwarps) == (static_cast<int>(threadIdx.x) >> 5))
+        sad_fused_finalize(L, aux, tile_of(k - 3), keys0 + c * 4 * nslot);
+    }
     sad_mbar_wait(bar_tma + 8u * b, static_cast<uint32_t>(k >> 1) & 1u);
     bool built = false;
     if constexpr (MODE == 2) {
@@ -1125,8 +1160,8 @@ sad_async_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ re
           }
         };
     if constexpr (MODE == 2)
-      sad_tile_work_fused(L, aux, tile_of(k), cur0 + b * cur_words, copies0 + c * 4 * L.CS, keys0 + b * nslot,
-                          cnt0 + b * nslot, refill);
+      sad_tile_work_fused(L, aux, tile_of(k), cur0 + b * cur_words, copies0 + c * 4 * L.CS, keys0 + c * 4 * nslot,
+                          cnt0, refill);
     else if constexpr (MODE == 1)
       sad_tile_work_warp<BLK, NBY, WXC>(L, out, aux, tile_of(k), cur0 + b * cur_words, copies0 + c * 4 * L.CS,
                                         keys0 + b * nslot, cnt0 + b * nslot, refill);
@@ -1135,6 +1170,12 @@ sad_async_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ re
                                       keys0 + b * nslot, cnt0 + b * nslot, refill);
     arrive(bar_done + 8u * c);
     if (k + 2 < nk) build(k + 2);
+  }
+  if constexpr (MODE == 2) {  // the records of the last (up to three) tiles
+    __syncthreads();
+    const int w = static_cast<int>(threadIdx.x) >> 5;
+    for (int t = nk > 3 ? nk - 3 : 0; t < nk; ++t)
+      if ((t % nwarps) == w) sad_fused_finalize(L, aux, tile_of(t), keys0 + (t % 3) * 4 * nslot);
   }
 }
 
@@ -1273,7 +1314,7 @@ merit_status launch_sad_t(const SadParams& p, const uint8_t* cur, const uint8_t*
   // barrier-free variant (TMA staging): two staging buffers, three copy buffers
   const size_t nslot_h = static_cast<size_t>(L.nby * L.TBX + (p.fuse2 ? L.TBX / 2 : 0));
   const size_t smem_async = 128 + 1ull * L.raw_buf + 2ull * L.cur_buf +
-                            4ull * (12ull * L.CS + 4ull * nslot_h + 2) + 8 + 64;
+                            4ull * (12ull * L.CS + (p.fuse2 ? 14ull : 4ull) * nslot_h + 2) + 8 + 64;
   const char* ae = getenv("MERIT_SAD_ASYNC");
   const bool use_async = L.tma && (!(ae && ae[0] == '0') || p.fuse2) && smem_async <= smem_cap;
   if (p.fuse2 && !(use_async && L.nby == 2 && L.by0 % 2 == 0 && L.by1 % 2 == 0))
