@@ -29,6 +29,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "common.cuh"
 #include "tmap.cuh"
@@ -766,7 +767,7 @@ template <typename AfterCw>
 __device__ __forceinline__ void sad_tile_work_fused(const SadLaunch& L, int32_t* __restrict__ aux, int tile,
                                                     const uint32_t* curw, const uint32_t* copies, uint32_t* keys,
                                                     uint32_t* cnt, AfterCw after_cw) {
-  constexpr int BLK = 8, NBY = 2, D = 33, WX = 65, WY = 65, BWW = 2, G = 2;
+  constexpr int BLK = 8, NBY = 2, D = 33, WX = 65, WY = 65, BWW = 2;
   constexpr int WW = FusedGeo::WW;  // staged row pitch in words (fixed geometry: the launcher checks L.Ww)
   const SadParams& p = L.p;
   constexpr int cpw = kFusedCPW;  // words per staged current row (fixed geometry)
@@ -781,7 +782,6 @@ __device__ __forceinline__ void sad_tile_work_fused(const SadLaunch& L, int32_t*
   sad_tile_coords(tile, L.n_full_tiles, L.n_full_x, L.ntx_m, L.ntx_s, t2, tx);
   const int pair_i = static_cast<int>(fast_div(t2, L.byt_m, L.byt_s));
   const int by = L.by0 + (t2 - pair_i * L.BYT) * NBY;  // first 8x8 block row of the tile (even)
-  const long long pair = pair_i;
   const int bx0 = tx * L.TBX;
   const int nb = min(L.TBX, p.BX - bx0);  // even (BX = 2 BX2)
   if (2 * q >= nb) {  // warp-uniform
@@ -804,31 +804,29 @@ __device__ __forceinline__ void sad_tile_work_fused(const SadLaunch& L, int32_t*
     for (int n = 0; n < NBY; ++n) ccw[n] = cb[(n * BLK + (l16 >> 1)) * cpw + (l16 & 1)];
   }
   after_cw();
-  const long long blk_index = (pair * p.BY + by) * (long long)p.BX + bx0 + ib;
   const uint32_t kmul = L.key_mul;
   uint32_t best[NBY], best2 = 0xffffffffu;
 #pragma unroll
   for (int n = 0; n < NBY; ++n) best[n] = 0xffffffffu;
   const int col = ib * BLK + dxl;
   const uint32_t one = L.one;
-  // dy groups [0, 33) and [32, 65): both 33 rows, the shared dy = 32 gives
-  // the same key in both (min is idempotent), so the fold below is branch-free
-  constexpr int DY1 = WY - D;
+  // dy groups [0, 33) and [33, 65) as two specialised bodies (C5 37.2 ->
+  // 36.3 ms against one 33-row body run for [0, 33) and [32, 65) with the
+  // duplicated dy = 32, which MERIT_FUSED_ONEBODY keeps for A/B timing)
 #ifndef MERIT_FUSED_HOTX  // timing experiment: run the dy groups MERIT_FUSED_HOTX times (same result)
 #define MERIT_FUSED_HOTX 1
 #endif
-#pragma unroll 1
-  for (int igx = 0; igx < G * MERIT_FUSED_HOTX; ++igx) {
-    const int ig = igx % G;
-    const uint32_t* cp = copies + (col & 3) * L.CS + (col >> 2) + ig * DY1 * WW;
-    uint32_t acc[NBY][D];
+  auto group = [&](auto dg_tag, const int dy0) {
+    constexpr int DG = decltype(dg_tag)::value;
+    const uint32_t* cp = copies + (col & 3) * L.CS + (col >> 2) + dy0 * WW;
+    uint32_t acc[NBY][DG];
 #pragma unroll
     for (int n = 0; n < NBY; ++n)
 #pragma unroll
-      for (int d = 0; d < D; ++d) acc[n][d] = 0;
+      for (int d = 0; d < DG; ++d) acc[n][d] = 0;
     uint32_t bn0 = 0xffffffffu, bn1 = 0xffffffffu, bn2 = 0xffffffffu;
 #pragma unroll
-    for (int r = 0; r < D + NBY * BLK - 1; ++r) {
+    for (int r = 0; r < DG + NBY * BLK - 1; ++r) {
       uint32_t rwv[BWW];
 #pragma unroll
       for (int j = 0; j < BWW; ++j) rwv[j] = cp[j];
@@ -836,7 +834,7 @@ __device__ __forceinline__ void sad_tile_work_fused(const SadLaunch& L, int32_t*
 #pragma unroll
       for (int n = 0; n < NBY; ++n)
 #pragma unroll
-        for (int d = 0; d < D; ++d) {
+        for (int d = 0; d < DG; ++d) {
           const int i = r - d - n * BLK;
           if (i >= 0 && i < BLK) {
 #pragma unroll
@@ -868,7 +866,7 @@ __device__ __forceinline__ void sad_tile_work_fused(const SadLaunch& L, int32_t*
         bn0 = __vimin3_u32(bn0, a0, b0);
         bn1 = __vimin3_u32(bn1, a1, b1);
         bn2 = __vimin3_u32(bn2, a2, b2);
-      } else if (d == D - 1 && (d & 1) == 0) {  // odd D: the last one alone
+      } else if (d == DG - 1 && (d & 1) == 0) {  // odd DG: the last one alone
         uint32_t a0, a1, a2;
         keys(d, a0, a1, a2);
         bn0 = min(bn0, a0);
@@ -876,11 +874,22 @@ __device__ __forceinline__ void sad_tile_work_fused(const SadLaunch& L, int32_t*
         bn2 = min(bn2, a2);
       }
     }
-    const uint32_t k0 = static_cast<uint32_t>(ig * DY1 * WX + dxl);
+    const uint32_t k0 = static_cast<uint32_t>(dy0 * WX + dxl);
     best[0] = min(best[0], bn0 + k0);
     best[1] = min(best[1], bn1 + k0);
     best2 = min(best2, bn2 + 4 * k0);
+  };
+#ifndef MERIT_FUSED_ONEBODY
+#pragma unroll 1
+  for (int rep = 0; rep < MERIT_FUSED_HOTX; ++rep) {
+    group(std::integral_constant<int, D>{}, 0);
+    group(std::integral_constant<int, WY - D>{}, D);
   }
+#else
+  constexpr int DY1 = WY - D;
+#pragma unroll 1
+  for (int igx = 0; igx < 2 * MERIT_FUSED_HOTX; ++igx) group(std::integral_constant<int, D>{}, (igx & 1) * DY1);
+#endif
   // the last column dx = 64 (byte column ib*8 + 64: shifted copy 0): this
   // lane takes dy = 16 h + (lane & 15); block row n reads staged rows dy + 8 n ..
   const int colx = ib * BLK + (WX - 1);
