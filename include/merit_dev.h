@@ -328,7 +328,10 @@ merit_status merit_dev_tiled_traffic(const merit_plan* plan, const int64_t* t_p,
  * range_time_ns is the GPU time spanned by the range (launch gaps included,
  * not a kernel time).  Synchronous; fails with MERIT_E_UNSUPPORTED_PROGRAM
  * when CUPTI (libcupti.so, the copy already in the process if any, else
- * loaded at the first call) or profiling permission is missing. */
+ * loaded at the first call) or profiling permission is missing, or the
+ * profiler refuses the session (e.g. the counters are held by another client
+ * of the GPU); merit_dev_last_error() then starts with
+ * "measure_traffic unavailable on this system: " and names the CUPTI step. */
 typedef struct merit_measured_traffic {
   double dram_read_bytes;
   double dram_write_bytes;

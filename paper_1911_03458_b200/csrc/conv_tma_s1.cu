@@ -122,6 +122,14 @@ conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
   if (threadIdx.x < 32) {  // zero pad read as the x = -1 column of slot 0's first row
     const uint32_t z = rring - 128 + 4u * threadIdx.x;
     asm volatile("st.shared.u32 [%0], %1;" ::"r"(z), "r"(0u) : "memory");
+    // ... and of slot s > 0: the last word of slot s - 1 (channel 31, last
+    // row, column slots - 1 >= W: every box writes a zero there).  On the
+    // first lap that box may still be in flight when slot s is read, and the
+    // word would be whatever the previous kernel left in shared memory.
+    if (static_cast<int>(threadIdx.x) < A.nr) {
+      asm volatile("st.shared.u32 [%0], %1;" ::"r"(rring + (threadIdx.x + 1u) * A.raw_bytes - 4u), "r"(0u) : "memory");
+      fence_proxy_async();
+    }
   }
   if (threadIdx.x == 0) {
     for (int s = 0; s < A.nr; ++s) {

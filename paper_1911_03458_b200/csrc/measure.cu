@@ -135,6 +135,13 @@ constexpr size_t kNumMetrics = 3;
 
 using namespace merit_dev;
 
+// The profiler refused (no CUPTI, no permission, counters held by another
+// client of this GPU, ...): one recognisable message prefix, so callers can
+// tell "this system cannot measure" from a failure of the run itself.
+static merit_status unavailable(const std::string& what) {
+  return fail(MERIT_E_UNSUPPORTED_PROGRAM, "measure_traffic unavailable on this system: " + what);
+}
+
 extern "C" merit_status merit_dev_measure_traffic(const merit_plan* plan, const void* d_a, const void* d_b,
                                                   void* d_out, void* d_aux, void* stream,
                                                   merit_measured_traffic* report) {
@@ -142,7 +149,7 @@ extern "C" merit_status merit_dev_measure_traffic(const merit_plan* plan, const 
   static std::mutex mu;  // one profiling session per process at a time
   std::lock_guard<std::mutex> lk(mu);
   Cupti& c = cupti();
-  if (!c.ok) return fail(MERIT_E_UNSUPPORTED_PROGRAM, "measure_traffic: " + c.why);
+  if (!c.ok) return unavailable(c.why);
   merit_status st = cuda_check(cudaFree(nullptr), "cudaFree(0)");
   if (st != MERIT_OK) return st;
   int dev = 0;
@@ -164,20 +171,20 @@ extern "C" merit_status merit_dev_measure_traffic(const merit_plan* plan, const 
   // host side: config image for the three metrics on this chip
   CUpti_Device_GetChipName_Params cn = {CUpti_Device_GetChipName_Params_STRUCT_SIZE};
   cn.deviceIndex = static_cast<size_t>(dev);
-  if (c.cuptiDeviceGetChipName(&cn) != CUPTI_SUCCESS) return fail(MERIT_E_UNSUPPORTED_PROGRAM, "cuptiDeviceGetChipName");
+  if (c.cuptiDeviceGetChipName(&cn) != CUPTI_SUCCESS) return unavailable("cuptiDeviceGetChipName");
   CUpti_Profiler_GetCounterAvailability_Params ca = {CUpti_Profiler_GetCounterAvailability_Params_STRUCT_SIZE};
   ca.ctx = ctx;
   if (c.cuptiProfilerGetCounterAvailability(&ca) != CUPTI_SUCCESS)
-    return fail(MERIT_E_UNSUPPORTED_PROGRAM, "counter availability (profiling not permitted?)");
+    return unavailable("counter availability (profiling not permitted?)");
   std::vector<uint8_t> avail(ca.counterAvailabilityImageSize);
   ca.pCounterAvailabilityImage = avail.data();
   if (c.cuptiProfilerGetCounterAvailability(&ca) != CUPTI_SUCCESS)
-    return fail(MERIT_E_UNSUPPORTED_PROGRAM, "counter availability image");
+    return unavailable("counter availability image");
   CUpti_Profiler_Host_Initialize_Params hi = {CUpti_Profiler_Host_Initialize_Params_STRUCT_SIZE};
   hi.profilerType = CUPTI_PROFILER_TYPE_RANGE_PROFILER;
   hi.pChipName = cn.pChipName;
   hi.pCounterAvailabilityImage = avail.data();
-  if (c.cuptiProfilerHostInitialize(&hi) != CUPTI_SUCCESS) return fail(MERIT_E_UNSUPPORTED_PROGRAM, "host initialize");
+  if (c.cuptiProfilerHostInitialize(&hi) != CUPTI_SUCCESS) return unavailable("host initialize");
   CUpti_Profiler_Host_Object* host = hi.pHostObject;
   auto host_done = [&] {
     CUpti_Profiler_Host_Deinitialize_Params hd = {CUpti_Profiler_Host_Deinitialize_Params_STRUCT_SIZE};
@@ -193,7 +200,7 @@ extern "C" merit_status merit_dev_measure_traffic(const merit_plan* plan, const 
   cs.pHostObject = host;
   if (c.cuptiProfilerHostConfigAddMetrics(&am) != CUPTI_SUCCESS || c.cuptiProfilerHostGetConfigImageSize(&cs) != CUPTI_SUCCESS) {
     host_done();
-    return fail(MERIT_E_UNSUPPORTED_PROGRAM, "metric configuration");
+    return unavailable("metric configuration");
   }
   std::vector<uint8_t> config(cs.configImageSize);
   CUpti_Profiler_Host_GetConfigImage_Params ci = {CUpti_Profiler_Host_GetConfigImage_Params_STRUCT_SIZE};
@@ -205,7 +212,7 @@ extern "C" merit_status merit_dev_measure_traffic(const merit_plan* plan, const 
   np.pConfigImage = config.data();
   if (c.cuptiProfilerHostGetConfigImage(&ci) != CUPTI_SUCCESS || c.cuptiProfilerHostGetNumOfPasses(&np) != CUPTI_SUCCESS) {
     host_done();
-    return fail(MERIT_E_UNSUPPORTED_PROGRAM, "config image");
+    return unavailable("config image");
   }
 
   // L2 flush: a write pass over twice the L2 evicts the sources a preceding
@@ -230,7 +237,7 @@ extern "C" merit_status merit_dev_measure_traffic(const merit_plan* plan, const 
   en.ctx = ctx;
   if (c.cuptiRangeProfilerEnable(&en) != CUPTI_SUCCESS) {
     host_done();
-    return fail(MERIT_E_UNSUPPORTED_PROGRAM, "range profiler enable (profiling not permitted?)");
+    return unavailable("range profiler enable (profiling not permitted?)");
   }
   CUpti_RangeProfiler_Object* obj = en.pRangeProfilerObject;
   auto target_done = [&] {
@@ -248,7 +255,7 @@ extern "C" merit_status merit_dev_measure_traffic(const merit_plan* plan, const 
   if (c.cuptiRangeProfilerGetCounterDataSize(&ds) != CUPTI_SUCCESS) {
     target_done();
     host_done();
-    return fail(MERIT_E_UNSUPPORTED_PROGRAM, "counter data size");
+    return unavailable("counter data size");
   }
   std::vector<uint8_t> counters(ds.counterDataSize);
   CUpti_RangeProfiler_CounterDataImage_Initialize_Params cdi = {
@@ -275,7 +282,7 @@ extern "C" merit_status merit_dev_measure_traffic(const merit_plan* plan, const 
       c.cuptiRangeProfilerSetConfig(&sc) != CUPTI_SUCCESS) {
     target_done();
     host_done();
-    return fail(MERIT_E_UNSUPPORTED_PROGRAM, "range profiler configuration");
+    return unavailable("range profiler configuration");
   }
   const int64_t l0 = merit_dev_launch_count();
   int npass = 0;
@@ -293,9 +300,12 @@ extern "C" merit_status merit_dev_measure_traffic(const merit_plan* plan, const 
     pr.pRangeName = "merit_dev_run";
     CUpti_RangeProfiler_PopRange_Params po = {CUpti_RangeProfiler_PopRange_Params_STRUCT_SIZE};
     po.pRangeProfilerObject = obj;
-    if (st != MERIT_OK || c.cuptiRangeProfilerStart(&sp) != CUPTI_SUCCESS ||
-        c.cuptiRangeProfilerPushRange(&pr) != CUPTI_SUCCESS) {
-      if (st == MERIT_OK) st = fail(MERIT_E_UNSUPPORTED_PROGRAM, "range profiler start");
+    CUptiResult rc_start = CUPTI_SUCCESS, rc_push = CUPTI_SUCCESS;
+    if (st != MERIT_OK || (rc_start = c.cuptiRangeProfilerStart(&sp)) != CUPTI_SUCCESS ||
+        (rc_push = c.cuptiRangeProfilerPushRange(&pr)) != CUPTI_SUCCESS) {
+      if (st == MERIT_OK)
+        st = unavailable("range profiler start (CUPTI result: start " + std::to_string(int(rc_start)) +
+                                                   ", push " + std::to_string(int(rc_push)) + ")");
       break;
     }
     st = merit_dev_run(plan, d_a, d_b, d_out, d_aux, stream);
@@ -303,11 +313,15 @@ extern "C" merit_status merit_dev_measure_traffic(const merit_plan* plan, const 
     cudaStreamSynchronize(s);
     so = {CUpti_RangeProfiler_Stop_Params_STRUCT_SIZE};
     so.pRangeProfilerObject = obj;
-    const bool stopped = c.cuptiRangeProfilerPopRange(&po) == CUPTI_SUCCESS && c.cuptiRangeProfilerStop(&so) == CUPTI_SUCCESS;
+    const CUptiResult rc_pop = c.cuptiRangeProfilerPopRange(&po);
+    const CUptiResult rc_stop = c.cuptiRangeProfilerStop(&so);
+    const bool stopped = rc_pop == CUPTI_SUCCESS && rc_stop == CUPTI_SUCCESS;
     ++npass;
     if (st != MERIT_OK) break;
     if (!stopped) {
-      st = fail(MERIT_E_UNSUPPORTED_PROGRAM, "range profiler stop");
+      st = unavailable("range profiler stop (CUPTI result: pop " + std::to_string(int(rc_pop)) +
+                                                 ", stop " + std::to_string(int(rc_stop)) + ", pass " +
+                                                 std::to_string(npass) + ")");
       break;
     }
     if (so.isAllPassSubmitted || npass > 64) break;
@@ -315,7 +329,7 @@ extern "C" merit_status merit_dev_measure_traffic(const merit_plan* plan, const 
   CUpti_RangeProfiler_DecodeData_Params dd = {CUpti_RangeProfiler_DecodeData_Params_STRUCT_SIZE};
   dd.pRangeProfilerObject = obj;
   if (st == MERIT_OK && c.cuptiRangeProfilerDecodeData(&dd) != CUPTI_SUCCESS)
-    st = fail(MERIT_E_UNSUPPORTED_PROGRAM, "range profiler decode");
+    st = unavailable("range profiler decode");
   if (st != MERIT_OK) {
     const std::string msg = run_err.empty() ? std::string(merit_dev_last_error()) : run_err;
     target_done();
@@ -328,7 +342,7 @@ extern "C" merit_status merit_dev_measure_traffic(const merit_plan* plan, const 
   if (c.cuptiRangeProfilerGetCounterDataInfo(&gi) != CUPTI_SUCCESS) {
     target_done();
     host_done();
-    return fail(MERIT_E_UNSUPPORTED_PROGRAM, "counter data info");
+    return unavailable("counter data info");
   }
   merit_measured_traffic r{};
   for (size_t i = 0; i < gi.numTotalRanges; ++i) {

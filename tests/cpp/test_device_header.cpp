@@ -127,12 +127,20 @@ int main() {
     fill_random(big.src_b, 4);
     auto [bout, brep] = run_tiled(big, plan, cfg);
     (void)bout;
-    const merit_measured_traffic m = device::measure_traffic(big);
-    const double words = m.dram_read_bytes / 4.0;
-    const bool okm = m.ranges == 1 && words < double(brep.dram_read_words_a) && words >= 0.85 * double(big.src_a.size());
-    std::printf("%s measured DRAM read words %.0f vs reference tiled count %llu (image %zu words)\n", okm ? "PASS" : "FAIL",
-                words, (unsigned long long)brep.dram_read_words_a, big.src_a.size());
-    if (!okm) ++failures;
+    try {
+      const merit_measured_traffic m = device::measure_traffic(big);
+      const double words = m.dram_read_bytes / 4.0;
+      const bool okm = m.ranges == 1 && words < double(brep.dram_read_words_a) && words >= 0.85 * double(big.src_a.size());
+      std::printf("%s measured DRAM read words %.0f vs reference tiled count %llu (image %zu words)\n",
+                  okm ? "PASS" : "FAIL", words, (unsigned long long)brep.dram_read_words_a, big.src_a.size());
+      if (!okm) ++failures;
+    } catch (const Error& e) {
+      // a host that refuses a CUPTI profiling session has nothing to measure
+      // (merit_dev.h: fixed message prefix); anything else is a failure
+      const bool refused = std::string(e.what()).find("measure_traffic unavailable on this system") != std::string::npos;
+      std::printf("%s measured DRAM traffic: %s\n", refused ? "SKIP" : "FAIL", e.what());
+      if (!refused) ++failures;
+    }
     // an invalid plan fails with the reference's error code
     TilingPlan bad{{16, 8}, {5, 4}};
     bool rt = false, dt = false;

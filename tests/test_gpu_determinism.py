@@ -1,0 +1,133 @@
+"""Run-to-run determinism with other kernels in between (GPU).
+
+Every kernel here stages its gather in shared memory through asynchronous
+copies, so a read that is not ordered after the copy that fills it sees
+whatever the PREVIOUS kernel left in that shared memory — a fault that a
+single launch, or the same launch repeated back to back (which finds its own
+bytes there), does not show.  Regression: K3d (conv_s1_kernel) read the x = -1
+halo word of raw slot s from the tail of slot s - 1 before that slot's first
+box had landed (NaN in the x = 0 column of one output row, about one launch in
+three once other kernels ran in between; tools/conv_stress.py).
+
+The launches of all five config kernels are interleaved round robin and every
+output is compared bit for bit with that plan's first one; the first outputs
+are checked against fp64 / oracle references."""
+import numpy as np
+import pytest
+
+from oracle import binding as O
+from paper_1911_03458_b200 import FLAG_ARGMIN, FLAG_NO_MAP, Plan, PlanGroup
+from paper_1911_03458_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+LAPS = 40
+
+
+def _bufs(plan, a, b, cuda):
+    import torch
+    ta = torch.from_numpy(np.ascontiguousarray(a)).to(cuda)
+    tb = torch.from_numpy(np.ascontiguousarray(b)).to(cuda) if b is not None else None
+    out = torch.empty(max(1, int(plan.info.out_bytes)), dtype=torch.uint8, device=cuda)
+    aux = torch.empty(max(1, int(plan.info.aux_elems)), dtype=torch.int32, device=cuda)
+    return ta, tb, out, aux
+
+
+def test_interleaved_kernels_repeat_bit_exact(cuda):
+    import torch
+    cases = {}
+    # K3d: C3 convolution (fp32, 3-term split), 8 images
+    w3 = W.config_workload("C3", scale=4, seed_offset=80)
+    p3 = Plan(w3)
+    cases["C3 conv_s1"] = (p3, *_bufs(p3, w3.src_a, w3.src_b, cuda), True)
+    # K3c: C4 convolution (bf16), 16 images
+    w4 = W.config_workload("C4", scale=16, seed_offset=81)
+    p4 = Plan(w4)
+    cases["C4 conv_tma"] = (p4, *_bufs(p4, w4.src_a, w4.src_b, cuda), True)
+    # K2: C2-geometry SAD map + argmin on a crop, and the fused C5 search
+    cur, ref = W.gen_me_pair(272, 512, 82)
+    w2 = W.me_view(272, 512, 16, 16)
+    w2.src_a, w2.src_b = cur, ref
+    p2 = Plan(w2, FLAG_ARGMIN)
+    cases["C2 sad"] = (p2, *_bufs(p2, cur, ref, cuda), False)
+    ws = [W.me_view(272, 512, b, 32) for b in (16, 8)]
+    p5 = PlanGroup(ws, FLAG_ARGMIN | FLAG_NO_MAP)
+    assert "fused" in p5.description
+    cases["C5 fused sad"] = (p5, *_bufs(p5, cur, ref, cuda), False)
+    # K1: C1 max-pool, 2 images
+    w1 = W.config_workload("C1", scale=4, seed_offset=83)
+    p1 = Plan(w1)
+    cases["C1 maxpool"] = (p1, *_bufs(p1, w1.src_a, np.zeros(1, np.float32), cuda), False)
+
+    for plan, ta, tb, out, aux, pack in cases.values():
+        if pack:
+            plan.pack_b(tb)
+
+    def launch(name):
+        plan, ta, tb, out, aux, pack = cases[name]
+        out.fill_(0xFF)
+        aux.fill_(-1)
+        plan.run(ta, None if pack else tb, out, aux if plan.info.aux_elems else None)
+
+    first = {}
+    for lap in range(LAPS):
+        for name in cases:
+            launch(name)
+            plan, ta, tb, out, aux, pack = cases[name]
+            if lap == 0:
+                first[name] = (out.clone(), aux.clone())
+            else:
+                assert torch.equal(out, first[name][0]), f"{name}: output differs on lap {lap}"
+                assert torch.equal(aux, first[name][1]), f"{name}: argmin records differ on lap {lap}"
+
+    # the first outputs against references
+    got3 = first["C3 conv_s1"][0].view(torch.float32).reshape(p3.out_shape)
+    want3 = torch.nn.functional.conv2d(cases["C3 conv_s1"][1].double(), cases["C3 conv_s1"][2].double(), padding=1)
+    assert float(((got3.double() - want3).abs() / (1 + want3.abs())).max()) <= 1e-4  # nan fails the comparison
+    got4 = first["C4 conv_tma"][0].view(torch.float32).reshape(p4.out_shape)
+    x4 = torch.from_numpy(W.bf16_bits_to_f32(w4.src_a)).to(cuda).double()
+    k4 = torch.from_numpy(W.bf16_bits_to_f32(w4.src_b)).to(cuda).double()
+    want4 = torch.nn.functional.conv2d(x4, k4, stride=2, padding=1)
+    assert float(((got4.double() - want4).abs() / (1 + want4.abs())).max()) <= 1e-4
+    want2 = O.me_sad(cur, ref, 16, 16)
+    got2 = first["C2 sad"][0].view(torch.int32).cpu().numpy().reshape(want2.shape)
+    assert np.array_equal(got2, want2)
+    assert np.array_equal(first["C2 sad"][1].cpu().numpy().reshape(-1, 3), O.me_argmin(want2, 16))
+    rec = first["C5 fused sad"][1].cpu().numpy()
+    for m, b in zip(p5.members, (16, 8)):
+        mv = rec[m["aux_offset"]:m["aux_offset"] + m["info"].aux_elems].reshape(-1, 3)
+        assert np.array_equal(mv, O.me_argmin(O.me_sad(cur, ref, b, 32), 32))
+    got1 = first["C1 maxpool"][0].view(torch.float32).cpu().numpy().reshape(p1.out_shape)
+    assert np.array_equal(got1.view(np.uint32), O.maxpool(w1.src_a, 56, 56).view(np.uint32))
+
+
+def test_c3_full_config_repeats_bit_exact_after_other_kernels(cuda):
+    """The benched C3 launch (32 images, 148 CTAs, ~6 units each) after a SAD
+    launch or a C4 convolution: the case that produced NaNs before the fix."""
+    import torch
+    w = W.config_workload("C3")
+    plan = Plan(w)
+    ta, tb, out, _ = _bufs(plan, w.src_a, w.src_b, cuda)
+    plan.pack_b(tb)
+    want = torch.nn.functional.conv2d(ta.double(), tb.double(), padding=1)
+    ws = W.config_workload("C2")
+    sad = Plan(ws, FLAG_ARGMIN | FLAG_NO_MAP)
+    sa, sb, sout, saux = _bufs(sad, ws.src_a, ws.src_b, cuda)
+    w4 = W.config_workload("C4", scale=16)
+    c4 = Plan(w4)
+    a4, b4, o4, _ = _bufs(c4, w4.src_a, w4.src_b, cuda)
+    c4.pack_b(b4)
+    ref_out = None
+    for i in range(60):
+        if i % 2 == 0:
+            sad.run(sa, sb, None, saux)
+        else:
+            c4.run(a4, None, o4)
+        out.fill_(0xFF)  # NaN bit pattern
+        plan.run(ta, None, out)
+        if ref_out is None:
+            ref_out = out.clone()
+            got = out.view(torch.float32).reshape(plan.out_shape)
+            assert float(((got.double() - want).abs() / (1 + want.abs())).max()) <= 1e-4
+        else:
+            assert torch.equal(out, ref_out), f"C3 output differs on launch {i}"

@@ -9,10 +9,22 @@ import numpy as np
 import pytest
 
 from oracle import binding as O
-from paper_1911_03458_b200 import FLAG_ARGMIN, Plan, run_tiled
+from paper_1911_03458_b200 import FLAG_ARGMIN, Error, Plan, run_tiled
 from paper_1911_03458_b200 import workloads as W
 
 pytestmark = pytest.mark.gpu
+
+UNAVAILABLE = "measure_traffic unavailable on this system"
+
+
+def _skip_if_profiler_refused(e):
+    """Some GPU hosts refuse a CUPTI profiling session (counters held by a
+    monitoring agent, profiling restricted): the library reports that with a
+    fixed message prefix (merit_dev.h), and there is nothing to measure.  Any
+    other failure of the call is a failure of this test."""
+    if UNAVAILABLE in str(e):
+        pytest.skip(str(e))
+    raise e
 
 
 def _measure(cuda, plan, a, b):
@@ -21,7 +33,10 @@ def _measure(cuda, plan, a, b):
     tb = torch.from_numpy(np.ascontiguousarray(b)).to(cuda)
     out = torch.empty(max(1, int(plan.info.out_bytes)), dtype=torch.uint8, device=cuda)
     aux = torch.empty(max(1, int(plan.info.aux_elems)), dtype=torch.int32, device=cuda)
-    return plan.measure_traffic(ta, tb, out, aux if plan.info.aux_elems else None)
+    try:
+        return plan.measure_traffic(ta, tb, out, aux if plan.info.aux_elems else None)
+    except Error as e:
+        _skip_if_profiler_refused(e)
 
 
 @pytest.mark.parametrize("config", ["C1", "C2", "C3", "C4"])
@@ -46,7 +61,10 @@ def test_run_tiled_report_with_measurement(cuda):
     # device reads the image once
     w = W.build_template("conv2d", {"h": 516, "w": 516, "k": 5, "pad": 0})
     W.fill_random(w, 3, 4)
-    out, rep = run_tiled(w, [16, 8], [5, 5], measure=True)
+    try:
+        out, rep = run_tiled(w, [16, 8], [5, 5], measure=True)
+    except Error as e:
+        _skip_if_profiler_refused(e)
     _, ref_traffic = O.ref_run_tiled(w, [16, 8], [5, 5])
     assert int(ref_traffic[0]) == rep["dram_read_words_a"]   # the reference's own count
     m = rep["measured"]
