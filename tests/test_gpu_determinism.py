@@ -9,9 +9,11 @@ halo word of raw slot s from the tail of slot s - 1 before that slot's first
 box had landed (NaN in the x = 0 column of one output row, about one launch in
 three once other kernels ran in between; tools/conv_stress.py).
 
-The launches of all five config kernels are interleaved round robin and every
-output is compared bit for bit with that plan's first one; the first outputs
-are checked against fp64 / oracle references."""
+The launches of all five config kernels are interleaved round robin — once as
+they are, once with every SM's shared memory filled with NaN patterns before
+each launch (tests/cuda/poison.cu; conftest.py also does that at the start of
+every GPU test) — and every output is compared bit for bit with that plan's
+first one; the first outputs are checked against fp64 / oracle references."""
 import numpy as np
 import pytest
 
@@ -33,7 +35,8 @@ def _bufs(plan, a, b, cuda):
     return ta, tb, out, aux
 
 
-def test_interleaved_kernels_repeat_bit_exact(cuda):
+@pytest.mark.parametrize("poison", [False, True], ids=["interleaved", "poisoned"])
+def test_interleaved_kernels_repeat_bit_exact(cuda, smem_poison, poison):
     import torch
     cases = {}
     # K3d: C3 convolution (fp32, 3-term split), 8 images
@@ -63,16 +66,21 @@ def test_interleaved_kernels_repeat_bit_exact(cuda):
         if pack:
             plan.pack_b(tb)
 
-    def launch(name):
+    flush = torch.zeros(256 << 20, dtype=torch.uint8, device=cuda)  # 2 x L2
+
+    def launch(name, lap):
         plan, ta, tb, out, aux, pack = cases[name]
         out.fill_(0xFF)
         aux.fill_(-1)
+        if poison:
+            flush.add_(1)  # cold L2: the staging copies come from DRAM and complete out of order
+            smem_poison(0xFFFFFFFF if lap % 2 else 0x7FC07FC0)
         plan.run(ta, None if pack else tb, out, aux if plan.info.aux_elems else None)
 
     first = {}
     for lap in range(LAPS):
         for name in cases:
-            launch(name)
+            launch(name, lap)
             plan, ta, tb, out, aux, pack = cases[name]
             if lap == 0:
                 first[name] = (out.clone(), aux.clone())
@@ -103,8 +111,10 @@ def test_interleaved_kernels_repeat_bit_exact(cuda):
 
 def test_c3_full_config_repeats_bit_exact_after_other_kernels(cuda):
     """The benched C3 launch (32 images, 148 CTAs, ~6 units each) after a SAD
-    launch or a C4 convolution: the case that produced NaNs before the fix."""
+    launch or a C4 convolution, with a cold L2: the case that produced NaNs
+    before the fix (the pre-fix kernel fails this test within a few launches)."""
     import torch
+    flush = torch.zeros(256 << 20, dtype=torch.uint8, device=cuda)
     w = W.config_workload("C3")
     plan = Plan(w)
     ta, tb, out, _ = _bufs(plan, w.src_a, w.src_b, cuda)
@@ -120,10 +130,11 @@ def test_c3_full_config_repeats_bit_exact_after_other_kernels(cuda):
     ref_out = None
     for i in range(60):
         if i % 2 == 0:
-            sad.run(sa, sb, None, saux)
+            sad.run(sa, sb, sout, saux)
         else:
             c4.run(a4, None, o4)
         out.fill_(0xFF)  # NaN bit pattern
+        flush.add_(1)
         plan.run(ta, None, out)
         if ref_out is None:
             ref_out = out.clone()
