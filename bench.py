@@ -390,11 +390,34 @@ def time_device(case, steps, warmup, soak, stream, lib, barrier, local, graph=Tr
 PER_CONFIG_STEPS = {"C1": 200, "C2": 200, "C3": 200, "C4": 100}
 
 
+def time_e2e(case, steps, warm, sp, barrier=lambda: None):
+    """The host-buffer C-ABI call (merit_dev_run_host: pinned host sources in,
+    host results out, both copies inside the timed region): wall seconds for
+    `steps` calls after `warm` untimed ones."""
+    import torch
+    case.e2e_setup()
+    for _ in range(max(1, warm)):
+        case.e2e_step(sp)
+    torch.cuda.synchronize()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        case.e2e_step(sp)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    barrier()
+    return dt
+
+
+E2E_PATH = "merit_dev_run_host per plan (pinned host buffers in, host results out)"
+
+
 def per_config_entries(args, device, stream, lib, local, peaks, peaks_kind):
     """The other configurations on the same GPU (N = 1 only), device-resident
     inputs, the same timing protocol as the headline (own K, W = 5, clock
     soak, CUDA-graph replay, rotating sets > L2): value, ms/step, the dominant
-    kernel's roofline fraction and the clocks seen."""
+    kernel's roofline fraction and the clocks seen; the host-buffer call
+    (e2e) and a short reference-engine sample on the host cores beside it."""
     import torch
     out = {}
     for c in ("C1", "C2", "C3", "C4"):
@@ -411,6 +434,13 @@ def per_config_entries(args, device, stream, lib, local, peaks, peaks_kind):
                   "roofline": {kk: rf[kk] for kk in ("bound", "achieved", "peak", "unit", "frac", "kernel")
                                if kk in rf},
                   "clocks": clk.summary("timed region + 0.3 s soak")}
+        n_e2e = max(1, min(args.e2e_steps, 10))
+        e2e_s = time_e2e(case, n_e2e, 2, stream.cuda_stream)
+        out[c]["e2e"] = {"value": round(case.outputs_per_step * n_e2e / e2e_s / 1e9, 4), "unit": UNIT,
+                         "h2d_bytes_per_step": int(case.h2d), "d2h_bytes_per_step": int(case.d2h),
+                         "steps": n_e2e, "path": E2E_PATH}
+        if not args.no_cpu_baseline:
+            out[c]["cpu_baseline"] = cpu_baseline(c, budget_s=args.cpu_budget / 3)
         del case
         torch.cuda.synchronize()
         torch.cuda.empty_cache()
@@ -449,18 +479,8 @@ def run_ours(args):
     outputs_all = float(total_per_step.item())
 
     # e2e through the host-buffer C-ABI call
-    case.e2e_setup()
-    for i in range(max(1, min(args.warmup, 3))):
-        case.e2e_step(sp)
-    torch.cuda.synchronize()
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
-    barrier()
-    t0 = time.perf_counter()
-    for i in range(e2e_steps):
-        case.e2e_step(sp)
-    torch.cuda.synchronize()
-    e2e_s = time.perf_counter() - t0
-    barrier()
+    e2e_s = time_e2e(case, e2e_steps, min(args.warmup, 3), sp, barrier)
     te = torch.tensor([e2e_s], dtype=torch.float64, device=device)
     if dist is not None:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
@@ -484,7 +504,7 @@ def run_ours(args):
         "roofline": rf,
         "e2e": {"value": round(outputs_all * e2e_steps / e2e_s / 1e9, 4), "unit": UNIT,
                 "h2d_bytes_per_step": int(case.h2d), "d2h_bytes_per_step": int(case.d2h),
-                "steps": e2e_steps, "path": "merit_dev_run_host per plan (pinned host buffers in, host results out)"},
+                "steps": e2e_steps, "path": E2E_PATH},
         "gpu_launches": int(launches),
         "clocks": clk,
     }
