@@ -29,6 +29,7 @@ def cuda():
 
 
 _POISON = None
+_FLUSH = None
 
 
 def poison_shared_memory(pattern: int = 0xFFFFFFFF) -> None:
@@ -62,6 +63,11 @@ def _poisoned_shared_memory(request):
         import torch
         if torch.cuda.is_available():
             torch.cuda.init()
-            torch.zeros(1, device="cuda")  # primary context current on this thread
+            # primary context current on this thread; the write pass over 2 x L2
+            # also leaves the test's first staging copies to come from DRAM
+            global _FLUSH
+            if _FLUSH is None:
+                _FLUSH = torch.zeros(256 << 20, dtype=torch.uint8, device="cuda")
+            _FLUSH.add_(1)
             poison_shared_memory()
     yield
