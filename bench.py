@@ -625,7 +625,9 @@ def relaunch_distributed(args) -> int:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=None,
+                    help="timed steps (default: 20 for C5; 200 / 200 / 200 / 100 for the microsecond-scale C1-C4, "
+                         "whose K-step CUDA graph would otherwise be shorter than its own launch cost)")
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="C5", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -642,6 +644,8 @@ def main():
     ap.add_argument("--sad-map", default="i32", choices=["i32", "u16"],
                     help="C2: SAD map element type (u16 is exact and halves the map's bytes)")
     args = ap.parse_args()
+    if args.steps is None:
+        args.steps = 20 if args.impl == "reference" else {"C5": 20, **PER_CONFIG_STEPS}[args.config]
     if args.warmup < 3:
         args.warmup = 3  # timing rule: at least 3 warm-up steps
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
