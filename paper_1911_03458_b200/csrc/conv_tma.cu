@@ -36,6 +36,14 @@ using namespace tc;
 constexpr int kRepackWarps = 8;
 constexpr int kRepackers = kRepackWarps * 32;
 constexpr int kWarpB = 8, kWarpMma = 9, kWarpEpi0 = 10, kWarpTma = 14;
+// A-ready signal: every repack thread arrives on a_full itself, right after
+// its own fence.proxy.async (the release pattern of the CUTLASS transform ->
+// MMA pipelines), instead of one elected lane per warp after a __syncwarp.
+// K3d's shared-memory-A variant lost rows with the elected-lane form (DESIGN
+// section 5); 0 = that form, for A/B timing.
+#ifndef MERIT_TMA_ALLARRIVE
+#define MERIT_TMA_ALLARRIVE 1
+#endif
 constexpr int kThreads = 15 * 32;
 constexpr int kMaxRing = 8;
 constexpr uint32_t kPlane = kAPlane;           // 16 KB
@@ -164,7 +172,11 @@ conv_tma_kernel(const __grid_constant__ CUtensorMap in_map, const __grid_constan
       mbar_init(r_empty(s), kRepackers / 2);  // one half of the repack warps
     }
     for (int s = 0; s < A.na; ++s) {
+#if MERIT_TMA_ALLARRIVE
+      mbar_init(a_full(s), kRepackers * kSplit);  // every repack thread, after its own proxy fence
+#else
       mbar_init(a_full(s), kRepackWarps * kSplit);  // one elected lane per repack warp
+#endif
       mbar_init(a_empty(s), 1);
     }
     for (int s = 0; s < A.nb; ++s) {
@@ -284,8 +296,12 @@ conv_tma_kernel(const __grid_constant__ CUtensorMap in_map, const __grid_constan
                        __byte_perm(wv[4], wv[5], 0x7632), __byte_perm(wv[6], wv[7], 0x7632));
         }
         fence_proxy_async();
+#if MERIT_TMA_ALLARRIVE
+        to_leader(a_full(as));
+#else
         __syncwarp();
         if (l == 0) to_leader(a_full(as));
+#endif
         if (++as == A.na) { as = 0; aph ^= 1; }
       }
     }

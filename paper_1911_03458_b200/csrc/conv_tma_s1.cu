@@ -39,6 +39,13 @@ using namespace tc;
 constexpr int kRepackWarps = 8;
 constexpr int kRepackers = kRepackWarps * 32;
 constexpr int kWarpB = 8, kWarpMma = 9, kWarpEpi0 = 10, kWarpTma = 14, kWarpEpi1 = 15;
+// Shared-memory-A variant: every repack thread arrives on a_full itself after
+// its own fence.proxy.async.  With one elected lane per warp (after a
+// __syncwarp) the N = 240 shape read stale A rows 96..127 on a CTA's first
+// tile; 0 = that form, for diagnosis.
+#ifndef MERIT_S1_ALLARRIVE
+#define MERIT_S1_ALLARRIVE 1
+#endif
 constexpr int kThreads = 19 * 32;
 constexpr int kEpiWarps = 8;  // two sets of four (one warp per TMEM lane quadrant each)
 constexpr int kEC = 8;        // output channels per epilogue chunk
@@ -137,7 +144,13 @@ conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
       mbar_init(r_empty(s), kRepackers / 2);  // one half of the repack warps
     }
     for (int s = 0; s < A.na; ++s) {
+#if MERIT_S1_ALLARRIVE
+      // shared-memory A: every repack thread arrives after its own proxy fence;
+      // TMEM A: one elected lane per warp after tcgen05.wait::st + __syncwarp
+      mbar_init(a_full(s), TMEMA ? kRepackWarps : kRepackers);
+#else
       mbar_init(a_full(s), kRepackWarps);  // one elected lane per repack warp
+#endif
       mbar_init(a_empty(s), 1);
     }
     for (int s = 0; s < A.nb; ++s) {
@@ -310,8 +323,12 @@ conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
           if (SPLIT3) st_shared_v4(phi + kAPlane + off, lo[0], lo[1], lo[2], lo[3]);
         }
         fence_proxy_async();
+#if MERIT_S1_ALLARRIVE
+        mbar_arrive(a_full(as));
+#else
         __syncwarp();
         if (lane == 0) mbar_arrive(a_full(as));
+#endif
         if (++as == A.na) { as = 0; aph ^= 1; }
       }
     }
@@ -515,6 +532,12 @@ conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
   }
 }
 
+// MERIT_S1_N240=1 re-admits N = 240 (diagnosis of the open fault only)
+int s1_max_n() {
+  const char* e = getenv("MERIT_S1_N240");
+  return (e && e[0] == '1') ? 240 : 192;
+}
+
 int slots_log2_for(int W) {
   for (int l = 5; l <= 7; ++l)
     if (W + 2 <= (1 << l)) return l;
@@ -535,7 +558,7 @@ bool conv_s1_eligible(const ConvParams& p, const void* a) {
          // one wrong output row (A rows 96..127) of a CTA's first tile in 2-5% of CTA
          // starts (tools/conv_sweep.py seed 7; not reproduced at N = 192), so Cout 65..80
          // goes to the general 3-wide kernels and that variant stays behind MERIT_S1_TMEMA=0
-         p.n_tiles_n == 1 && 3 * p.BN <= 192 && p.BN % 16 == 0 && slots_log2_for(p.W) > 0 && p.W % 4 == 0 &&
+         p.n_tiles_n == 1 && 3 * p.BN <= s1_max_n() && p.BN % 16 == 0 && slots_log2_for(p.W) > 0 && p.W % 4 == 0 &&
          // row segments of at most 30 output columns (32 lanes with both halo columns)
          (p.W + (1 << (slots_log2_for(p.W) - 5)) - 1) >> (slots_log2_for(p.W) - 5) <= 30 &&
          (reinterpret_cast<uintptr_t>(a) % 16) == 0 && tensor_map_encoder() != nullptr;

@@ -21,9 +21,19 @@ else:
     w.src_a, w.src_b = x, wt
     xr, wr = x, wt
 want = O.conv2d(xr, wr, s, pad, 1, bool(relu))
+poison = None
+import os
+if os.environ.get("CONV_CASE_POISON"):  # NaN-fill every SM's shared memory before each run (tests/cuda/poison.cu)
+    import ctypes
+    sys.path.insert(0, "tests/cuda")
+    import build_helpers
+    poison = ctypes.CDLL(str(build_helpers.build()))
+    poison.poison_shared_memory.argtypes = [ctypes.c_uint32, ctypes.c_void_p]
 for i in range(reps):
+    if poison is not None:
+        assert poison.poison_shared_memory(0xFFFFFFFF, None) == 0
     got = run_full(w)
     e = np.abs(got - want) / (1 + np.abs(want))
     bad = np.argwhere(~(e <= 1e-4))
     kern = (_capi.load().merit_dev_last_kernel() or b"").decode()
-    print(f"err {float(np.nanmax(e)):.3e} bad {len(bad)} first {bad[:3].tolist()} last {bad[-2:].tolist()} | {kern}")
+    print(f"err {float(np.nanmax(e)):.3e} nan {int(np.isnan(got).sum())} bad {len(bad)} first {bad[:3].tolist()} last {bad[-2:].tolist()} | {kern}")
