@@ -38,11 +38,13 @@ constexpr int kRepackers = kRepackWarps * 32;
 constexpr int kWarpB = 8, kWarpMma = 9, kWarpEpi0 = 10, kWarpTma = 14;
 // A-ready signal: every repack thread arrives on a_full itself, right after
 // its own fence.proxy.async (the release pattern of the CUTLASS transform ->
-// MMA pipelines), instead of one elected lane per warp after a __syncwarp.
-// K3d's shared-memory-A variant lost rows with the elected-lane form (DESIGN
-// section 5); 0 = that form, for A/B timing.
+// MMA pipelines), instead of one elected lane per warp after a __syncwarp
+// (time-neutral at C4); 0 = that form, for A/B timing.
 #ifndef MERIT_TMA_ALLARRIVE
 #define MERIT_TMA_ALLARRIVE 1
+#endif
+#ifndef MERIT_RAW_RELEASE_FENCE
+#define MERIT_RAW_RELEASE_FENCE 1
 #endif
 constexpr int kThreads = 15 * 32;
 constexpr int kMaxRing = 8;
@@ -280,6 +282,11 @@ conv_tma_kernel(const __grid_constant__ CUtensorMap in_map, const __grid_constan
               asm volatile("ld.shared.u32 %0, [%1];" : "=r"(t) : "r"(src + (c * 4u + k) * rowbytes));
             v[k][c] = t;
           }
+        // the loads above must have RETURNED before the slot is handed back
+        // (the arrive alone does not wait for them: conv_tma_s1.cu raw_release)
+#if MERIT_RAW_RELEASE_FENCE
+        __threadfence_block();
+#endif
         mbar_arrive(r_empty(rs));
         rs += 2;
         while (rs >= A.nr) { rs -= A.nr; rph ^= 1; }

@@ -1,6 +1,6 @@
 // K3d — stride-1, 3-wide convolution with the three horizontal taps stacked
 // along the MMA's N dimension (the C3 shape: NCHW fp32, 3x3, stride 1, pad 1,
-// Cout <= 64).
+// Cout <= 80).
 //
 // For a fixed kernel row ky and channel block, the tap-kx partial sums
 //   P_kx[x][co] = sum_ci in[ci][y + ky - 1][x] * w[co][ci][ky][kx]
@@ -40,9 +40,8 @@ constexpr int kRepackWarps = 8;
 constexpr int kRepackers = kRepackWarps * 32;
 constexpr int kWarpB = 8, kWarpMma = 9, kWarpEpi0 = 10, kWarpTma = 14, kWarpEpi1 = 15;
 // Shared-memory-A variant: every repack thread arrives on a_full itself after
-// its own fence.proxy.async.  With one elected lane per warp (after a
-// __syncwarp) the N = 240 shape read stale A rows 96..127 on a CTA's first
-// tile; 0 = that form, for diagnosis.
+// its own fence.proxy.async (the CUTLASS transform -> MMA form); 0 = one
+// elected lane per warp after a __syncwarp (A/B).
 #ifndef MERIT_S1_ALLARRIVE
 #define MERIT_S1_ALLARRIVE 1
 #endif
@@ -84,6 +83,25 @@ __device__ __forceinline__ void tma_load_4d_s1(uint32_t dst, const CUtensorMap* 
       "[%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(c), "r"(n), "r"(bar)
       : "memory");
+}
+
+// Hand a raw slot back to the TMA warp.  The slot's values were only REQUESTED
+// by the ld.shared instructions before this point: the arrive does not wait
+// for them (no register dependence; the SASS shows no scoreboard wait before
+// SYNCS.ARRIVE), and with the shared-memory pipe saturated by the tensor
+// core's operand reads the last loads were still queued when the next box
+// landed in the slot (the N = 240 fault: rows loaded last
+// came from the next group).  A CTA-scope fence first: it completes only when
+// this thread's prior loads have returned.  MERIT_RAW_RELEASE_FENCE=0: the
+// bare arrive (diagnosis).
+#ifndef MERIT_RAW_RELEASE_FENCE
+#define MERIT_RAW_RELEASE_FENCE 1
+#endif
+__device__ __forceinline__ void raw_release(uint32_t bar) {
+#if MERIT_RAW_RELEASE_FENCE
+  __threadfence_block();
+#endif
+  mbar_arrive(bar);
 }
 
 __device__ __forceinline__ void twait_s1(uint32_t bar, uint32_t par, unsigned long long& acc, bool on) {
@@ -265,7 +283,7 @@ conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
         const float* sp = reinterpret_cast<const float*>(smem_raw + (src - smem_u32(smem_raw)));
 #pragma unroll
         for (int c = 0; c < 32; ++c) v[c] = sp[c * 128];
-        mbar_arrive(r_empty(rs));
+        raw_release(r_empty(rs));
         rs += 2;
         while (rs >= A.nr) { rs -= A.nr; rph ^= 1; }
         uint32_t hi[16], lo[16];
@@ -307,7 +325,7 @@ conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
 #pragma unroll
           for (int c = 0; c < 8; ++c) v[j][c] = sp[c * 128];
         }
-        mbar_arrive(r_empty(rs));
+        raw_release(r_empty(rs));
         rs += 2;
         while (rs >= A.nr) { rs -= A.nr; rph ^= 1; }
         twait_s1(a_empty(as), aph ^ 1, w2, pon);
@@ -532,10 +550,12 @@ conv_s1_kernel(const __grid_constant__ CUtensorMap in_map, S1Args A) {
   }
 }
 
-// MERIT_S1_N240=1 re-admits N = 240 (diagnosis of the open fault only)
+// N = 3 BN <= 240: Cout <= 64 runs with A in TMEM (N <= 192), Cout 65..80 with
+// A in shared memory.  MERIT_S1_N240=0 sends the latter to the general 3-wide
+// kernels (where they ran while the raw-slot release fault was open).
 int s1_max_n() {
   const char* e = getenv("MERIT_S1_N240");
-  return (e && e[0] == '1') ? 240 : 192;
+  return (e && e[0] == '0') ? 192 : 240;
 }
 
 int slots_log2_for(int W) {
@@ -553,11 +573,6 @@ bool conv_s1_eligible(const ConvParams& p, const void* a) {
   const char* e = getenv("MERIT_CONV_S1");
   if (e && e[0] == '0') return false;
   return p.KW == 3 && p.dx == 1 && p.ox == -1 && p.sx == 1 && p.sy == 1 && p.Wo == p.W && !p.in_bf16 &&
-         // N = 3 BN <= 192: the TMEM-resident-A kernel.  The shared-memory-A variant took
-         // BN = 80 (N = 240) until round 2: with two or more channel blocks it returned
-         // one wrong output row (A rows 96..127) of a CTA's first tile in 2-5% of CTA
-         // starts (tools/conv_sweep.py seed 7; not reproduced at N = 192), so Cout 65..80
-         // goes to the general 3-wide kernels and that variant stays behind MERIT_S1_TMEMA=0
          p.n_tiles_n == 1 && 3 * p.BN <= s1_max_n() && p.BN % 16 == 0 && slots_log2_for(p.W) > 0 && p.W % 4 == 0 &&
          // row segments of at most 30 output columns (32 lanes with both halo columns)
          (p.W + (1 << (slots_log2_for(p.W) - 5)) - 1) >> (slots_log2_for(p.W) - 5) <= 30 &&

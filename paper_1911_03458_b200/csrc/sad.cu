@@ -1158,6 +1158,9 @@ sad_async_kernel(const uint8_t* __restrict__ cur, const uint8_t* __restrict__ re
     sad_mbar_wait(bar_full + 8u * c, static_cast<uint32_t>(k / 3) & 1u);
     auto refill = [&] {
           // the last warp done with cur[b] for tile k refills buffer b with tile k + 2
+          // (every lane's loads of its current rows must have returned first:
+          // they were only requested so far, conv_tma_s1.cu raw_release)
+          __threadfence_block();
           __syncwarp();
           if ((threadIdx.x & 31) == 0) {
             __threadfence_block();

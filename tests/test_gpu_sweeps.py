@@ -5,8 +5,9 @@ sizes, stride 1 / 2, fp32 / bf16, relu) and runs each through six dispatch
 variants against the oracle; tools/misc_sweep.py does the same for max-pool
 views, SAD maps + argmin (single and batched pairs), the fused 16x16 + 8x8
 search and correlation (bit-exact).  Fresh processes matter: the fault these
-sweeps found in round 2 (K3d's shared-memory-A variant) showed on
-the first launch of a process far more often than on later ones."""
+sweeps found in round 2 (a raw slot handed back to the TMA engine before its
+loads had returned) showed on the first launch of a process far
+more often than on later ones."""
 import subprocess
 import sys
 from pathlib import Path
@@ -40,7 +41,8 @@ def test_misc_sweep(cuda, seed):
 @pytest.mark.parametrize("args", ["3 70 37 28 80 3 1 1 0", "3 128 37 28 64 3 1 1 0", "6 70 37 28 16 3 1 0 0"])
 def test_conv_first_launch_of_a_process(cuda, args):
     """The first convolution launch of a fresh process, four times per shape
-    (the Cout = 80 shape failed 7 times in 8 before K3d stopped taking it)."""
+    (the Cout = 80 shape failed 7 times in 8 before the raw-slot release waited
+    for its loads)."""
     for _ in range(4):
         out = _run("conv_case.py", *args.split(), 1)
         assert " bad 0 " in out.strip().splitlines()[-1], out[-500:]
