@@ -19,8 +19,13 @@ pytestmark = pytest.mark.gpu
 
 
 def _run(script, *args):
-    r = subprocess.run([sys.executable, str(ROOT / "tools" / script), *map(str, args)], cwd=ROOT,
-                       capture_output=True, text=True, timeout=900)
+    cmd = [sys.executable, str(ROOT / "tools" / script), *map(str, args)]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
+    if "initialization error" in r.stdout + r.stderr:
+        # the CUDA driver occasionally refuses a context to a process started
+        # right after another one exited (seen once in ~150 starts): not a
+        # result of the kernels under test, so start the process once more
+        r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     return r.stdout
 
